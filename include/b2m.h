@@ -1,0 +1,236 @@
+/*
+ * b2m.h — C ABI of the B200-native particle mover (libb2m.so).
+ *
+ * Drop-in boundary for the reference "minipic" mover path
+ * (/root/reference/proj).  Every entry point names the reference interface it
+ * replaces.  Plain C: pointers, sizes and status codes; no exceptions and no
+ * torch/CUDA types cross it (streams are passed as opaque `void*`).
+ *
+ * Threading: a b2m_ctx is single-owner (engines.hpp:9-11, "an engine is owned
+ * by exactly one worker") but may be driven from any host thread; every call
+ * binds the ctx's device first.
+ *
+ * Errors map one-to-one onto the reference taxonomy (errors.hpp:12-44).  The
+ * message of the most recent failure on the calling thread is returned by
+ * b2m_last_error().  A context that saw a NumericalFault, CflViolation or a
+ * CUDA error is POISONED: every later call returns B2M_ENGINE_FAULT, like the
+ * reference's queue (command_queue.cpp:45-49, :71-72) and Simulation
+ * (runtime.cpp:192, :205-208).
+ */
+#ifndef B2M_H_
+#define B2M_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2M_ABI_VERSION 1
+
+typedef enum b2m_status {
+  B2M_OK = 0,
+  B2M_CONFIG_ERROR = 1,     /* pic::ConfigError     errors.hpp:15-17 */
+  B2M_DOMAIN_ERROR = 2,     /* pic::DomainError     errors.hpp:20-22 */
+  B2M_ALLOC_ERROR = 3,      /* pic::AllocError      errors.hpp:25-27 */
+  B2M_NUMERICAL_FAULT = 4,  /* pic::NumericalFault  errors.hpp:30-32 */
+  B2M_CFL_VIOLATION = 5,    /* pic::CflViolation    errors.hpp:35-37 */
+  B2M_ENGINE_FAULT = 6,     /* pic::EngineFault     errors.hpp:40-42 */
+  B2M_METRIC_ERROR = 7,     /* pic::MetricError     errors.hpp:45-47 */
+  B2M_CUDA_ERROR = 8,       /* device/runtime failure (adapters raise EngineFault) */
+  B2M_INVALID_ARGUMENT = 9  /* null pointer, bad species id, ... */
+} b2m_status;
+
+/* Layout-identical to pic::Grid (grid.hpp:15-41): 64 bytes, offsets nx 0,
+ * ny 4, nz 8, lx 16, ly 24, lz 32, dx 40, dy 48, dz 56. */
+typedef struct b2m_grid {
+  int32_t nx, ny, nz;
+  int32_t pad_;
+  double lx, ly, lz;
+  double dx, dy, dz;
+} b2m_grid;
+
+/* Layout-identical to pic::MoverParams (kernels.hpp:30-39): 32 bytes,
+ * dt 0, qom 8, pc_iterations 16, beta 24.  beta = qom*dt*0.5 is used as given. */
+typedef struct b2m_mover_params {
+  double dt;
+  double qom;
+  int32_t pc_iterations;
+  int32_t pad_;
+  double beta;
+} b2m_mover_params;
+
+/* Arithmetic mode of the mover kernel.
+ *   STRICT: the reference's operation order with every product and sum
+ *           rounded separately and IEEE division -> bit-identical to
+ *           pic::move_batch (kernels.cpp:52-104).
+ *   FAST:   fused multiply-add, per-cell polynomial gather and cell-unit
+ *           predictor; positions/velocities within 1e-12 (vector-relative)
+ *           of the reference, final periodic wrap bit-exact given the
+ *           unwrapped coordinate. */
+typedef enum b2m_mode { B2M_MODE_STRICT = 0, B2M_MODE_FAST = 1 } b2m_mode;
+
+typedef struct b2m_ctx b2m_ctx;
+
+/* ---- library ------------------------------------------------------------ */
+int b2m_abi_version(void);
+const char* b2m_status_name(b2m_status s);
+/* Message of the last failing call on this thread ("" if none). */
+const char* b2m_last_error(void);
+/* Number of visible CUDA devices (0 when none); never fails. */
+int b2m_device_count(void);
+/* Number of kernel launches this process issued through libb2m. */
+uint64_t b2m_launch_count(void);
+
+/* ---- value types (grid.hpp:20-29 Grid::make, kernels.hpp:36-38) ---------- */
+/* ConfigError unless n >= 2 and l > 0 per axis; dx = lx/nx etc. */
+b2m_status b2m_grid_make(int nx, int ny, int nz, double lx, double ly, double lz,
+                         b2m_grid* out);
+/* MoverParams::make: beta = qom*dt*0.5. */
+b2m_status b2m_mover_params_make(double dt, double qom, int pc_iterations,
+                                 b2m_mover_params* out);
+
+/* ---- kernel-level boundary ------------------------------------------------
+ * Replaces  void pic::move_batch(ParticleSpan p, const FieldView& f,
+ *                                const Grid& g, const MoverParams& mp)
+ * (kernels.hpp:49, called at engines.cpp:24 and :97).
+ *
+ * Host pointers in the reference layouts: six SoA arrays of n doubles
+ * (ParticleSpan, particle_batch.hpp:13-21) updated in place, and E/B as
+ * 3 doubles per node, (nx+1)(ny+1)(nz+1) nodes with mirrored seams
+ * (FieldView, field_mesh.hpp:13-16).  Synchronous.  On a non-finite result
+ * returns B2M_NUMERICAL_FAULT with *first_bad = index of the first faulting
+ * particle; particles [0, first_bad) are updated and [first_bad, n) left
+ * untouched, exactly like the reference (kernels.cpp:98-99).
+ * Runs on the current device (device 0 unless b2m_set_device was called). */
+b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp,
+                               const double* E, const double* B, double* x, double* y,
+                               double* z, double* u, double* v, double* w, uint64_t n,
+                               int mode, int64_t* first_bad);
+b2m_status b2m_set_device(int device);
+
+/* ---- engine-level boundary ------------------------------------------------
+ * Replaces pic::Engine (engines.hpp:20-48) + DeviceArena
+ * (device_arena.hpp:23-75) + CommandQueue (command_queue.hpp:17-112): one
+ * context = one GPU's device-resident particle store, field buffers and
+ * stream.  All device memory is allocated here, so capacity errors surface at
+ * creation as B2M_ALLOC_ERROR (device_arena.cpp:20-55), never mid-run. */
+b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species,
+                          const uint64_t* capacity, int mode, b2m_ctx** out);
+b2m_status b2m_ctx_destroy(b2m_ctx* ctx);
+/* Run all work on an external stream (e.g. torch's current stream);
+ * NULL restores the context's own stream. */
+b2m_status b2m_ctx_set_stream(b2m_ctx* ctx, void* cuda_stream);
+b2m_status b2m_ctx_set_mode(b2m_ctx* ctx, int mode);
+
+/* Pin a host range so the copies below run asynchronously (cudaHostRegister). */
+b2m_status b2m_host_register(void* ptr, size_t bytes);
+b2m_status b2m_host_unregister(void* ptr);
+/* Page-locked host allocation (cudaHostAlloc) for staging buffers. */
+b2m_status b2m_host_alloc(size_t bytes, void** out);
+b2m_status b2m_host_free(void* ptr);
+
+/* Field upload (enqueue_field_h2d, engines.cpp:52-60): E/B in FieldView
+ * layout from host memory; the device relayout for the gather is enqueued
+ * behind the copy.  n_nodes must equal (nx+1)(ny+1)(nz+1). */
+b2m_status b2m_field_upload(b2m_ctx* ctx, const double* E, const double* B, uint64_t n_nodes);
+/* Same from device memory (e.g. after an NCCL broadcast). */
+b2m_status b2m_field_upload_device(b2m_ctx* ctx, const double* dE, const double* dB,
+                                   uint64_t n_nodes);
+
+/* Species transfers (enqueue_species_h2d/d2h, engines.cpp:62-93).  host6 =
+ * {x,y,z,u,v,w}.  Upload sets the device count to n (AllocError above
+ * capacity).  Download copies count() particles. */
+b2m_status b2m_species_upload(b2m_ctx* ctx, int s, const double* const* host6, uint64_t n);
+b2m_status b2m_species_download(b2m_ctx* ctx, int s, double* const* host6, uint64_t max_n,
+                                uint64_t* n_out);
+/* Partial transfers for chunked pipelines: [offset, offset+n). */
+b2m_status b2m_species_upload_range(b2m_ctx* ctx, int s, const double* const* host6,
+                                    uint64_t offset, uint64_t n);
+b2m_status b2m_species_download_range(b2m_ctx* ctx, int s, double* const* host6,
+                                      uint64_t offset, uint64_t n);
+b2m_status b2m_species_set_count(b2m_ctx* ctx, int s, uint64_t n);
+b2m_status b2m_species_count(b2m_ctx* ctx, int s, uint64_t* n);
+b2m_status b2m_species_capacity(b2m_ctx* ctx, int s, uint64_t* cap);
+/* Device addresses of the six SoA arrays of species s. */
+b2m_status b2m_species_device_ptrs(b2m_ctx* ctx, int s, double** out6);
+
+/* The mover kernel on device-resident species s (enqueue_kernel,
+ * engines.cpp:95-99).  Asynchronous; a fault is recorded on the device and
+ * reported by b2m_sync. */
+b2m_status b2m_move(b2m_ctx* ctx, int s, const b2m_mover_params* mp);
+/* All species in one launch: mp[n_species]. */
+b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp);
+/* Range variant for chunked pipelines. */
+b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint64_t offset,
+                          uint64_t n);
+
+/* Engine-level mover cycle for HOST-resident batches (the whole
+ * enqueue_species_h2d -> enqueue_kernel -> enqueue_species_d2h schedule of
+ * engines.cpp:62-99 / :157-200 in one call): every species is cut into chunks
+ * of `chunk` particles that flow H2D -> mover -> D2H on three streams, so both
+ * PCIe directions and the kernel overlap.  host6_all[6*s + a] is array a of
+ * species s (page-locked memory for full overlap), counts[s] its size, mp[s]
+ * its parameters.  The field must have been uploaded.  Blocking: on return
+ * the host arrays hold the moved particles; faults as b2m_sync. */
+b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_all,
+                              const uint64_t* counts, const b2m_mover_params* mp,
+                              uint64_t chunk);
+
+/* Optional cell-sort pass for gather locality (north star): stable
+ * reordering of species s by cell index of its current position.  The
+ * particle multiset is unchanged (the reference's own exchange reorders too,
+ * runtime.cpp:64-76). */
+b2m_status b2m_sort_species(b2m_ctx* ctx, int s);
+
+/* Wait for all enqueued work (CommandQueue::synchronize,
+ * command_queue.cpp:45-49).  Returns B2M_NUMERICAL_FAULT with the species and
+ * particle index of the first recorded fault (message text as
+ * kernels.cpp:98-99), B2M_CFL_VIOLATION for an exchange violation, and
+ * poisons the context. */
+b2m_status b2m_sync(b2m_ctx* ctx, int* bad_species, int64_t* first_bad);
+/* Record / measure device time on the context's stream (CUDA events). */
+b2m_status b2m_event_record(b2m_ctx* ctx, int slot);
+b2m_status b2m_event_elapsed_ms(b2m_ctx* ctx, int slot_a, int slot_b, float* ms);
+
+/* ---- partition layer (runtime.cpp:22-76; one context per GPU/rank) -------
+ * y-slab decomposition exactly as pic::decompose / pic::owner_of
+ * (runtime.cpp:22-44).  ConfigError unless world divides ny and slabs have
+ * >= 2 cells. */
+b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world);
+/* owner_of(y) (runtime.cpp:39-44), for host-side checks. */
+int b2m_owner_of(const b2m_grid* g, int world, double y);
+/* Mover fused with the migration scan of partition_outgoing
+ * (runtime.cpp:46-62): particles whose new y belongs to the previous / next
+ * slab are appended to that outbox (48-byte PartRec records
+ * {x,y,z,u,v,w}, runtime.hpp:35-37) and removed; survivors are compacted in
+ * place preserving scan order.  A particle landing in a non-neighbour slab
+ * records a CflViolation.  Asynchronous. */
+b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp);
+/* After b2m_sync: outbox of species s towards dir (0 = prev, 1 = next);
+ * device pointer to count records. */
+b2m_status b2m_outbox(b2m_ctx* ctx, int s, int dir, double** d_recs, uint64_t* count);
+/* Append n received PartRec records (device memory) to species s
+ * (merge_incoming, runtime.cpp:64-76).  AllocError above capacity. */
+b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t n);
+
+/* ---- synthetic GEM input (init.cpp:62-102, rng.hpp:12-56) ----------------
+ * Bit-identical to pic::init_gem for the default GEM parameters
+ * (sim_config.hpp:30-39) on grid g: the 4 species (bg e-, bg i+, sheet e-,
+ * sheet i+) and the Harris B field with E = 0.  Host memory; uses `threads`
+ * host threads (0 = all). */
+b2m_status b2m_gem_counts(const b2m_grid* g, int ppc, uint64_t* counts4);
+b2m_status b2m_gem_species_params(const b2m_grid* g, int ppc, double* qom4, double* qpp4);
+b2m_status b2m_gem_fill_species(const b2m_grid* g, int ppc, uint64_t seed, int s,
+                                double* const* host6, int threads);
+b2m_status b2m_gem_field(const b2m_grid* g, double* E, double* B);
+/* Test/bench field fixture with nonzero E (test_offload.cpp:60-71):
+ * E=(0.01 sin y, 0, 0.02), B=(tanh((y-ly/2)/0.5), 0.05 sin x, 0). */
+b2m_status b2m_gem_like_field(const b2m_grid* g, double* E, double* B);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B2M_H_ */

@@ -1,0 +1,930 @@
+// b2m_capi.cu — the C ABI (include/b2m.h): contexts, transfers, launches,
+// fault surfacing and the y-slab migration steps.
+//
+// Context = the B200 replacement of one offload engine's DeviceArena +
+// CommandQueue (device_arena.cpp:17-111, command_queue.cpp:9-95): device
+// memory is carved up front, work goes to one CUDA stream, faults poison the
+// context.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "b2m_internal.hpp"
+
+namespace b2m {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+b2m_status fail(b2m_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+void note_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n)); }
+
+// Thresholds of the exact floor(v/l) window (see WrapAxis in b2m_mover.cuh):
+// RN(v/l) is monotone in v, so walk from a candidate with nextafter and
+// confirm each side with the host's IEEE division.
+static double last_below(double l, double k, double start) {
+  double v = start;
+  // move up while still below k, then down until below k
+  for (int it = 0; it < 64 && v / l < k; ++it) {
+    const double nv = std::nextafter(v, std::numeric_limits<double>::infinity());
+    if (!(nv / l < k)) break;
+    v = nv;
+  }
+  for (int it = 0; it < 64 && !(v / l < k); ++it) v = std::nextafter(v, -std::numeric_limits<double>::infinity());
+  return v;
+}
+
+static double first_at_least(double l, double k, double start) {
+  double v = start;
+  for (int it = 0; it < 64 && v / l >= k; ++it) {
+    const double nv = std::nextafter(v, -std::numeric_limits<double>::infinity());
+    if (!(nv / l >= k)) break;
+    v = nv;
+  }
+  for (int it = 0; it < 64 && !(v / l >= k); ++it) v = std::nextafter(v, std::numeric_limits<double>::infinity());
+  return v;
+}
+
+WrapAxis make_wrap_axis(double l) {
+  WrapAxis a;
+  a.l = l;
+  a.hi0 = last_below(l, 1.0, l);
+  a.hi1 = last_below(l, 2.0, 2.0 * l);
+  a.lom1 = first_at_least(l, -1.0, -l);
+  return a;
+}
+
+DevGrid to_dev(const b2m_grid& g) {
+  DevGrid d;
+  d.nx = g.nx; d.ny = g.ny; d.nz = g.nz;
+  d.lx = g.lx; d.ly = g.ly; d.lz = g.lz;
+  d.dx = g.dx; d.dy = g.dy; d.dz = g.dz;
+  return d;
+}
+
+FastGrid to_fast(const b2m_grid& g) {
+  FastGrid f;
+  f.nx = g.nx; f.ny = g.ny; f.nz = g.nz;
+  f.nxd = g.nx; f.nyd = g.ny; f.nzd = g.nz;
+  f.rnx = 1.0 / g.nx; f.rny = 1.0 / g.ny; f.rnz = 1.0 / g.nz;
+  f.rdx = 1.0 / g.dx; f.rdy = 1.0 / g.dy; f.rdz = 1.0 / g.dz;
+  f.lx = g.lx; f.ly = g.ly; f.lz = g.lz;
+  f.ax = make_wrap_axis(g.lx);
+  f.ay = make_wrap_axis(g.ly);
+  f.az = make_wrap_axis(g.lz);
+  return f;
+}
+
+}  // namespace b2m
+
+using namespace b2m;
+
+namespace {
+
+constexpr int kEventSlots = 16;
+
+struct Species {
+  double* a[6] = {};
+  uint64_t capacity = 0;
+  uint64_t count = 0;
+  // migration scratch
+  uint8_t* flags = nullptr;
+  uint32_t* blk = nullptr;  // [3][nb] counts + [3][nb] offsets
+  double* out[2] = {};
+  uint64_t cap_out = 0;
+  unsigned long long* holes = nullptr;
+  unsigned long long* totals = nullptr;   // device [3]
+  unsigned long long* totals_h = nullptr; // pinned [3]
+  uint64_t n_out[2] = {0, 0};
+  uint64_t n_holes = 0;
+  uint64_t pre_count = 0;  // count before the last migration step
+  bool migrate_pending = false;
+};
+
+}  // namespace
+
+struct b2m_ctx {
+  int device = 0;
+  b2m_grid grid{};
+  int mode = B2M_MODE_FAST;
+  std::vector<Species> sp;
+  uint64_t n_nodes = 0;
+  double* dE = nullptr;
+  double* dB = nullptr;
+  double2* cells = nullptr;
+  bool field_ready = false;
+  FaultWord* fault = nullptr;
+  FaultWord* fault_h = nullptr;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[kEventSlots] = {};
+  bool poisoned = false;
+  std::string poison_msg;
+  // sort scratch (lazily sized to the largest species)
+  void* sort_temp = nullptr;
+  size_t sort_temp_bytes = 0;
+  uint32_t* keys[2] = {};
+  uint32_t* vals[2] = {};
+  double* scratch = nullptr;
+  uint64_t sort_cap = 0;
+  void* scan_temp = nullptr;
+  size_t scan_temp_bytes = 0;
+  // host pipeline (b2m_run_mover_host)
+  cudaStream_t up = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
+  // slab partition
+  bool slab_on = false;
+  SlabLaunch sl{};
+  std::vector<void*> allocations;
+};
+
+namespace {
+
+b2m_status cuda_fail(b2m_ctx* ctx, cudaError_t e, const char* what) {
+  std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  if (ctx) {
+    ctx->poisoned = true;
+    ctx->poison_msg = msg;
+  }
+  return fail(B2M_CUDA_ERROR, msg);
+}
+
+#define B2M_CUDA(ctx, call)                                   \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call); \
+  } while (0)
+
+b2m_status check_ctx(b2m_ctx* ctx) {
+  if (!ctx) return fail(B2M_INVALID_ARGUMENT, "null context");
+  if (ctx->poisoned)
+    return fail(B2M_ENGINE_FAULT, "device state is invalid after an earlier fault: " + ctx->poison_msg);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  return B2M_OK;
+}
+
+b2m_status check_species(b2m_ctx* ctx, int s) {
+  if (s < 0 || s >= static_cast<int>(ctx->sp.size()))
+    return fail(B2M_INVALID_ARGUMENT, "species id " + std::to_string(s) + " out of range");
+  return B2M_OK;
+}
+
+template <class T>
+b2m_status dalloc(b2m_ctx* ctx, T** p, size_t count, const char* what) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(B2M_ALLOC_ERROR, std::string("device allocation failed for ") + what + " (" +
+                                     std::to_string(count * sizeof(T)) + " bytes): " +
+                                     cudaGetErrorString(e));
+  }
+  ctx->allocations.push_back(*p);
+  return B2M_OK;
+}
+
+SpeciesLaunch make_launch(b2m_ctx* ctx, int s, const b2m_mover_params& mp, uint64_t offset,
+                          uint64_t n) {
+  SpeciesLaunch L{};
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  L.x = S.a[0] + offset; L.y = S.a[1] + offset; L.z = S.a[2] + offset;
+  L.u = S.a[3] + offset; L.v = S.a[4] + offset; L.w = S.a[5] + offset;
+  L.n = n;
+  L.base = offset;
+  L.dt = mp.dt;
+  L.dto2 = 0.5 * mp.dt;
+  L.beta = mp.beta;
+  L.dto2_cell[0] = L.dto2 / ctx->grid.dx;
+  L.dto2_cell[1] = L.dto2 / ctx->grid.dy;
+  L.dto2_cell[2] = L.dto2 / ctx->grid.dz;
+  L.rounds = mp.pc_iterations;
+  L.species = s;
+  return L;
+}
+
+b2m_status check_params(const b2m_mover_params* mp) {
+  if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
+  if (mp->pc_iterations < 1) return fail(B2M_CONFIG_ERROR, "pc_iterations: must be >= 1");
+  return B2M_OK;
+}
+
+b2m_status ensure_sort_scratch(b2m_ctx* ctx, uint64_t n) {
+  if (n <= ctx->sort_cap) return B2M_OK;
+  for (void* p : {static_cast<void*>(ctx->keys[0]), static_cast<void*>(ctx->keys[1]),
+                  static_cast<void*>(ctx->vals[0]), static_cast<void*>(ctx->vals[1]),
+                  static_cast<void*>(ctx->scratch), ctx->sort_temp}) {
+    if (!p) continue;
+    cudaFree(p);
+    ctx->allocations.erase(std::remove(ctx->allocations.begin(), ctx->allocations.end(), p),
+                           ctx->allocations.end());
+  }
+  ctx->sort_cap = 0;
+  b2m_status st;
+  for (int i = 0; i < 2; ++i) {
+    if ((st = dalloc(ctx, &ctx->keys[i], n, "sort keys")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &ctx->vals[i], n, "sort values")) != B2M_OK) return st;
+  }
+  if ((st = dalloc(ctx, &ctx->scratch, n, "sort scratch")) != B2M_OK) return st;
+  ctx->sort_temp_bytes = sort_temp_bytes(n, 32);
+  char* tmp = nullptr;
+  if ((st = dalloc(ctx, &tmp, ctx->sort_temp_bytes, "sort temp")) != B2M_OK) return st;
+  ctx->sort_temp = tmp;
+  ctx->sort_cap = n;
+  return B2M_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int b2m_abi_version(void) { return B2M_ABI_VERSION; }
+
+const char* b2m_status_name(b2m_status s) {
+  switch (s) {
+    case B2M_OK: return "ok";
+    case B2M_CONFIG_ERROR: return "ConfigError";
+    case B2M_DOMAIN_ERROR: return "DomainError";
+    case B2M_ALLOC_ERROR: return "AllocError";
+    case B2M_NUMERICAL_FAULT: return "NumericalFault";
+    case B2M_CFL_VIOLATION: return "CflViolation";
+    case B2M_ENGINE_FAULT: return "EngineFault";
+    case B2M_METRIC_ERROR: return "MetricError";
+    case B2M_CUDA_ERROR: return "CudaError";
+    case B2M_INVALID_ARGUMENT: return "InvalidArgument";
+  }
+  return "unknown";
+}
+
+const char* b2m_last_error(void) { return g_last_error.c_str(); }
+
+int b2m_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+uint64_t b2m_launch_count(void) { return g_launches.load(); }
+
+b2m_status b2m_grid_make(int nx, int ny, int nz, double lx, double ly, double lz,
+                         b2m_grid* out) {
+  if (!out) return fail(B2M_INVALID_ARGUMENT, "null grid");
+  // grid.hpp:20-29
+  if (nx < 2 || ny < 2 || nz < 2) return fail(B2M_CONFIG_ERROR, "grid: nx,ny,nz must each be >= 2");
+  if (!(lx > 0.0) || !(ly > 0.0) || !(lz > 0.0))
+    return fail(B2M_CONFIG_ERROR, "grid: lx,ly,lz must be positive");
+  std::memset(out, 0, sizeof(*out));
+  out->nx = nx; out->ny = ny; out->nz = nz;
+  out->lx = lx; out->ly = ly; out->lz = lz;
+  out->dx = lx / nx; out->dy = ly / ny; out->dz = lz / nz;
+  return B2M_OK;
+}
+
+b2m_status b2m_mover_params_make(double dt, double qom, int pc_iterations,
+                                 b2m_mover_params* out) {
+  if (!out) return fail(B2M_INVALID_ARGUMENT, "null params");
+  std::memset(out, 0, sizeof(*out));
+  out->dt = dt;
+  out->qom = qom;
+  out->pc_iterations = pc_iterations;
+  out->beta = qom * dt * 0.5;  // kernels.hpp:36-38
+  return B2M_OK;
+}
+
+b2m_status b2m_set_device(int device) {
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  return B2M_OK;
+}
+
+b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const uint64_t* capacity,
+                          int mode, b2m_ctx** out) {
+  if (!out || !g || (n_species > 0 && !capacity))
+    return fail(B2M_INVALID_ARGUMENT, "null argument to b2m_ctx_create");
+  *out = nullptr;
+  if (n_species < 0 || n_species > 64) return fail(B2M_CONFIG_ERROR, "n_species out of range");
+  if (mode != B2M_MODE_STRICT && mode != B2M_MODE_FAST)
+    return fail(B2M_CONFIG_ERROR, "mode: unknown mover mode");
+  if (g->nx < 2 || g->ny < 2 || g->nz < 2 || !(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0))
+    return fail(B2M_CONFIG_ERROR, "grid: invalid (use b2m_grid_make)");
+  auto* ctx = new b2m_ctx();
+  ctx->device = device;
+  ctx->grid = *g;
+  ctx->mode = mode;
+  auto bail = [&](b2m_status st) {
+    const std::string msg = g_last_error;
+    b2m_ctx_destroy(ctx);
+    g_last_error = msg;
+    return st;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return fail(B2M_CUDA_ERROR, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  if ((e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking)) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return fail(B2M_CUDA_ERROR, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own;
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  const uint64_t nodes = static_cast<uint64_t>(g->nx + 1) * (g->ny + 1) * (g->nz + 1);
+  const uint64_t ncell = static_cast<uint64_t>(g->nx) * g->ny * g->nz;
+  ctx->n_nodes = nodes;
+  b2m_status st;
+  if ((st = dalloc(ctx, &ctx->dE, 3 * nodes, "field E")) != B2M_OK) return bail(st);
+  if ((st = dalloc(ctx, &ctx->dB, 3 * nodes, "field B")) != B2M_OK) return bail(st);
+  if ((st = dalloc(ctx, &ctx->cells, ncell * (kCellDoubles / 2), "field cells")) != B2M_OK)
+    return bail(st);
+  if ((st = dalloc(ctx, &ctx->fault, 1, "fault word")) != B2M_OK) return bail(st);
+  if (cudaMallocHost(&ctx->fault_h, sizeof(FaultWord)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(B2M_ALLOC_ERROR, "pinned fault word"));
+  }
+  ctx->sp.resize(static_cast<size_t>(n_species));
+  for (int s = 0; s < n_species; ++s) {
+    Species& S = ctx->sp[static_cast<size_t>(s)];
+    S.capacity = capacity[s];
+    for (int a = 0; a < 6; ++a)
+      if ((st = dalloc(ctx, &S.a[a], S.capacity, "species arrays")) != B2M_OK) return bail(st);
+  }
+  launch_fault_reset(ctx->fault, ctx->stream);
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
+    cuda_fail(ctx, e, "context init");
+    return bail(B2M_CUDA_ERROR);
+  }
+  *out = ctx;
+  return B2M_OK;
+}
+
+b2m_status b2m_ctx_destroy(b2m_ctx* ctx) {
+  if (!ctx) return B2M_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->allocations) cudaFree(p);
+  for (Species& S : ctx->sp)
+    if (S.totals_h) cudaFreeHost(S.totals_h);
+  if (ctx->fault_h) cudaFreeHost(ctx->fault_h);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ctx->pipe_ev) cudaEventDestroy(ev);
+  if (ctx->up) cudaStreamDestroy(ctx->up);
+  if (ctx->down) cudaStreamDestroy(ctx->down);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  cudaGetLastError();
+  delete ctx;
+  return B2M_OK;
+}
+
+b2m_status b2m_ctx_set_stream(b2m_ctx* ctx, void* cuda_stream) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
+  return B2M_OK;
+}
+
+b2m_status b2m_ctx_set_mode(b2m_ctx* ctx, int mode) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (mode != B2M_MODE_STRICT && mode != B2M_MODE_FAST)
+    return fail(B2M_CONFIG_ERROR, "mode: unknown mover mode");
+  ctx->mode = mode;
+  return B2M_OK;
+}
+
+b2m_status b2m_host_register(void* ptr, size_t bytes) {
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaHostRegister");
+  return B2M_OK;
+}
+
+b2m_status b2m_host_unregister(void* ptr) {
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaHostUnregister");
+  return B2M_OK;
+}
+
+b2m_status b2m_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(B2M_INVALID_ARGUMENT, "null out");
+  cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(B2M_ALLOC_ERROR, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  }
+  return B2M_OK;
+}
+
+b2m_status b2m_host_free(void* ptr) {
+  cudaError_t e = cudaFreeHost(ptr);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaFreeHost");
+  return B2M_OK;
+}
+
+static b2m_status relayout(b2m_ctx* ctx) {
+  launch_field_to_cells(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB, ctx->cells,
+                        ctx->stream);
+  B2M_CUDA(ctx, cudaGetLastError());
+  ctx->field_ready = true;
+  return B2M_OK;
+}
+
+b2m_status b2m_field_upload(b2m_ctx* ctx, const double* E, const double* B, uint64_t n_nodes) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!E || !B) return fail(B2M_INVALID_ARGUMENT, "null field pointer");
+  if (n_nodes != ctx->n_nodes)
+    return fail(B2M_CONFIG_ERROR, "field: node count " + std::to_string(n_nodes) +
+                                      " does not match the grid (" +
+                                      std::to_string(ctx->n_nodes) + ")");
+  const size_t bytes = 3 * n_nodes * sizeof(double);
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dE, E, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dB, B, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return relayout(ctx);
+}
+
+b2m_status b2m_field_upload_device(b2m_ctx* ctx, const double* dE, const double* dB,
+                                   uint64_t n_nodes) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!dE || !dB) return fail(B2M_INVALID_ARGUMENT, "null field pointer");
+  if (n_nodes != ctx->n_nodes) return fail(B2M_CONFIG_ERROR, "field: node count mismatch");
+  const size_t bytes = 3 * n_nodes * sizeof(double);
+  if (dE != ctx->dE)
+    B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dE, dE, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (dB != ctx->dB)
+    B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dB, dB, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return relayout(ctx);
+}
+
+b2m_status b2m_species_upload_range(b2m_ctx* ctx, int s, const double* const* host6,
+                                    uint64_t offset, uint64_t n) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (offset + n > S.capacity)
+    return fail(B2M_ALLOC_ERROR, "species " + std::to_string(s) + ": " +
+                                     std::to_string(offset + n) + " particles exceed capacity " +
+                                     std::to_string(S.capacity));
+  if (n == 0) return B2M_OK;
+  if (!host6) return fail(B2M_INVALID_ARGUMENT, "null host arrays");
+  for (int a = 0; a < 6; ++a)
+    B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a] + offset, host6[a], n * sizeof(double),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+  return B2M_OK;
+}
+
+b2m_status b2m_species_upload(b2m_ctx* ctx, int s, const double* const* host6, uint64_t n) {
+  b2m_status st = b2m_species_upload_range(ctx, s, host6, 0, n);
+  if (st == B2M_OK) ctx->sp[static_cast<size_t>(s)].count = n;
+  return st;
+}
+
+b2m_status b2m_species_download_range(b2m_ctx* ctx, int s, double* const* host6, uint64_t offset,
+                                      uint64_t n) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (offset + n > S.capacity) return fail(B2M_INVALID_ARGUMENT, "download range beyond capacity");
+  if (n == 0) return B2M_OK;
+  if (!host6) return fail(B2M_INVALID_ARGUMENT, "null host arrays");
+  for (int a = 0; a < 6; ++a)
+    B2M_CUDA(ctx, cudaMemcpyAsync(host6[a], S.a[a] + offset, n * sizeof(double),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  return B2M_OK;
+}
+
+b2m_status b2m_species_download(b2m_ctx* ctx, int s, double* const* host6, uint64_t max_n,
+                                uint64_t* n_out) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  const uint64_t n = ctx->sp[static_cast<size_t>(s)].count;
+  if (n_out) *n_out = n;
+  if (n > max_n)
+    return fail(B2M_ALLOC_ERROR, "download: host arrays hold " + std::to_string(max_n) +
+                                     " particles, species has " + std::to_string(n));
+  return b2m_species_download_range(ctx, s, host6, 0, n);
+}
+
+b2m_status b2m_species_set_count(b2m_ctx* ctx, int s, uint64_t n) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (n > S.capacity) return fail(B2M_ALLOC_ERROR, "particle batch count > capacity");
+  S.count = n;
+  return B2M_OK;
+}
+
+b2m_status b2m_species_count(b2m_ctx* ctx, int s, uint64_t* n) {
+  if (!ctx || !n) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  b2m_status st = check_species(ctx, s);
+  if (st != B2M_OK) return st;
+  *n = ctx->sp[static_cast<size_t>(s)].count;
+  return B2M_OK;
+}
+
+b2m_status b2m_species_capacity(b2m_ctx* ctx, int s, uint64_t* cap) {
+  if (!ctx || !cap) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  b2m_status st = check_species(ctx, s);
+  if (st != B2M_OK) return st;
+  *cap = ctx->sp[static_cast<size_t>(s)].capacity;
+  return B2M_OK;
+}
+
+b2m_status b2m_species_device_ptrs(b2m_ctx* ctx, int s, double** out6) {
+  if (!ctx || !out6) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  b2m_status st = check_species(ctx, s);
+  if (st != B2M_OK) return st;
+  for (int a = 0; a < 6; ++a) out6[a] = ctx->sp[static_cast<size_t>(s)].a[a];
+  return B2M_OK;
+}
+
+b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint64_t offset,
+                          uint64_t n) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  if ((st = check_params(mp)) != B2M_OK) return st;
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (offset + n > S.count) return fail(B2M_INVALID_ARGUMENT, "move range beyond species count");
+  const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
+  if (ctx->mode == B2M_MODE_STRICT)
+    launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
+  else
+    launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream);
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_move(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
+  if (!ctx) return fail(B2M_INVALID_ARGUMENT, "null context");
+  b2m_status st = check_species(ctx, s);
+  if (st != B2M_OK) return st;
+  return b2m_move_range(ctx, s, mp, 0, ctx->sp[static_cast<size_t>(s)].count);
+}
+
+b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
+  const int ns = static_cast<int>(ctx->sp.size());
+  if (ctx->mode == B2M_MODE_STRICT) {
+    for (int s = 0; s < ns; ++s)
+      if ((st = b2m_move(ctx, s, &mp[s])) != B2M_OK) return st;
+    return B2M_OK;
+  }
+  std::vector<SpeciesLaunch> L;
+  for (int s = 0; s < ns; ++s) {
+    if ((st = check_params(&mp[s])) != B2M_OK) return st;
+    L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
+  }
+  launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault, ctx->stream);
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_all,
+                              const uint64_t* counts, const b2m_mover_params* mp, uint64_t chunk) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!host6_all || !counts || !mp) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  if (n_species != static_cast<int>(ctx->sp.size()))
+    return fail(B2M_CONFIG_ERROR, "run_mover: species count does not match the context");
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
+  if (chunk == 0) chunk = 1u << 21;
+  for (int s = 0; s < n_species; ++s) {
+    if ((st = check_params(&mp[s])) != B2M_OK) return st;
+    if (counts[s] > ctx->sp[static_cast<size_t>(s)].capacity)
+      return fail(B2M_ALLOC_ERROR, "species " + std::to_string(s) + ": " +
+                                       std::to_string(counts[s]) + " particles exceed capacity");
+  }
+  if (!ctx->up) {
+    B2M_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
+    B2M_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->down, cudaStreamNonBlocking));
+  }
+  size_t n_chunks = 0;
+  for (int s = 0; s < n_species; ++s) n_chunks += (counts[s] + chunk - 1) / chunk;
+  while (ctx->pipe_ev.size() < 2 * n_chunks + 1) {
+    cudaEvent_t e;
+    B2M_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->pipe_ev.push_back(e);
+  }
+  // uploads start after everything already on the compute stream (field)
+  cudaEvent_t* ev = ctx->pipe_ev.data();
+  B2M_CUDA(ctx, cudaEventRecord(ev[2 * n_chunks], ctx->stream));
+  B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->up, ev[2 * n_chunks], 0));
+  size_t c = 0;
+  for (int s = 0; s < n_species; ++s) {
+    Species& S = ctx->sp[static_cast<size_t>(s)];
+    S.count = counts[s];
+    double* const* h = host6_all + 6 * s;
+    for (uint64_t off = 0; off < counts[s]; off += chunk, ++c) {
+      const uint64_t n = std::min<uint64_t>(chunk, counts[s] - off);
+      for (int a = 0; a < 6; ++a)
+        B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a] + off, h[a] + off, n * sizeof(double),
+                                      cudaMemcpyHostToDevice, ctx->up));
+      B2M_CUDA(ctx, cudaEventRecord(ev[2 * c], ctx->up));
+      B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev[2 * c], 0));
+      const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
+      if (ctx->mode == B2M_MODE_STRICT)
+        launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
+      else
+        launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream);
+      B2M_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], ctx->stream));
+      B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->down, ev[2 * c + 1], 0));
+      for (int a = 0; a < 6; ++a)
+        B2M_CUDA(ctx, cudaMemcpyAsync(h[a] + off, S.a[a] + off, n * sizeof(double),
+                                      cudaMemcpyDeviceToHost, ctx->down));
+    }
+  }
+  B2M_CUDA(ctx, cudaGetLastError());
+  B2M_CUDA(ctx, cudaStreamSynchronize(ctx->down));
+  return b2m_sync(ctx, nullptr, nullptr);
+}
+
+b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  const uint64_t n = S.count;
+  if (n < 2) return B2M_OK;
+  if (n > 0xffffffffull) return fail(B2M_CONFIG_ERROR, "sort: species larger than 2^32");
+  if ((st = ensure_sort_scratch(ctx, n)) != B2M_OK) return st;
+  const uint64_t ncell = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
+  int bits = 1;
+  while ((1ull << bits) <= ncell) ++bits;
+  launch_cell_keys(to_dev(ctx->grid), S.a[0], S.a[1], S.a[2], n, ctx->keys[0], ctx->vals[0],
+                   ctx->stream);
+  launch_sort_pairs(ctx->sort_temp, ctx->sort_temp_bytes, ctx->keys[0], ctx->keys[1],
+                    ctx->vals[0], ctx->vals[1], n, bits, ctx->stream);
+  for (int a = 0; a < 6; ++a) {
+    launch_gather(S.a[a], ctx->vals[1], n, ctx->scratch, ctx->stream);
+    B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a], ctx->scratch, n * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_sync(b2m_ctx* ctx, int* bad_species, int64_t* first_bad) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (bad_species) *bad_species = -1;
+  if (first_bad) *first_bad = -1;
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->fault_h, ctx->fault, sizeof(FaultWord),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const FaultWord f = *ctx->fault_h;
+  if (f.numerical != ~0ull) {
+    const int s = static_cast<int>(f.numerical >> 48);
+    const int64_t i = static_cast<int64_t>(f.numerical & ((1ull << 48) - 1));
+    if (bad_species) *bad_species = s;
+    if (first_bad) *first_bad = i;
+    ctx->poisoned = true;
+    // kernels.cpp:71-72 / :98-99 message text
+    ctx->poison_msg = "mover produced non-finite state at particle index " + std::to_string(i);
+    return fail(B2M_NUMERICAL_FAULT, ctx->poison_msg);
+  }
+  if (f.cfl != ~0ull) {
+    const int s = static_cast<int>(f.cfl >> 48);
+    const int64_t i = static_cast<int64_t>(f.cfl & ((1ull << 48) - 1));
+    if (bad_species) *bad_species = s;
+    if (first_bad) *first_bad = i;
+    double y = 0.0;
+    cudaMemcpy(&y, ctx->sp[static_cast<size_t>(s)].a[1] + i, sizeof(double),
+               cudaMemcpyDeviceToHost);
+    const int dest = b2m_owner_of(&ctx->grid, ctx->sl.world, y);
+    ctx->poisoned = true;
+    // runtime.cpp:55-59 message text
+    ctx->poison_msg = "particle " + std::to_string(i) + " of species " + std::to_string(s) +
+                      " moved from slab " + std::to_string(ctx->sl.rank) +
+                      " to non-neighbor slab " + std::to_string(dest) + " in one step";
+    return fail(B2M_CFL_VIOLATION, ctx->poison_msg);
+  }
+  return B2M_OK;
+}
+
+b2m_status b2m_event_record(b2m_ctx* ctx, int slot) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (slot < 0 || slot >= kEventSlots) return fail(B2M_INVALID_ARGUMENT, "event slot");
+  B2M_CUDA(ctx, cudaEventRecord(ctx->ev[slot], ctx->stream));
+  return B2M_OK;
+}
+
+b2m_status b2m_event_elapsed_ms(b2m_ctx* ctx, int a, int b, float* ms) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (a < 0 || a >= kEventSlots || b < 0 || b >= kEventSlots || !ms)
+    return fail(B2M_INVALID_ARGUMENT, "event slot");
+  B2M_CUDA(ctx, cudaEventSynchronize(ctx->ev[b]));
+  B2M_CUDA(ctx, cudaEventElapsedTime(ms, ctx->ev[a], ctx->ev[b]));
+  return B2M_OK;
+}
+
+// ---- kernel-level one-shot ---------------------------------------------------
+
+b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp, const double* E,
+                               const double* B, double* x, double* y, double* z, double* u,
+                               double* v, double* w, uint64_t n, int mode, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (!g || !mp || !E || !B) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  b2m_status st = check_params(mp);
+  if (st != B2M_OK) return st;
+  if (n == 0) return B2M_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  b2m_ctx* ctx = nullptr;
+  const uint64_t cap = n;
+  if ((st = b2m_ctx_create(dev, g, 1, &cap, mode, &ctx)) != B2M_OK) return st;
+  const uint64_t nodes = static_cast<uint64_t>(g->nx + 1) * (g->ny + 1) * (g->nz + 1);
+  const double* src[6] = {x, y, z, u, v, w};
+  double* dst[6] = {x, y, z, u, v, w};
+  int bad_s = -1;
+  int64_t bad = -1;
+  if ((st = b2m_field_upload(ctx, E, B, nodes)) == B2M_OK &&
+      (st = b2m_species_upload(ctx, 0, src, n)) == B2M_OK &&
+      (st = b2m_move(ctx, 0, mp)) == B2M_OK) {
+    st = b2m_sync(ctx, &bad_s, &bad);
+    if (st == B2M_OK || st == B2M_NUMERICAL_FAULT) {
+      const std::string msg = g_last_error;
+      // reference semantics: [0, bad) updated, [bad, n) untouched
+      const uint64_t keep = st == B2M_OK ? n : static_cast<uint64_t>(bad);
+      ctx->poisoned = false;
+      b2m_status st2 = b2m_species_download_range(ctx, 0, dst, 0, keep);
+      if (st2 == B2M_OK) st2 = b2m_sync(ctx, nullptr, nullptr);
+      if (st == B2M_OK) st = st2;
+      else g_last_error = msg;
+      if (first_bad) *first_bad = bad;
+    }
+  }
+  const std::string msg = g_last_error;
+  b2m_ctx_destroy(ctx);
+  g_last_error = msg;
+  return st;
+}
+
+// ---- partition layer ----------------------------------------------------------
+
+int b2m_owner_of(const b2m_grid* g, int world, double y) {
+  // runtime.cpp:39-44
+  int j = static_cast<int>(y / g->dy);
+  if (j >= g->ny) j = g->ny - 1;
+  if (j < 0) j = 0;
+  return j / (g->ny / world);
+}
+
+b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  // runtime.cpp:22-37 decompose
+  if (world < 1) return fail(B2M_CONFIG_ERROR, "workers: must be >= 1");
+  if (ctx->grid.ny % world != 0)
+    return fail(B2M_CONFIG_ERROR, "workers: " + std::to_string(world) +
+                                      " does not divide ny=" + std::to_string(ctx->grid.ny));
+  const int slab = ctx->grid.ny / world;
+  if (slab < 2)
+    return fail(B2M_CONFIG_ERROR, "workers: slab would be " + std::to_string(slab) +
+                                      " cells; each slab needs at least 2");
+  if (rank < 0 || rank >= world) return fail(B2M_CONFIG_ERROR, "rank out of range");
+  ctx->sl.rank = rank;
+  ctx->sl.world = world;
+  ctx->sl.prev = (rank + world - 1) % world;
+  ctx->sl.next = (rank + 1) % world;
+  ctx->sl.slab = slab;
+  ctx->sl.dy = ctx->grid.dy;
+  ctx->sl.ny = ctx->grid.ny;
+  ctx->slab_on = true;
+  // migration scratch per species
+  for (Species& S : ctx->sp) {
+    if (S.flags) continue;
+    const uint64_t cap = S.capacity;
+    const int nb = std::max(1, flag_blocks(cap));
+    S.cap_out = std::max<uint64_t>(std::min<uint64_t>(cap, 1u << 16), cap / 8);
+    if ((st = dalloc(ctx, &S.flags, cap, "migration flags")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.blk, 6 * static_cast<size_t>(nb), "block counts")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.out[0], 6 * S.cap_out, "outbox prev")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.out[1], 6 * S.cap_out, "outbox next")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.holes, cap, "hole list")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.totals, 3, "migration totals")) != B2M_OK) return st;
+    if (cudaMallocHost(&S.totals_h, 3 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(B2M_ALLOC_ERROR, "pinned migration totals");
+    }
+    const size_t need = scan_temp_bytes(nb);
+    if (need > ctx->scan_temp_bytes) {
+      char* tmp = nullptr;
+      if ((st = dalloc(ctx, &tmp, need, "scan temp")) != B2M_OK) return st;
+      ctx->scan_temp = tmp;
+      ctx->scan_temp_bytes = need;
+    }
+  }
+  return B2M_OK;
+}
+
+b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  if ((st = check_params(mp)) != B2M_OK) return st;
+  if (!ctx->slab_on) return fail(B2M_CONFIG_ERROR, "move_migrate: call b2m_slab_config first");
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  const SpeciesLaunch L = make_launch(ctx, s, *mp, 0, S.count);
+  S.pre_count = S.count;
+  S.migrate_pending = true;
+  if (S.count == 0) {
+    std::memset(S.totals_h, 0, 3 * sizeof(unsigned long long));
+    return B2M_OK;
+  }
+  const int nb = flag_blocks(S.count);
+  launch_move_flag(ctx->mode == B2M_MODE_STRICT, to_dev(ctx->grid), ctx->dE, ctx->dB,
+                   to_fast(ctx->grid), ctx->cells, L, ctx->sl, S.flags, S.blk, ctx->fault,
+                   ctx->stream);
+  launch_scan_blocks(ctx->scan_temp, ctx->scan_temp_bytes, S.blk, nb, S.totals, ctx->stream);
+  launch_scatter_out(L, S.flags, S.blk, S.out[0], S.out[1], S.cap_out, S.holes, ctx->stream);
+  B2M_CUDA(ctx, cudaMemcpyAsync(S.totals_h, S.totals, 3 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_outbox(b2m_ctx* ctx, int s, int dir, double** d_recs, uint64_t* count) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  if (dir != 0 && dir != 1) return fail(B2M_INVALID_ARGUMENT, "dir must be 0 (prev) or 1 (next)");
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (!S.migrate_pending) return fail(B2M_CONFIG_ERROR, "outbox: no migration step pending");
+  const uint64_t n = S.totals_h[dir];
+  if (n > S.cap_out) {
+    ctx->poisoned = true;
+    ctx->poison_msg = "outbox capacity exceeded (" + std::to_string(n) + " > " +
+                      std::to_string(S.cap_out) + ")";
+    return fail(B2M_ALLOC_ERROR, ctx->poison_msg);
+  }
+  if (d_recs) *d_recs = S.out[dir];
+  if (count) *count = n;
+  return B2M_OK;
+}
+
+b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t n) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (n > 0 && !d_recs) return fail(B2M_INVALID_ARGUMENT, "null inbox");
+  uint64_t holes = 0;
+  uint64_t old_n = S.count;
+  if (S.migrate_pending) {
+    holes = S.totals_h[2];
+    old_n = S.pre_count;
+  }
+  const uint64_t new_n = old_n - holes + n;
+  if (new_n > S.capacity)
+    return fail(B2M_ALLOC_ERROR, "particle batch capacity exceeded (fixed at allocation)");
+  SpeciesLaunch L{};
+  L.x = S.a[0]; L.y = S.a[1]; L.z = S.a[2];
+  L.u = S.a[3]; L.v = S.a[4]; L.w = S.a[5];
+  L.n = old_n;
+  L.species = s;
+  if (S.migrate_pending) {
+    launch_fill(L, S.holes, holes, d_recs, n, S.flags, ctx->stream);
+  } else if (n > 0) {
+    // plain append: no holes
+    launch_fill(L, S.holes, 0, d_recs, n, S.flags, ctx->stream);
+  }
+  B2M_CUDA(ctx, cudaGetLastError());
+  S.count = new_n;
+  S.migrate_pending = false;
+  return B2M_OK;
+}
+
+}  // extern "C"

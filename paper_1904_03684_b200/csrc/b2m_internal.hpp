@@ -1,0 +1,81 @@
+// b2m_internal.hpp — host-side declarations shared by the libb2m translation
+// units (kernel launchers, context, GEM generator).  Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "b2m.h"
+#include "b2m_mover.cuh"
+
+namespace b2m {
+
+// Thread-local last-error text (b2m_last_error).
+void set_error(const std::string& msg);
+b2m_status fail(b2m_status s, const std::string& msg);
+
+// Count of kernel launches issued by this process (b2m_launch_count).
+void note_launch(int n = 1);
+
+// Host computation of the exact-wrap thresholds for one axis length.
+WrapAxis make_wrap_axis(double l);
+DevGrid to_dev(const b2m_grid& g);
+FastGrid to_fast(const b2m_grid& g);
+
+// ---- launchers (b2m_kernels.cu) -------------------------------------------
+// All launches are asynchronous on `st`.
+
+// STRICT mover on one species span.  field = node AoS E (3*nodes) and B.
+void launch_move_strict(const DevGrid& g, const double* E, const double* B,
+                        const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st);
+// FAST mover on a batch of species spans (one launch).
+void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+                      int n_spans, FaultWord* fault, cudaStream_t st);
+// Node AoS E/B -> per-cell polynomial coefficients (48 doubles per cell).
+void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
+                           double2* cells, cudaStream_t st);
+// Reset the fault words to "clean".
+void launch_fault_reset(FaultWord* fault, cudaStream_t st);
+
+// Cell keys of the current positions (exact grid_cell_of), for sorting.
+void launch_cell_keys(const DevGrid& g, const double* x, const double* y, const double* z,
+                      uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+// out[i] = in[perm[i]]
+void launch_gather(const double* in, const uint32_t* perm, uint64_t n, double* out,
+                   cudaStream_t st);
+// Temp bytes needed by the radix sort of n (key,value) pairs.
+size_t sort_temp_bytes(uint64_t n, int key_bits);
+void launch_sort_pairs(void* temp, size_t temp_bytes, const uint32_t* kin, uint32_t* kout,
+                       const uint32_t* vin, uint32_t* vout, uint64_t n, int key_bits,
+                       cudaStream_t st);
+
+// ---- migration (y-slab partition layer) ----------------------------------
+struct SlabLaunch {
+  int rank, world, prev, next;
+  int slab;        // ny / world
+  double dy;       // owner_of divisor (grid.hpp Grid::dy)
+  int ny;
+};
+
+// FAST or STRICT mover fused with the owner_of scan: writes flags[i]
+// (0 stay, 1 prev, 2 next) and per-block counts blk[3*b + {0:prev,1:next,2:any}].
+void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const double* B,
+                      const FastGrid& fg, const double2* cells, const SpeciesLaunch& sp,
+                      const SlabLaunch& sl, uint8_t* flags, uint32_t* blk, FaultWord* fault,
+                      cudaStream_t st);
+int flag_blocks(uint64_t n);
+// In-place exclusive scan of the 3-wide per-block counts; totals[3] written.
+size_t scan_temp_bytes(int n_blocks);
+void launch_scan_blocks(void* temp, size_t temp_bytes, uint32_t* blk, int n_blocks,
+                        unsigned long long* totals, cudaStream_t st);
+// Leavers -> outboxes (AoS PartRec, scan order); hole list (ascending).
+void launch_scatter_out(const SpeciesLaunch& sp, const uint8_t* flags, const uint32_t* blk,
+                        double* out_prev, double* out_next, uint64_t cap_out,
+                        unsigned long long* holes, cudaStream_t st);
+// Fill holes with incoming records, then append / compact the tail.
+void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
+                 const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st);
+
+}  // namespace b2m

@@ -1,0 +1,432 @@
+// b2m_kernels.cu — sm_100a kernels and their launchers.
+//
+//   move_strict_kernel    bit-exact reference mover (kernels.cpp:52-104)
+//   move_fast_kernel      production mover, several species per launch
+//   field_to_cells_kernel node-layout E/B (field_mesh.hpp:13-60) -> per-cell
+//                         trilinear polynomial for the FAST gather
+//   cell_keys / gather    the optional cell-sort pass
+//   move_flag_kernel      mover fused with the y-slab owner scan
+//                         (partition_outgoing, runtime.cpp:46-62)
+//   scatter_out / fill    outbox compaction and hole filling
+//                         (merge_incoming, runtime.cpp:64-76)
+#include <cub/cub.cuh>
+
+#include "b2m_internal.hpp"
+
+namespace b2m {
+
+namespace {
+
+constexpr int kMaxSpans = 8;
+
+struct FastBatch {
+  SpeciesLaunch sp[kMaxSpans];
+  unsigned long long block_start[kMaxSpans + 1];
+  int n;
+};
+
+__device__ __forceinline__ void load6(const SpeciesLaunch& sp, unsigned long long i, double* p) {
+  p[0] = sp.x[i]; p[1] = sp.y[i]; p[2] = sp.z[i];
+  p[3] = sp.u[i]; p[4] = sp.v[i]; p[5] = sp.w[i];
+}
+
+__device__ __forceinline__ void store6(const SpeciesLaunch& sp, unsigned long long i,
+                                       const double* p) {
+  sp.x[i] = p[0]; sp.y[i] = p[1]; sp.z[i] = p[2];
+  sp.u[i] = p[3]; sp.v[i] = p[4]; sp.w[i] = p[5];
+}
+
+__global__ void __launch_bounds__(kMoverThreads)
+    move_strict_kernel(const __grid_constant__ DevGrid g, const double* __restrict__ E,
+                       const double* __restrict__ B, const __grid_constant__ SpeciesLaunch sp,
+                       FaultWord* fault) {
+  const unsigned long long i =
+      static_cast<unsigned long long>(blockIdx.x) * kMoverThreads + threadIdx.x;
+  if (i >= sp.n) return;
+  double p[6];
+  load6(sp, i, p);
+  if (push_strict(g, E, B, sp.beta, sp.dt, sp.dto2, sp.rounds, p))
+    store6(sp, i, p);
+  else
+    atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
+}
+
+__global__ void __launch_bounds__(kMoverThreads)
+    move_fast_kernel(const __grid_constant__ FastGrid g, const double2* __restrict__ cells,
+                     const __grid_constant__ FastBatch b, FaultWord* fault) {
+  int s = 0;
+  while (s + 1 < b.n && blockIdx.x >= b.block_start[s + 1]) ++s;
+  const SpeciesLaunch& sp = b.sp[s];
+  const unsigned long long i =
+      (static_cast<unsigned long long>(blockIdx.x) - b.block_start[s]) * kMoverThreads +
+      threadIdx.x;
+  if (i >= sp.n) return;
+  double p[6];
+  load6(sp, i, p);
+  if (push_fast(g, cells, sp.beta, sp.dt, sp.dto2_cell, sp.rounds, p))
+    store6(sp, i, p);
+  else
+    atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
+}
+
+// One thread per cell: 8 corners x 6 components -> 48 coefficients.
+__global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __restrict__ E,
+                                      const double* __restrict__ B, double2* __restrict__ cells) {
+  const long long cell = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long ncell = static_cast<long long>(nx) * ny * nz;
+  if (cell >= ncell) return;
+  const int i = static_cast<int>(cell % nx);
+  const int j = static_cast<int>((cell / nx) % ny);
+  const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
+  const long long sx = nx + 1, sy = ny + 1;
+  long long node[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int di = c & 1, dj = (c >> 1) & 1, dk = (c >> 2) & 1;
+    node[c] = (i + di) + sx * ((j + dj) + sy * (k + dk));
+  }
+  double2* out = cells + cell * (kCellDoubles / 2);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const double* F = q < 3 ? E : B;
+    const int a = q % 3;
+    // f<di dj dk>
+    const double f000 = F[3 * node[0] + a], f100 = F[3 * node[1] + a];
+    const double f010 = F[3 * node[2] + a], f110 = F[3 * node[3] + a];
+    const double f001 = F[3 * node[4] + a], f101 = F[3 * node[5] + a];
+    const double f011 = F[3 * node[6] + a], f111 = F[3 * node[7] + a];
+    const double d00 = f001 - f000, d10 = f101 - f100, d01 = f011 - f010, d11 = f111 - f110;
+    out[4 * q + 0] = make_double2(f000, d00);
+    out[4 * q + 1] = make_double2(f010 - f000, d01 - d00);
+    out[4 * q + 2] = make_double2(f100 - f000, d10 - d00);
+    out[4 * q + 3] = make_double2((f110 - f100) - (f010 - f000), (d11 - d10) - (d01 - d00));
+  }
+}
+
+__global__ void fault_reset_kernel(FaultWord* f) {
+  f->numerical = ~0ull;
+  f->cfl = ~0ull;
+}
+
+__global__ void cell_keys_kernel(const __grid_constant__ DevGrid g, const double* __restrict__ x,
+                                 const double* __restrict__ y, const double* __restrict__ z,
+                                 unsigned long long n, uint32_t* keys, uint32_t* vals) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long idx[8];
+  double wt[8];
+  uint32_t key = static_cast<uint32_t>(static_cast<long long>(g.nx) * g.ny * g.nz);
+  if (weights_strict(g, x[i], y[i], z[i], idx, wt)) {
+    // cell of corner 0: node (i,j,k) -> cell i + nx*(j + ny*k)
+    const long long node = idx[0];
+    const long long sx = g.nx + 1, sy = g.ny + 1;
+    const long long ci = node % sx, cj = (node / sx) % sy, ck = node / (sx * sy);
+    key = static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
+  }
+  keys[i] = key;
+  vals[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __restrict__ perm,
+                              unsigned long long n, double* __restrict__ out) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[perm[i]];
+}
+
+// ---- migration ------------------------------------------------------------
+
+constexpr int kFlagThreads = 256;
+
+// owner_of (runtime.cpp:39-44) with the reference's IEEE division.
+__device__ __forceinline__ int owner_of_dev(double y, const SlabLaunch& sl) {
+  int j = __double2int_rz(__ddiv_rn(y, sl.dy));
+  if (j >= sl.ny) j = sl.ny - 1;
+  if (j < 0) j = 0;
+  return j / sl.slab;
+}
+
+__global__ void __launch_bounds__(kFlagThreads)
+    move_flag_kernel(int strict, const __grid_constant__ DevGrid dg, const double* __restrict__ E,
+                     const double* __restrict__ B, const __grid_constant__ FastGrid fg,
+                     const double2* __restrict__ cells, const __grid_constant__ SpeciesLaunch sp,
+                     const __grid_constant__ SlabLaunch sl, uint8_t* __restrict__ flags,
+                     uint32_t* __restrict__ blk, unsigned n_blocks, FaultWord* fault) {
+  const unsigned long long i =
+      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
+  int flag = 0;
+  if (i < sp.n) {
+    double p[6];
+    load6(sp, i, p);
+    const bool ok = strict ? push_strict(dg, E, B, sp.beta, sp.dt, sp.dto2, sp.rounds, p)
+                           : push_fast(fg, cells, sp.beta, sp.dt, sp.dto2_cell, sp.rounds, p);
+    if (ok) {
+      store6(sp, i, p);
+      const int dest = owner_of_dev(p[1], sl);
+      if (dest != sl.rank) {
+        if (dest == sl.prev)
+          flag = 1;
+        else if (dest == sl.next)
+          flag = 2;
+        else
+          atomicMin(&fault->cfl, fault_key(sp.species, sp.base + i));
+      }
+    } else {
+      atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
+    }
+    flags[i] = static_cast<uint8_t>(flag);
+  }
+  const int c_prev = __syncthreads_count(flag == 1);
+  const int c_next = __syncthreads_count(flag == 2);
+  const int c_any = __syncthreads_count(flag != 0);
+  if (threadIdx.x == 0) {
+    blk[blockIdx.x] = static_cast<uint32_t>(c_prev);
+    blk[n_blocks + blockIdx.x] = static_cast<uint32_t>(c_next);
+    blk[2 * n_blocks + blockIdx.x] = static_cast<uint32_t>(c_any);
+  }
+}
+
+__global__ void totals_kernel(const uint32_t* counts, const uint32_t* offsets, unsigned n_blocks,
+                              unsigned long long* totals) {
+  const int t = threadIdx.x;
+  if (t < 3) {
+    const unsigned last = n_blocks - 1;
+    totals[t] = static_cast<unsigned long long>(offsets[t * n_blocks + last]) +
+                counts[t * n_blocks + last];
+  }
+}
+
+// Block-wide exclusive ranks of three predicates via warp ballots.
+__device__ __forceinline__ void block_ranks(int flag, int* r_prev, int* r_next, int* r_any) {
+  __shared__ int warp_tot[3][kFlagThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned bp = __ballot_sync(~0u, flag == 1);
+  const unsigned bn = __ballot_sync(~0u, flag == 2);
+  const unsigned ba = __ballot_sync(~0u, flag != 0);
+  if (lane == 0) {
+    warp_tot[0][wid] = __popc(bp);
+    warp_tot[1][wid] = __popc(bn);
+    warp_tot[2][wid] = __popc(ba);
+  }
+  __syncthreads();
+  int op = 0, on = 0, oa = 0;
+  for (int w = 0; w < wid; ++w) {
+    op += warp_tot[0][w];
+    on += warp_tot[1][w];
+    oa += warp_tot[2][w];
+  }
+  *r_prev = op + __popc(bp & lt);
+  *r_next = on + __popc(bn & lt);
+  *r_any = oa + __popc(ba & lt);
+}
+
+__global__ void __launch_bounds__(kFlagThreads)
+    scatter_out_kernel(const __grid_constant__ SpeciesLaunch sp, const uint8_t* __restrict__ flags,
+                       const uint32_t* __restrict__ offs, unsigned n_blocks,
+                       double* __restrict__ out_prev, double* __restrict__ out_next,
+                       unsigned long long cap_out, unsigned long long* __restrict__ holes) {
+  const unsigned long long i =
+      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
+  const int flag = i < sp.n ? flags[i] : 0;
+  int rp, rn, ra;
+  block_ranks(flag, &rp, &rn, &ra);
+  if (flag == 0) return;
+  const unsigned long long hp = offs[blockIdx.x] + static_cast<unsigned long long>(rp);
+  const unsigned long long hn = offs[n_blocks + blockIdx.x] + static_cast<unsigned long long>(rn);
+  const unsigned long long ha = offs[2 * n_blocks + blockIdx.x] + static_cast<unsigned long long>(ra);
+  holes[ha] = i;
+  double* dst = nullptr;
+  if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
+  if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
+  if (dst) {
+    double p[6];
+    load6(sp, i, p);
+#pragma unroll
+    for (int a = 0; a < 6; ++a) dst[a] = p[a];
+  }
+}
+
+// Phase A (incoming -> holes / tail append).
+__global__ void fill_in_kernel(const __grid_constant__ SpeciesLaunch sp,
+                               const unsigned long long* __restrict__ holes,
+                               unsigned long long n_holes, const double* __restrict__ in_recs,
+                               unsigned long long n_in) {
+  const unsigned long long t = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_in) return;
+  const unsigned long long dst = t < n_holes ? holes[t] : sp.n + (t - n_holes);
+  double p[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) p[a] = in_recs[6 * t + a];
+  store6(sp, dst, p);
+}
+
+// Phase C (m < L): the k-th surviving particle of [n', n) fills the k-th
+// remaining hole below n'.  Single CTA; the tail is ~L-m particles long.
+__global__ void __launch_bounds__(1024)
+    fill_tail_kernel(const __grid_constant__ SpeciesLaunch sp,
+                     const unsigned long long* __restrict__ holes, unsigned long long n_in,
+                     const uint8_t* __restrict__ flags, unsigned long long new_n) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (unsigned long long base = new_n; base < sp.n; base += 1024) {
+    const unsigned long long i = base + threadIdx.x;
+    const int keep = (i < sp.n && flags[i] == 0) ? 1 : 0;
+    int rank, total;
+    Scan(tmp).ExclusiveSum(keep, rank, total);
+    if (keep) {
+      const unsigned long long dst = holes[n_in + carry + rank];
+      double p[6];
+      load6(sp, i, p);
+      store6(sp, dst, p);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+}
+
+unsigned grid_for(uint64_t n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+void launch_move_strict(const DevGrid& g, const double* E, const double* B,
+                        const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st) {
+  if (sp.n == 0) return;
+  move_strict_kernel<<<grid_for(sp.n, kMoverThreads), kMoverThreads, 0, st>>>(g, E, B, sp, fault);
+  note_launch();
+}
+
+void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+                      int n_spans, FaultWord* fault, cudaStream_t st) {
+  for (int base = 0; base < n_spans; base += kMaxSpans) {
+    FastBatch b{};
+    b.n = 0;
+    unsigned long long blocks = 0;
+    for (int s = base; s < n_spans && b.n < kMaxSpans; ++s) {
+      if (sp[s].n == 0) continue;
+      b.sp[b.n] = sp[s];
+      b.block_start[b.n] = blocks;
+      blocks += (sp[s].n + kMoverThreads - 1) / kMoverThreads;
+      ++b.n;
+    }
+    b.block_start[b.n] = blocks;
+    if (b.n == 0) continue;
+    move_fast_kernel<<<static_cast<unsigned>(blocks), kMoverThreads, 0, st>>>(g, cells, b, fault);
+    note_launch();
+  }
+}
+
+void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
+                           double2* cells, cudaStream_t st) {
+  const long long ncell = static_cast<long long>(nx) * ny * nz;
+  field_to_cells_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(nx, ny, nz, E, B, cells);
+  note_launch();
+}
+
+void launch_fault_reset(FaultWord* fault, cudaStream_t st) {
+  fault_reset_kernel<<<1, 1, 0, st>>>(fault);
+  note_launch();
+}
+
+void launch_cell_keys(const DevGrid& g, const double* x, const double* y, const double* z,
+                      uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+  if (n == 0) return;
+  cell_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, x, y, z, n, keys, vals);
+  note_launch();
+}
+
+void launch_gather(const double* in, const uint32_t* perm, uint64_t n, double* out,
+                   cudaStream_t st) {
+  if (n == 0) return;
+  gather_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, perm, n, out);
+  note_launch();
+}
+
+size_t sort_temp_bytes(uint64_t n, int key_bits) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0,
+                                  key_bits);
+  return bytes;
+}
+
+void launch_sort_pairs(void* temp, size_t temp_bytes, const uint32_t* kin, uint32_t* kout,
+                       const uint32_t* vin, uint32_t* vout, uint64_t n, int key_bits,
+                       cudaStream_t st) {
+  if (n == 0) return;
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, static_cast<int>(n), 0,
+                                  key_bits, st);
+  note_launch((key_bits + 7) / 8 + 1);
+}
+
+int flag_blocks(uint64_t n) { return static_cast<int>(grid_for(n, kFlagThreads)); }
+
+void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const double* B,
+                      const FastGrid& fg, const double2* cells, const SpeciesLaunch& sp,
+                      const SlabLaunch& sl, uint8_t* flags, uint32_t* blk, FaultWord* fault,
+                      cudaStream_t st) {
+  const unsigned nb = static_cast<unsigned>(flag_blocks(sp.n));
+  if (nb == 0) return;
+  move_flag_kernel<<<nb, kFlagThreads, 0, st>>>(strict ? 1 : 0, dg, E, B, fg, cells, sp, sl,
+                                                 flags, blk, nb, fault);
+  note_launch();
+}
+
+size_t scan_temp_bytes(int n_blocks) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), n_blocks);
+  return bytes;
+}
+
+void launch_scan_blocks(void* temp, size_t temp_bytes, uint32_t* blk, int n_blocks,
+                        unsigned long long* totals, cudaStream_t st) {
+  // blk holds [3][n_blocks] counts followed by [3][n_blocks] offsets
+  uint32_t* counts = blk;
+  uint32_t* offs = blk + 3 * static_cast<size_t>(n_blocks);
+  for (int t = 0; t < 3; ++t) {
+    size_t b = temp_bytes;
+    cub::DeviceScan::ExclusiveSum(temp, b, counts + static_cast<size_t>(t) * n_blocks,
+                                  offs + static_cast<size_t>(t) * n_blocks, n_blocks, st);
+    note_launch();
+  }
+  totals_kernel<<<1, 32, 0, st>>>(counts, offs, static_cast<unsigned>(n_blocks), totals);
+  note_launch();
+}
+
+void launch_scatter_out(const SpeciesLaunch& sp, const uint8_t* flags, const uint32_t* blk,
+                        double* out_prev, double* out_next, uint64_t cap_out,
+                        unsigned long long* holes, cudaStream_t st) {
+  const unsigned nb = static_cast<unsigned>(flag_blocks(sp.n));
+  if (nb == 0) return;
+  const uint32_t* offs = blk + 3 * static_cast<size_t>(nb);
+  scatter_out_kernel<<<nb, kFlagThreads, 0, st>>>(sp, flags, offs, nb, out_prev, out_next,
+                                                   cap_out, holes);
+  note_launch();
+}
+
+void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
+                 const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st) {
+  if (n_in > 0) {
+    fill_in_kernel<<<grid_for(n_in, 256), 256, 0, st>>>(sp, holes, n_holes, in_recs, n_in);
+    note_launch();
+  }
+  if (n_in < n_holes) {
+    const unsigned long long new_n = sp.n - n_holes + n_in;
+    fill_tail_kernel<<<1, 1024, 0, st>>>(sp, holes, n_in, flags, new_n);
+    note_launch();
+  }
+}
+
+}  // namespace b2m

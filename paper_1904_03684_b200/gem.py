@@ -1,0 +1,95 @@
+"""Synthetic GEM input (the reference's ``init_gem``, init.cpp:62-102).
+
+Native, multithreaded and bit-identical to the reference generator
+(``b2m_gem_*`` in csrc/b2m_gem.cpp).  The mover never sees E != 0 in a stock
+GEM run, so benchmarks and parity fixtures add the nonzero E of
+the reference's own ``gem_like_field`` fixture (test_offload.cpp:60-71).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _capi
+from .mover import FieldMesh, Grid, MoverParams, ParticleBatch
+
+DEFAULT_SEED = 12345  # sim_config.hpp:32
+
+
+def gem_counts(grid: Grid, ppc: int):
+    c = (C.c_uint64 * 4)()
+    _capi.check(_capi.lib().b2m_gem_counts(C.byref(grid.to_c()), ppc, c))
+    return [int(v) for v in c]
+
+
+def gem_species_params(grid: Grid, ppc: int):
+    qom = np.zeros(4)
+    qpp = np.zeros(4)
+    _capi.check(_capi.lib().b2m_gem_species_params(C.byref(grid.to_c()), ppc, _capi.dptr(qom),
+                                                   _capi.dptr(qpp)))
+    return qom, qpp
+
+
+def init_gem_species(grid: Grid, ppc: int, seed: int = DEFAULT_SEED, pinned: bool = False,
+                     threads: int = 0, species=(0, 1, 2, 3)):
+    """The four GEM ParticleBatches (bg e-, bg i+, sheet e-, sheet i+).  The
+    two sequential sheet species are generated concurrently with the
+    parallel background ones."""
+    counts = gem_counts(grid, ppc)
+    qom, qpp = gem_species_params(grid, ppc)
+    batches = {s: ParticleBatch(s, float(qom[s]), float(qpp[s]), counts[s], pinned=pinned)
+               for s in species}
+    g = grid.to_c()
+    errs = []
+
+    def fill(s):
+        b = batches[s]
+        st = _capi.lib().b2m_gem_fill_species(C.byref(g), ppc, seed, s, _capi.ptr6(b.arrays),
+                                              threads)
+        if st != 0:
+            errs.append((st, _capi.last_error()))
+        b.set_count(counts[s])
+
+    sheet = [threading.Thread(target=fill, args=(s,)) for s in species if s >= 2]
+    for t in sheet:
+        t.start()
+    for s in species:
+        if s < 2:
+            fill(s)
+    for t in sheet:
+        t.join()
+    if errs:
+        _capi.check(errs[0][0])
+    return [batches[s] for s in species]
+
+
+def gem_field(grid: Grid) -> FieldMesh:
+    """Harris-sheet B with the psi perturbation, E = 0 (init.cpp:72-86)."""
+    f = FieldMesh(grid)
+    _capi.check(_capi.lib().b2m_gem_field(C.byref(grid.to_c()), _capi.dptr(f.E), _capi.dptr(f.B)))
+    return f
+
+
+def gem_like_field(grid: Grid) -> FieldMesh:
+    """E=(0.01 sin y, 0, 0.02), B=(tanh((y-ly/2)/0.5), 0.05 sin x, 0)
+    (test_offload.cpp:60-71)."""
+    f = FieldMesh(grid)
+    _capi.check(_capi.lib().b2m_gem_like_field(C.byref(grid.to_c()), _capi.dptr(f.E),
+                                               _capi.dptr(f.B)))
+    return f
+
+
+def gem_bench_field(grid: Grid) -> FieldMesh:
+    """Benchmark field: init_gem's B plus the gem_like_field E (nonzero, so
+    the mover's E path is exercised)."""
+    f = gem_field(grid)
+    E = gem_like_field(grid).E
+    f.E[:] = E
+    return f
+
+
+def gem_mover_params(ppc_grid: Grid, ppc: int, dt: float = 0.1, pc: int = 3):
+    qom, _ = gem_species_params(ppc_grid, ppc)
+    return [MoverParams.make(dt, float(q), pc) for q in qom]

@@ -1,0 +1,120 @@
+"""Shared test helpers: digests, bitwise and tolerance comparisons."""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+
+def digest(arrs) -> str:
+    h = hashlib.sha256()
+    for a in arrs:
+        h.update(np.ascontiguousarray(a, dtype="<f8").tobytes())
+    return h.hexdigest()
+
+
+def from_hex(lst):
+    return np.array([float.fromhex(s) for s in lst])
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want, what=""):
+    for a, (g, w) in enumerate(zip(got, want)):
+        gb, wb = bits(g), bits(w)
+        if not np.array_equal(gb, wb):
+            bad = np.nonzero(gb != wb)[0]
+            i = int(bad[0])
+            raise AssertionError(f"{what} array {a}: {len(bad)} of {len(gb)} differ; first at {i}: "
+                                 f"{g[i]!r} vs {w[i]!r}")
+
+
+# The north-star contract (BASELINE.json): positions and velocities within
+# 1e-12 relative, FMA reordering only.  Per SURVEY §8c the relative measure is
+#   velocity: per-particle vector-relative |dv| <= 1e-12 * max(|v|, 1)
+#             (the reference's own max(1,|ref|) form, test_kernels.cpp:177-179)
+#   position: periodic |dx| <= 1e-12 * L per axis
+# with particle count and cell indices exact.
+TOL = 1e-12
+
+
+def periodic_delta(a, b, L):
+    d = np.abs(a - b)
+    return np.minimum(d, L - d)
+
+
+def assert_within_contract(got, want, grid, tol=TOL, what=""):
+    nx, ny, nz, lx, ly, lz = grid
+    for a, L in zip(range(3), (lx, ly, lz)):
+        d = periodic_delta(got[a], want[a], L)
+        m = float(np.max(d)) if len(d) else 0.0
+        assert m <= tol * L, f"{what} position axis {a}: max |dx| = {m:.3e} > {tol * L:.3e}"
+    dv = np.sqrt(sum((got[a] - want[a]) ** 2 for a in range(3, 6)))
+    vn = np.sqrt(sum(want[a] ** 2 for a in range(3, 6)))
+    lim = tol * np.maximum(vn, 1.0)
+    if len(dv):
+        worst = float(np.max(dv / np.maximum(vn, 1.0)))
+        assert np.all(dv <= lim), f"{what} velocity: max |dv|/max(|v|,1) = {worst:.3e}"
+
+
+def cells_of(p6, grid):
+    """Reference grid_cell_of cell indices (grid.hpp:64-82): trunc(pos/d),
+    clamped to n-1, as one flat index."""
+    nx, ny, nz, lx, ly, lz = grid
+    dx, dy, dz = lx / nx, ly / ny, lz / nz
+    i = np.minimum(np.trunc(p6[0] / dx).astype(np.int64), nx - 1)
+    j = np.minimum(np.trunc(p6[1] / dy).astype(np.int64), ny - 1)
+    k = np.minimum(np.trunc(p6[2] / dz).astype(np.int64), nz - 1)
+    return i + nx * (j + ny * k)
+
+
+def random_particles(grid, n, seed, vscale=0.5):
+    nx, ny, nz, lx, ly, lz = grid
+    r = np.random.default_rng(seed)
+    return [r.random(n) * lx, r.random(n) * ly, r.random(n) * lz,
+            vscale * r.standard_normal(n), vscale * r.standard_normal(n),
+            vscale * r.standard_normal(n)]
+
+
+def random_field(grid, seed, scale=1.0):
+    nx, ny, nz = grid[:3]
+    r = np.random.default_rng(seed)
+    F = []
+    for _ in range(2):
+        G = scale * r.standard_normal((nz + 1, ny + 1, nx + 1, 3))
+        G[:, :, nx] = G[:, :, 0]
+        G[:, ny, :] = G[:, 0, :]
+        G[nz, :, :] = G[0, :, :]
+        F.append(np.ascontiguousarray(G.reshape(-1)))
+    return F[0], F[1]
+
+
+def uniform_field(grid, E0, B0):
+    nx, ny, nz = grid[:3]
+    n = (nx + 1) * (ny + 1) * (nz + 1)
+    return np.tile(np.asarray(E0, dtype=np.float64), n), np.tile(np.asarray(B0, dtype=np.float64), n)
+
+
+def cramer_vbar(vn, E, B, beta):
+    """Independent solve of (I - beta[x B]) vbar = vn + beta E by Cramer's rule
+    (the reference's own test oracle, test_kernels.cpp:30-53), vectorised."""
+    rhs = vn + beta * E
+    M = np.zeros(vn.shape[:-1] + (3, 3))
+    M[..., 0, 0] = 1.0
+    M[..., 1, 1] = 1.0
+    M[..., 2, 2] = 1.0
+    M[..., 0, 1] = -beta * B[..., 2]
+    M[..., 0, 2] = beta * B[..., 1]
+    M[..., 1, 0] = beta * B[..., 2]
+    M[..., 1, 2] = -beta * B[..., 0]
+    M[..., 2, 0] = -beta * B[..., 1]
+    M[..., 2, 1] = beta * B[..., 0]
+    d = np.linalg.det(M)
+    out = np.empty_like(rhs)
+    for c in range(3):
+        Mc = M.copy()
+        Mc[..., :, c] = rhs
+        out[..., c] = np.linalg.det(Mc) / d
+    return out

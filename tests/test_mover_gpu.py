@@ -1,0 +1,314 @@
+"""Parity of the sm_100a mover (through the C ABI) with the oracle and the
+reference's golden vectors.  Needs a B200: ``pytest -m gpu``.
+
+STRICT mode must be bit-identical to the reference; FAST mode must meet the
+north-star contract (1e-12, count and cell indices exact; tests/_util.py)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1904_03684_b200 import gem
+from paper_1904_03684_b200.engine import B200Engine, DeviceStore
+from paper_1904_03684_b200.errors import EngineFault, NumericalFault
+from paper_1904_03684_b200.mover import FieldMesh, Grid, MoverParams, move_batch
+from tests._util import (assert_bitwise, assert_within_contract, cells_of, digest, from_hex,
+                         random_field, random_particles, uniform_field)
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["strict", "fast"]
+
+
+def port_move(p6, E, B, grid, dt, qom, pc):
+    out = [np.ascontiguousarray(a, dtype=np.float64).copy() for a in p6]
+    assert oracle.port_move_batch(out, E, B, grid, dt, qom, pc) == -1
+    return out
+
+
+def gpu_move(p6, E, B, grid, dt, qom, pc, mode):
+    out = [np.ascontiguousarray(a, dtype=np.float64).copy() for a in p6]
+    move_batch(out, (E, B), Grid.make(*grid), MoverParams.make(dt, qom, pc), mode=mode)
+    return out
+
+
+def check(got, want, grid, mode, what=""):
+    if mode == "strict":
+        assert_bitwise(got, want, what)
+    else:
+        assert_within_contract(got, want, grid, what=what)
+        np.testing.assert_array_equal(cells_of(got, grid), cells_of(want, grid))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case,field", [("c1_move", "like"), ("c1_move_gemfield_pc5", "gem"),
+                                        ("c1_move_pc1", "like"), ("desk_move", "like+gemB")])
+def test_golden_cases(gpu, golden, mode, case, field):
+    gd = golden[case]
+    grid = tuple(gd["grid"])
+    init = golden["desk_init" if case.startswith("desk") else "c1_init"]
+    g = Grid.make(*grid)
+    batches = gem.init_gem_species(g, init["ppc"], init["seed"])
+    if field == "gem":
+        f = gem.gem_field(g)
+    elif field == "like":
+        f = gem.gem_like_field(g)
+    else:
+        f = gem.gem_bench_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    assert digest([E, B]) == gd["field_sha"]
+    for s, sp in enumerate(gd["species"]):
+        p0 = batches[s].span()
+        assert digest(p0) == sp["in_sha"]
+        got = gpu_move(p0, E, B, grid, gd["dt"], sp["qom"], gd["pc"], mode)
+        if mode == "strict":
+            assert digest(got) == sp["out_sha"], f"species {s} not bit-identical to the reference"
+        else:
+            want = port_move(p0, E, B, grid, gd["dt"], sp["qom"], gd["pc"])
+            assert digest(want) == sp["out_sha"]
+            check(got, want, grid, mode, f"species {s}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_spec_kat(gpu, golden, mode):
+    k = golden["kat"]
+    grid = tuple(k["grid"])
+    E, B = uniform_field(grid, [0, 0, 0], [0, 0, 1])
+    p0 = [np.array([v]) for v in list(from_hex(k["x0"])) + list(from_hex(k["v0"]))]
+    got = gpu_move(p0, E, B, grid, k["dt"], k["qom"], k["pc"], mode)
+    want = [np.array([v]) for v in list(from_hex(k["x1"])) + list(from_hex(k["v1"]))]
+    check(got, want, grid, mode, "KAT")
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("seed,qom,pc", [(1, -25.0, 3), (2, 1.0, 3), (3, -25.0, 5), (4, 1.0, 1),
+                                         (5, -25.0, 2), (6, 1.0, 4)])
+def test_random_fields_vs_oracle(gpu, mode, seed, qom, pc):
+    grid = (6, 5, 4, 2.4, 2.0, 1.6)
+    E, B = random_field(grid, seed, scale=0.7)
+    p0 = random_particles(grid, 50000, seed)
+    check(gpu_move(p0, E, B, grid, 0.1, qom, pc, mode), port_move(p0, E, B, grid, 0.1, qom, pc),
+          grid, mode, "random fields")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_edge_positions_vs_oracle(gpu, mode):
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    E, B = random_field(grid, 9, scale=0.5)
+    L = 4.0
+    edge = [0.0, -0.0, 1.0, 2.0, 3.0, np.nextafter(L, 0.0), np.nextafter(1.0, 0.0),
+            np.nextafter(3.0, 4.0), 5e-324, 1e-17]
+    xs = np.array(np.meshgrid(edge, edge, edge)).reshape(3, -1)
+    n = xs.shape[1]
+    r = np.random.default_rng(5)
+    for vs in (0.3, 1e-18, 4.0):  # tiny velocities keep positions on the edges
+        p0 = [xs[0].copy(), xs[1].copy(), xs[2].copy()] + [vs * r.standard_normal(n) for _ in range(3)]
+        for qom in (-25.0, 1.0):
+            check(gpu_move(p0, E, B, grid, 0.1, qom, 3, mode),
+                  port_move(p0, E, B, grid, 0.1, qom, 3), grid, mode, f"edges vs={vs}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_seam_crossings_wrap_exactly(gpu, mode):
+    """Particles crossing the periodic seam in the final update, with exactly
+    representable x0 + v*dt (dt = 1/8, offsets in units of ulp(L)): every
+    mode must then produce the reference's wrap_len bit for bit, including
+    the rounding fix-ups of grid.hpp:45-50."""
+    grid = (8, 8, 8, 6.4, 6.4, 6.4)
+    E, B = uniform_field(grid, [0, 0, 0], [0, 0, 0])
+    L = 6.4
+    ulp = 2.0 ** -50  # spacing of doubles in [4, 8)
+    r = np.random.default_rng(11)
+    n = 8192
+    k = r.integers(0, 64, n).astype(np.float64)
+    m = r.integers(-64, 64, n).astype(np.float64)
+    top = np.nextafter(L, 0.0) - k * ulp          # just below L
+    bot = k * 2.0 ** -60                           # just above 0
+    x = np.where(np.arange(n) % 2 == 0, top, bot)
+    v = m * ulp * 8.0                              # v*dt = m*ulp exactly
+    v = np.where(np.arange(n) % 2 == 0, np.abs(v), -np.abs(v) * 2.0 ** -10)
+    p0 = [x.copy(), x.copy(), x.copy(), v.copy(), v.copy(), v.copy()]
+    got = gpu_move(p0, E, B, grid, 0.125, 1.0, 3, mode)
+    want = port_move(p0, E, B, grid, 0.125, 1.0, 3)
+    assert_bitwise(got, want, "seam")
+    for a in range(3):
+        assert np.all((got[a] >= 0) & (got[a] < L))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_nan_fault_semantics(gpu, golden, mode):
+    gd = golden["nan_fault"]
+    g = Grid.make(4, 4, 4, 4.0, 4.0, 4.0)
+    E, B = uniform_field(g.as_tuple(), [0, 0, 0], [0, 0, 1])
+    p = [np.array([1.0, 2.0, 3.0]), np.array([1.0, 2.0, 3.0]), np.array([1.0, 2.0, 3.0]),
+         np.array([0.1, np.nan, 0.1]), np.zeros(3), np.zeros(3)]
+    with pytest.raises(NumericalFault, match="particle index 1$") as ei:
+        move_batch(p, (E, B), g, MoverParams.make(0.1, 1.0, 2), mode=mode)
+    assert ei.value.index == 1
+    for a in range(6):
+        want = from_hex(gd["after"][a])
+        if mode == "strict":
+            np.testing.assert_array_equal(np.nan_to_num(p[a]), np.nan_to_num(want))
+        else:
+            np.testing.assert_allclose(np.nan_to_num(p[a]), np.nan_to_num(want), rtol=1e-12, atol=1e-14)
+        # the faulting particle and every later one are untouched
+        assert p[a][2] == [3.0, 3.0, 3.0, 0.1, 0.0, 0.0][a]
+        if a != 3:
+            assert p[a][1] == [2.0, 2.0, 2.0, 0.0, 0.0, 0.0][a]
+    assert np.isnan(p[3][1])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_out_of_domain_input_faults(gpu, mode):
+    g = Grid.make(4, 4, 4, 4.0, 4.0, 4.0)
+    E, B = uniform_field(g.as_tuple(), [0, 0, 0], [0, 0, 1])
+    p = [np.array([1.0, 4.0, 2.0, -0.5]), np.ones(4), np.ones(4), np.zeros(4), np.zeros(4),
+         np.zeros(4)]
+    with pytest.raises(NumericalFault) as ei:
+        move_batch(p, (E, B), g, MoverParams.make(0.1, 1.0, 3), mode=mode)
+    assert ei.value.index == 1
+    assert p[0][0] == 1.0 and p[0][1] == 4.0 and p[0][3] == -0.5
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_empty_batch_is_noop(gpu, mode):
+    g = Grid.make(4, 4, 4, 4.0, 4.0, 4.0)
+    E, B = uniform_field(g.as_tuple(), [0, 0, 0], [0, 0, 1])
+    p = [np.zeros(0) for _ in range(6)]
+    move_batch(p, (E, B), g, MoverParams.make(0.1, 1.0, 3), mode=mode)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_uniform_field_pc_fixed_point(gpu, mode):
+    """SPEC.md: uniform fields make the corrector a fixed point -> pc 1 and 3
+    give identical results (bitwise in strict mode, as in the reference)."""
+    grid = (8, 8, 8, 4.0, 4.0, 4.0)
+    E, B = uniform_field(grid, [0.3, -0.2, 0.1], [0.5, 0.25, -0.75])
+    p0 = random_particles(grid, 20000, 3)
+    a = gpu_move(p0, E, B, grid, 0.1, -25.0, 1, mode)
+    b = gpu_move(p0, E, B, grid, 0.1, -25.0, 3, mode)
+    if mode == "strict":
+        assert_bitwise(a, b)
+    else:
+        assert_within_contract(a, b, grid)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_device_store_sort_preserves_multiset(gpu, mode):
+    g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
+    grid = g.as_tuple()
+    p0 = random_particles(grid, 100000, 21)
+    f = FieldMesh(g, *random_field(grid, 2, 0.3))
+    st = DeviceStore(g, [len(p0[0])], mode)
+    st.upload_field(f)
+    st.upload(0, p0)
+    st.sort(0)
+    srt = [np.empty_like(a) for a in p0]
+    assert st.download(0, srt) == len(p0[0])
+    st.sync()
+    np.testing.assert_array_equal(oracle.multiset(srt), oracle.multiset(p0))
+    keys = cells_of(srt, grid)
+    assert np.all(np.diff(keys) >= 0)
+    # moving the sorted batch == moving those particles with the oracle
+    st.move(0, MoverParams.make(0.1, -25.0, 3))
+    out = [np.empty_like(a) for a in p0]
+    st.download(0, out)
+    st.sync()
+    want = port_move(srt, f.E.ravel(), f.B.ravel(), grid, 0.1, -25.0, 3)
+    check(out, want, grid, mode, "sorted move")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_engine_matches_oracle_over_steps(gpu, mode):
+    """test_offload.cpp:435-462: 4 species x 5000 particles, gem_like_field,
+    3 steps through the engine == 3 oracle steps."""
+    g = Grid.make(8, 8, 8, 6.4, 6.4, 6.4)
+    grid = g.as_tuple()
+    f = gem.gem_like_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    from paper_1904_03684_b200.mover import ParticleBatch
+    batches, refs, mps = [], [], []
+    for s in range(4):
+        qom = 1.0 if s % 2 else -25.0
+        p0 = random_particles(grid, 5000, 7 + s, vscale=0.1)
+        b = ParticleBatch(s, qom, 0.01, 5000, pinned=True)
+        b.assign(p0)
+        batches.append(b)
+        refs.append([a.copy() for a in p0])
+        mps.append(MoverParams.make(0.05, qom, 3))
+    for schedule in ("pipeline", "prefetch", "sync"):
+        eng = B200Engine(g, mode=mode, schedule=schedule, chunk=1536)
+        bs = []
+        for s in range(4):
+            b = ParticleBatch(s, batches[s].qom, 0.01, 5000, pinned=(schedule == "pipeline"))
+            b.assign(refs[s])
+            bs.append(b)
+        eng.prime(f, bs)
+        for step in range(3):
+            eng.run_mover(f, bs, mps)
+        for s in range(4):
+            want = [a.copy() for a in refs[s]]
+            for step in range(3):
+                assert oracle.port_move_batch(want, E, B, grid, 0.05, mps[s].qom, 3) == -1
+            if mode == "strict":
+                assert_bitwise(bs[s].span(), want, f"{schedule} species {s}")
+            else:
+                assert_within_contract(bs[s].span(), want, grid, tol=1e-11, what=f"{schedule} s{s}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_engine_fault_poisons(gpu, mode):
+    """test_offload.cpp:464-481: a kernel fault surfaces as EngineFault naming
+    the particle; the engine stays poisoned."""
+    g = Grid.make(8, 8, 8, 6.4, 6.4, 6.4)
+    f = gem.gem_like_field(g)
+    from paper_1904_03684_b200.mover import ParticleBatch
+    bs = []
+    for s in range(2):
+        b = ParticleBatch(s, -25.0 if s == 0 else 1.0, 0.01, 10)
+        b.assign(random_particles(g.as_tuple(), 10, s, 0.1))
+        bs.append(b)
+    bs[1].arrays[3][3] = np.nan
+    eng = B200Engine(g, mode=mode, schedule="sync")
+    eng.prime(f, bs)
+    mps = [MoverParams.make(0.05, b.qom, 3) for b in bs]
+    with pytest.raises(EngineFault, match="particle"):
+        eng.run_mover(f, bs, mps)
+    with pytest.raises(EngineFault):
+        eng.run_mover(f, bs, mps)
+
+
+def test_full_c2_sampled_parity(gpu):
+    """BASELINE config 2 at full size (61,046,784 particles): FAST move of
+    the whole GEM state on the GPU; a 200k-particle random sample per species
+    is checked against the oracle (the mover is per-particle independent,
+    kernels.hpp:46-48), plus size-independent properties on all particles."""
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    assert sum(b.count() for b in batches) == 61046784
+    f = gem.gem_bench_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    st = DeviceStore(g, [b.count() for b in batches], "fast")
+    st.upload_field(f)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    st.move_all(mps)
+    outs = []
+    for s, b in enumerate(batches):
+        out = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, out)
+        outs.append(out)
+    st.sync()
+    r = np.random.default_rng(0)
+    for s, b in enumerate(batches):
+        out = outs[s]
+        for a, L in zip(range(3), grid[3:]):
+            assert np.all((out[a] >= 0) & (out[a] < L))
+        assert all(np.all(np.isfinite(a)) for a in out)
+        idx = np.sort(r.choice(b.count(), size=min(200000, b.count()), replace=False))
+        p0 = [a[idx].copy() for a in b.span()]
+        want = port_move(p0, E, B, grid, 0.1, b.qom, 3)
+        got = [a[idx] for a in out]
+        assert_within_contract(got, want, grid, what=f"C2 species {s}")
+        np.testing.assert_array_equal(cells_of(got, grid), cells_of(want, grid))
