@@ -593,17 +593,16 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
   if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
   if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
   const int ns = static_cast<int>(ctx->sp.size());
-  if (ctx->mode == B2M_MODE_STRICT) {
-    for (int s = 0; s < ns; ++s)
-      if ((st = b2m_move(ctx, s, &mp[s])) != B2M_OK) return st;
-    return B2M_OK;
-  }
   std::vector<SpeciesLaunch> L;
   for (int s = 0; s < ns; ++s) {
     if ((st = check_params(&mp[s])) != B2M_OK) return st;
     L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
   }
-  launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault, ctx->stream);
+  if (ctx->mode == B2M_MODE_STRICT)
+    launch_move_strict_batch(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
+                             ctx->stream);
+  else
+    launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault, ctx->stream);
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }

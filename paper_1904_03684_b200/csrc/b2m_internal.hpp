@@ -30,6 +30,9 @@ FastGrid to_fast(const b2m_grid& g);
 // STRICT mover on one species span.  field = node AoS E (3*nodes) and B.
 void launch_move_strict(const DevGrid& g, const double* E, const double* B,
                         const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st);
+void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st);
 // FAST mover on a batch of species spans (one launch).
 void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st);

@@ -12,18 +12,11 @@
 #include <cub/cub.cuh>
 
 #include "b2m_internal.hpp"
+#include "b2m_tile.cuh"
 
 namespace b2m {
 
 namespace {
-
-constexpr int kMaxSpans = 8;
-
-struct FastBatch {
-  SpeciesLaunch sp[kMaxSpans];
-  unsigned long long block_start[kMaxSpans + 1];
-  int n;
-};
 
 __device__ __forceinline__ void load6(const SpeciesLaunch& sp, unsigned long long i, double* p) {
   p[0] = sp.x[i]; p[1] = sp.y[i]; p[2] = sp.z[i];
@@ -36,37 +29,140 @@ __device__ __forceinline__ void store6(const SpeciesLaunch& sp, unsigned long lo
   sp.u[i] = p[3]; sp.v[i] = p[4]; sp.w[i] = p[5];
 }
 
-__global__ void __launch_bounds__(kMoverThreads)
-    move_strict_kernel(const __grid_constant__ DevGrid g, const double* __restrict__ E,
-                       const double* __restrict__ B, const __grid_constant__ SpeciesLaunch sp,
-                       FaultWord* fault) {
-  const unsigned long long i =
-      static_cast<unsigned long long>(blockIdx.x) * kMoverThreads + threadIdx.x;
-  if (i >= sp.n) return;
-  double p[6];
-  load6(sp, i, p);
-  if (push_strict(g, E, B, sp.beta, sp.dt, sp.dto2, sp.rounds, p))
-    store6(sp, i, p);
-  else
-    atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
-}
+// Persistent TMA-staged mover (b2m_tile.cuh).  Tiles of PPT*128 particles
+// are distributed round-robin over the grid; each block keeps kTileStages
+// tiles in flight through shared memory (bulk TMA in, bulk TMA out).
+template <bool STRICT>
+__global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : kTileMinBlocks)
+    tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TileSpans S,
+                unsigned long long total_tiles, FaultWord* fault) {
+  constexpr int PPT = TileShape<STRICT>::ppt;
+  constexpr int TILE = TileShape<STRICT>::tile;
+  extern __shared__ __align__(128) unsigned char tile_smem[];
+  auto buf = reinterpret_cast<double(*)[6][TILE]>(tile_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tile_smem + kTileStages * 6 * TILE * 8);
+  const int tid = threadIdx.x;
+  const unsigned long long G = gridDim.x;
 
-__global__ void __launch_bounds__(kMoverThreads)
-    move_fast_kernel(const __grid_constant__ FastGrid g, const double2* __restrict__ cells,
-                     const __grid_constant__ FastBatch b, FaultWord* fault) {
-  int s = 0;
-  while (s + 1 < b.n && blockIdx.x >= b.block_start[s + 1]) ++s;
-  const SpeciesLaunch& sp = b.sp[s];
-  const unsigned long long i =
-      (static_cast<unsigned long long>(blockIdx.x) - b.block_start[s]) * kMoverThreads +
-      threadIdx.x;
-  if (i >= sp.n) return;
-  double p[6];
-  load6(sp, i, p);
-  if (push_fast(g, cells, sp.beta, sp.dt, sp.dto2_cell, sp.rounds, p))
-    store6(sp, i, p);
-  else
-    atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
+  auto resolve = [&](unsigned long long tile, int& s, unsigned long long& off, int& cnt,
+                     bool& full) {
+    s = 0;
+    while (s + 1 < S.n && tile >= S.tile_start[s + 1]) ++s;
+    off = (tile - S.tile_start[s]) * TILE;
+    const unsigned long long left = S.sp[s].n - off;
+    cnt = left < static_cast<unsigned long long>(TILE) ? static_cast<int>(left) : TILE;
+    full = (cnt == TILE) && S.tma_ok[s];
+  };
+  auto issue = [&](unsigned long long k) {  // thread 0
+    const unsigned long long tile = blockIdx.x + k * G;
+    if (tile >= total_tiles) return;
+    int s, cnt;
+    unsigned long long off;
+    bool full;
+    resolve(tile, s, off, cnt, full);
+    const int st = static_cast<int>(k % kTileStages);
+    if (full) {
+      const SpeciesLaunch& sp = S.sp[s];
+      mbar_arrive_tx(&bar[st], 6 * TILE * sizeof(double));
+      const double* src[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+        tma_load_1d(buf[st][a], src[a] + off, TILE * sizeof(double), &bar[st]);
+    } else {
+      mbar_arrive(&bar[st]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kTileStages; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < kTileStages; ++k) issue(k);
+
+  for (unsigned long long k = 0;; ++k) {
+    const unsigned long long tile = blockIdx.x + k * G;
+    if (tile >= total_tiles) break;
+    int s, cnt;
+    unsigned long long off;
+    bool full;
+    resolve(tile, s, off, cnt, full);
+    const int st = static_cast<int>(k % kTileStages);
+    mbar_wait(&bar[st], static_cast<uint32_t>((k / kTileStages) & 1));
+    const SpeciesLaunch& sp = S.sp[s];
+    double* ptr[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
+    const int i0 = PPT * tid;
+    bool has[PPT], ok[PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) has[i] = i0 + i < cnt;
+    if (STRICT) {
+      double p[PPT][6];
+      if (full) {
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+#pragma unroll
+          for (int i = 0; i < PPT; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(&buf[st][a][i0 + i]);
+            p[i][a] = v.x;
+            p[i + 1][a] = v.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+          for (int i = 0; i < PPT; ++i) p[i][a] = has[i] ? ptr[a][off + i0 + i] : 0.0;
+      }
+      if (has[0]) {
+        push_group<true, PPT>(F, sp, p, has, ok);
+      } else {
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) ok[i] = false;
+      }
+      // a faulting particle keeps its input (the reference leaves it untouched)
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+          if (!(has[i] && ok[i])) continue;
+          if (full)
+            buf[st][a][i0 + i] = p[i][a];
+          else
+            ptr[a][off + i0 + i] = p[i][a];
+        }
+    } else {
+      // inputs are read from (and results written to) the staged tile; a
+      // faulting particle is never stored, so its input stays in place
+      auto load = [&](int i, int a) -> double {
+        return full ? buf[st][a][i0 + i] : ptr[a][off + i0 + i];
+      };
+      auto store = [&](int i, int a, double v) {
+        if (full)
+          buf[st][a][i0 + i] = v;
+        else
+          ptr[a][off + i0 + i] = v;
+      };
+      push_fast_stream<PPT>(F.fg, F.cells, sp, has, ok, load, store);
+    }
+#pragma unroll
+    for (int i = 0; i < PPT; ++i)
+      if (has[i] && !ok[i])
+        atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
+    if (full) fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      if (full) {
+#pragma unroll
+        for (int a = 0; a < 6; ++a) tma_store_1d(ptr[a] + off, buf[st][a], TILE * sizeof(double));
+      }
+      tma_commit();
+      // refill the buffer just consumed once its bulk store has read it
+      tma_wait_read<0>();
+      issue(k + kTileStages);
+    }
+  }
+  if (tid == 0) tma_wait_all();
 }
 
 // One thread per cell: 8 corners x 6 components -> 48 coefficients.
@@ -298,31 +394,78 @@ unsigned grid_for(uint64_t n, int threads) {
 // launchers
 // ---------------------------------------------------------------------------
 
+namespace {
+
+template <bool STRICT>
+int tile_grid(unsigned long long total_tiles) {
+  static int blocks_per_sm = -1, sms = 0;
+  if (blocks_per_sm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(tile_kernel<STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TileShape<STRICT>::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tile_kernel<STRICT>,
+                                                  kTileThreads, TileShape<STRICT>::smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const unsigned long long g = static_cast<unsigned long long>(sms) * blocks_per_sm;
+  return static_cast<int>(total_tiles < g ? total_tiles : g);
+}
+
+template <bool STRICT>
+void launch_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                  cudaStream_t st) {
+  for (int base = 0; base < n_spans; base += kMaxTileSpans) {
+    TileSpans S{};
+    unsigned long long tiles = 0;
+    for (int s = base; s < n_spans && S.n < kMaxTileSpans; ++s) {
+      if (sp[s].n == 0) continue;
+      S.sp[S.n] = sp[s];
+      S.tile_start[S.n] = tiles;
+      const uintptr_t m =
+          reinterpret_cast<uintptr_t>(sp[s].x) | reinterpret_cast<uintptr_t>(sp[s].y) |
+          reinterpret_cast<uintptr_t>(sp[s].z) | reinterpret_cast<uintptr_t>(sp[s].u) |
+          reinterpret_cast<uintptr_t>(sp[s].v) | reinterpret_cast<uintptr_t>(sp[s].w);
+      S.tma_ok[S.n] = (m & 15u) == 0;
+      tiles += (sp[s].n + TileShape<STRICT>::tile - 1) / TileShape<STRICT>::tile;
+      ++S.n;
+    }
+    S.tile_start[S.n] = tiles;
+    if (S.n == 0) continue;
+    tile_kernel<STRICT><<<tile_grid<STRICT>(tiles), kTileThreads, TileShape<STRICT>::smem, st>>>(
+        F, S, tiles, fault);
+    note_launch();
+  }
+}
+
+}  // namespace
+
 void launch_move_strict(const DevGrid& g, const double* E, const double* B,
                         const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st) {
-  if (sp.n == 0) return;
-  move_strict_kernel<<<grid_for(sp.n, kMoverThreads), kMoverThreads, 0, st>>>(g, E, B, sp, fault);
-  note_launch();
+  TileField F{};
+  F.dg = g;
+  F.E = E;
+  F.B = B;
+  launch_tiles<true>(F, &sp, 1, fault, st);
+}
+
+void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st) {
+  TileField F{};
+  F.dg = g;
+  F.E = E;
+  F.B = B;
+  launch_tiles<true>(F, sp, n_spans, fault, st);
 }
 
 void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st) {
-  for (int base = 0; base < n_spans; base += kMaxSpans) {
-    FastBatch b{};
-    b.n = 0;
-    unsigned long long blocks = 0;
-    for (int s = base; s < n_spans && b.n < kMaxSpans; ++s) {
-      if (sp[s].n == 0) continue;
-      b.sp[b.n] = sp[s];
-      b.block_start[b.n] = blocks;
-      blocks += (sp[s].n + kMoverThreads - 1) / kMoverThreads;
-      ++b.n;
-    }
-    b.block_start[b.n] = blocks;
-    if (b.n == 0) continue;
-    move_fast_kernel<<<static_cast<unsigned>(blocks), kMoverThreads, 0, st>>>(g, cells, b, fault);
-    note_launch();
-  }
+  TileField F{};
+  F.fg = g;
+  F.cells = cells;
+  launch_tiles<false>(F, sp, n_spans, fault, st);
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,

@@ -1,0 +1,578 @@
+// b2m_tile.cuh — the production mover: persistent, TMA-staged, two particles
+// per thread sharing a register-resident cell cache.
+//
+// Why this shape (profiles/r01_fast_v1.md): a thread-per-particle gather pulls
+// 48 doubles of field per particle per predictor round into registers, and on
+// sm_100a the L1->register writeback (128 B/clk/SM) saturates long before the
+// FP64 pipe or HBM do.  The field of a cell is identical for every round in
+// which the particle stays in that cell (>99% of rounds: |v| dt/2 is a few
+// percent of a cell) and for both particles of a thread after the cell sort,
+// so the 48 values are loaded into registers once per (thread, cell) and
+// reused: 3 rounds x 2 particles per load instead of 1.
+//
+// Particle tiles (256 particles x 6 SoA arrays = 12 KB) stream through shared
+// memory with 1-D bulk TMA copies (cp.async.bulk + mbarrier, 3 stages), and
+// results leave through bulk TMA stores, so HBM latency hides behind the
+// FP64 work of the previous tiles without spending registers on prefetch.
+// Partial tail tiles (and unaligned spans) use plain loads/stores.
+#pragma once
+
+#include "b2m_mover.cuh"
+
+namespace b2m {
+
+constexpr int kTileThreads = 128;
+constexpr int kTileStages = 2;
+constexpr int kTileMinBlocks = 3;
+// particles per thread: FAST streams coefficients to 4 particles, STRICT
+// keeps a register cell cache shared by 2
+template <bool STRICT>
+struct TileShape {
+  static constexpr int ppt = STRICT ? 2 : 4;
+  static constexpr int tile = kTileThreads * ppt;
+  static constexpr int smem = kTileStages * 6 * tile * 8 + 64;
+};
+constexpr int kMaxTileSpans = 8;
+
+struct TileSpans {
+  SpeciesLaunch sp[kMaxTileSpans];
+  unsigned long long tile_start[kMaxTileSpans + 1];
+  int tma_ok[kMaxTileSpans];
+  int n;
+};
+
+// ---------------------------------------------------------------------------
+// TMA / mbarrier primitives (PTX ISA 8.x, sm_90+; SASS: UBLKCP, SYNCS)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_1d(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// per-particle state machines
+// ---------------------------------------------------------------------------
+
+struct PState {
+  double x0, y0, z0, u0, v0, w0;
+  double tx, ty, tz;   // predictor position (FAST: cell units, STRICT: physical)
+  double cx0, cy0, cz0;  // FAST: x0 in cell units
+  double bx, by, bz;   // time-centred velocity
+  bool ok;
+};
+
+// Cell field cache.  FAST: 24 double2 polynomial pairs (b2m_mover.cuh
+// layout).  STRICT: the 8 corner nodes' (E, B) in corner order.
+struct CellCache {
+  double2 c[24];
+  int cell;
+};
+
+__device__ __forceinline__ void cache_load_fast(CellCache& cc, const double2* __restrict__ cells,
+                                                int cell) {
+  const double2* src = cells + static_cast<long long>(cell) * 24;
+#pragma unroll
+  for (int q = 0; q < 24; ++q) cc.c[q] = __ldg(src + q);
+  cc.cell = cell;
+}
+
+__device__ __forceinline__ void cache_load_strict(CellCache& cc, const DevGrid& g,
+                                                  const double* __restrict__ E,
+                                                  const double* __restrict__ B, int cell) {
+  const int i = cell % g.nx;
+  const int j = (cell / g.nx) % g.ny;
+  const int k = cell / (g.nx * g.ny);
+  const long long sx1 = g.nx + 1, sy1 = g.ny + 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int di = c & 1, dj = (c >> 1) & 1, dk = (c >> 2) & 1;
+    const long long n = 3 * ((i + di) + sx1 * ((j + dj) + sy1 * (k + dk)));
+    cc.c[3 * c + 0] = make_double2(__ldg(E + n + 0), __ldg(E + n + 1));
+    cc.c[3 * c + 1] = make_double2(__ldg(E + n + 2), __ldg(B + n + 0));
+    cc.c[3 * c + 2] = make_double2(__ldg(B + n + 1), __ldg(B + n + 2));
+  }
+  cc.cell = cell;
+}
+
+__device__ __forceinline__ void begin(PState& P, const double* p) {
+  P.x0 = p[0]; P.y0 = p[1]; P.z0 = p[2];
+  P.u0 = p[3]; P.v0 = p[4]; P.w0 = p[5];
+  P.tx = P.x0; P.ty = P.y0; P.tz = P.z0;
+  P.bx = P.u0; P.by = P.v0; P.bz = P.w0;
+  P.ok = true;
+}
+
+// ---- FAST -----------------------------------------------------------------
+
+__device__ __forceinline__ void fast_begin(PState& P, const FastGrid& g, const double* p) {
+  begin(P, p);
+  // grid.hpp:65-67: the first locate rejects x0 outside [0,l)
+  P.ok = (P.x0 >= 0.0 && P.x0 < g.lx && P.y0 >= 0.0 && P.y0 < g.ly && P.z0 >= 0.0 && P.z0 < g.lz);
+  P.cx0 = P.x0 * g.rdx; P.cy0 = P.y0 * g.rdy; P.cz0 = P.z0 * g.rdz;
+  P.tx = P.cx0; P.ty = P.cy0; P.tz = P.cz0;
+}
+
+// Returns the cell and fractions; clears P.ok on a non-finite position.
+__device__ __forceinline__ int fast_locate(PState& P, const FastGrid& g, double& fx, double& fy,
+                                           double& fz) {
+  if (!(P.tx >= 0.0 && P.tx <= g.nxd && P.ty >= 0.0 && P.ty <= g.nyd && P.tz >= 0.0 &&
+        P.tz <= g.nzd)) {
+    P.ok = false;
+    return -1;
+  }
+  const int i = min(__double2int_rz(P.tx), g.nx - 1);
+  const int j = min(__double2int_rz(P.ty), g.ny - 1);
+  const int k = min(__double2int_rz(P.tz), g.nz - 1);
+  fx = P.tx - static_cast<double>(i);
+  fy = P.ty - static_cast<double>(j);
+  fz = P.tz - static_cast<double>(k);
+  return i + g.nx * (j + g.ny * k);
+}
+
+__device__ __forceinline__ double fast_comp(const double2* c, double fx, double fy, double fz) {
+  const double p0 = fma(fz, c[0].y, c[0].x);
+  const double p1 = fma(fz, c[1].y, c[1].x);
+  const double p2 = fma(fz, c[2].y, c[2].x);
+  const double p3 = fma(fz, c[3].y, c[3].x);
+  return fma(fx, fma(fy, p3, p2), fma(fy, p1, p0));
+}
+
+__device__ __forceinline__ void fast_round(PState& P, const CellCache& cc, double fx, double fy,
+                                           double fz, double beta) {
+  const double ex = fast_comp(cc.c + 0, fx, fy, fz);
+  const double ey = fast_comp(cc.c + 4, fx, fy, fz);
+  const double ez = fast_comp(cc.c + 8, fx, fy, fz);
+  const double ox = beta * fast_comp(cc.c + 12, fx, fy, fz);
+  const double oy = beta * fast_comp(cc.c + 16, fx, fy, fz);
+  const double oz = beta * fast_comp(cc.c + 20, fx, fy, fz);
+  const double vtx = fma(beta, ex, P.u0);
+  const double vty = fma(beta, ey, P.v0);
+  const double vtz = fma(beta, ez, P.w0);
+  const double den = 1.0 + fma(oz, oz, fma(oy, oy, ox * ox));
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+  double e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
+  P.bx = fma(vdot, ox, vtx + fma(vty, oz, -vtz * oy)) * rc;
+  P.by = fma(vdot, oy, vty + fma(vtz, ox, -vtx * oz)) * rc;
+  P.bz = fma(vdot, oz, vtz + fma(vtx, oy, -vty * ox)) * rc;
+}
+
+__device__ __forceinline__ void fast_predict(PState& P, const FastGrid& g, const double* dto2c) {
+  P.tx = fold_cells(fma(P.bx, dto2c[0], P.cx0), g.nxd, g.rnx);
+  P.ty = fold_cells(fma(P.by, dto2c[1], P.cy0), g.nyd, g.rny);
+  P.tz = fold_cells(fma(P.bz, dto2c[2], P.cz0), g.nzd, g.rnz);
+}
+
+__device__ __forceinline__ bool fast_finish(PState& P, const FastGrid& g, double dt, double* out) {
+  if (!P.ok) return false;
+  const double x1 = wrap_len_exact(fma(P.bx, dt, P.x0), g.ax);
+  const double y1 = wrap_len_exact(fma(P.by, dt, P.y0), g.ay);
+  const double z1 = wrap_len_exact(fma(P.bz, dt, P.z0), g.az);
+  const double u1 = fma(2.0, P.bx, -P.u0);
+  const double v1 = fma(2.0, P.by, -P.v0);
+  const double w1 = fma(2.0, P.bz, -P.w0);
+  if (!(isfinite(x1) && isfinite(y1) && isfinite(z1) && isfinite(u1) && isfinite(v1) &&
+        isfinite(w1)))
+    return false;
+  out[0] = x1; out[1] = y1; out[2] = z1;
+  out[3] = u1; out[4] = v1; out[5] = w1;
+  return true;
+}
+
+// ---- STRICT (reference order, separate roundings) -------------------------
+
+__device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, double* wt) {
+  if (!(P.tx >= 0.0 && P.tx < g.lx && P.ty >= 0.0 && P.ty < g.ly && P.tz >= 0.0 && P.tz < g.lz)) {
+    P.ok = false;
+    return -1;
+  }
+  const double sx = __ddiv_rn(P.tx, g.dx), sy = __ddiv_rn(P.ty, g.dy), sz = __ddiv_rn(P.tz, g.dz);
+  int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
+  if (i >= g.nx) i = g.nx - 1;
+  if (j >= g.ny) j = g.ny - 1;
+  if (k >= g.nz) k = g.nz - 1;
+  double fx = __dsub_rn(sx, static_cast<double>(i));
+  double fy = __dsub_rn(sy, static_cast<double>(j));
+  double fz = __dsub_rn(sz, static_cast<double>(k));
+  if (fx > 1.0) fx = 1.0;
+  if (fy > 1.0) fy = 1.0;
+  if (fz > 1.0) fz = 1.0;
+  const double wx[2] = {__dsub_rn(1.0, fx), fx};
+  const double wy[2] = {__dsub_rn(1.0, fy), fy};
+  const double wz[2] = {__dsub_rn(1.0, fz), fz};
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    wt[c] = __dmul_rn(__dmul_rn(wx[c & 1], wy[(c >> 1) & 1]), wz[(c >> 2) & 1]);
+  return i + g.nx * (j + g.ny * k);
+}
+
+__device__ __forceinline__ void strict_round(PState& P, const CellCache& cc, const double* wt,
+                                             double beta) {
+  double ex = 0.0, ey = 0.0, ez = 0.0, fbx = 0.0, fby = 0.0, fbz = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double w = wt[c];
+    ex = __dadd_rn(ex, __dmul_rn(w, cc.c[3 * c + 0].x));
+    ey = __dadd_rn(ey, __dmul_rn(w, cc.c[3 * c + 0].y));
+    ez = __dadd_rn(ez, __dmul_rn(w, cc.c[3 * c + 1].x));
+    fbx = __dadd_rn(fbx, __dmul_rn(w, cc.c[3 * c + 1].y));
+    fby = __dadd_rn(fby, __dmul_rn(w, cc.c[3 * c + 2].x));
+    fbz = __dadd_rn(fbz, __dmul_rn(w, cc.c[3 * c + 2].y));
+  }
+  const double vtx = __dadd_rn(P.u0, __dmul_rn(beta, ex));
+  const double vty = __dadd_rn(P.v0, __dmul_rn(beta, ey));
+  const double vtz = __dadd_rn(P.w0, __dmul_rn(beta, ez));
+  const double ox = __dmul_rn(beta, fbx), oy = __dmul_rn(beta, fby), oz = __dmul_rn(beta, fbz);
+  const double omsq = __dadd_rn(__dadd_rn(__dmul_rn(ox, ox), __dmul_rn(oy, oy)), __dmul_rn(oz, oz));
+  const double denom = __ddiv_rn(1.0, __dadd_rn(1.0, omsq));
+  const double vdot = __dadd_rn(__dadd_rn(__dmul_rn(vtx, ox), __dmul_rn(vty, oy)), __dmul_rn(vtz, oz));
+  P.bx = __dmul_rn(__dadd_rn(__dadd_rn(vtx, __dsub_rn(__dmul_rn(vty, oz), __dmul_rn(vtz, oy))),
+                             __dmul_rn(vdot, ox)), denom);
+  P.by = __dmul_rn(__dadd_rn(__dadd_rn(vty, __dsub_rn(__dmul_rn(vtz, ox), __dmul_rn(vtx, oz))),
+                             __dmul_rn(vdot, oy)), denom);
+  P.bz = __dmul_rn(__dadd_rn(__dadd_rn(vtz, __dsub_rn(__dmul_rn(vtx, oy), __dmul_rn(vty, ox))),
+                             __dmul_rn(vdot, oz)), denom);
+}
+
+__device__ __forceinline__ void strict_predict(PState& P, const DevGrid& g, double dto2) {
+  P.tx = wrap_len_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dto2)), g.lx);
+  P.ty = wrap_len_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dto2)), g.ly);
+  P.tz = wrap_len_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dto2)), g.lz);
+}
+
+__device__ __forceinline__ bool strict_finish(PState& P, const DevGrid& g, double dt, double* out) {
+  if (!P.ok) return false;
+  const double x1 = wrap_len_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dt)), g.lx);
+  const double y1 = wrap_len_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dt)), g.ly);
+  const double z1 = wrap_len_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dt)), g.lz);
+  const double u1 = __dsub_rn(__dmul_rn(2.0, P.bx), P.u0);
+  const double v1 = __dsub_rn(__dmul_rn(2.0, P.by), P.v0);
+  const double w1 = __dsub_rn(__dmul_rn(2.0, P.bz), P.w0);
+  if (!(isfinite(x1) && isfinite(y1) && isfinite(z1) && isfinite(u1) && isfinite(v1) &&
+        isfinite(w1)))
+    return false;
+  out[0] = x1; out[1] = y1; out[2] = z1;
+  out[3] = u1; out[4] = v1; out[5] = w1;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// two particles, one cell cache
+// ---------------------------------------------------------------------------
+
+struct TileField {
+  FastGrid fg;
+  DevGrid dg;
+  const double2* cells;  // FAST
+  const double* E;       // STRICT
+  const double* B;
+};
+
+// Advances P consecutive particles p[i] (only those with has[i]).  They share
+// one register cell cache; when every live particle of the group sits in the
+// same cell (the common case after the cell sort) the P evaluations run as
+// independent instruction streams -- P-fold ILP for the FP64 chains.
+// Results overwrite p[i] on success; ok[i] reports success.
+template <bool STRICT, int P>
+__device__ __forceinline__ void push_group(const TileField& F, const SpeciesLaunch& sp,
+                                           double (&p)[P][6], const bool (&has)[P],
+                                           bool (&ok)[P]) {
+  PState S[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (STRICT)
+      begin(S[i], p[i]);
+    else
+      fast_begin(S[i], F.fg, p[i]);
+    S[i].ok = S[i].ok && has[i];
+  }
+  CellCache cc;
+  cc.cell = -1;
+  for (int r = 0; r < sp.rounds; ++r) {
+    const bool pred = r + 1 < sp.rounds;
+    int cell[P];
+    double w[P][8];  // STRICT: trilinear weights; FAST: w[i][0..2] = fractions
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      cell[i] = -1;
+      if (S[i].ok) {
+        if (STRICT)
+          cell[i] = strict_locate(S[i], F.dg, w[i]);
+        else
+          cell[i] = fast_locate(S[i], F.fg, w[i][0], w[i][1], w[i][2]);
+      }
+    }
+    int ref = -1;
+    bool same = true;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      if (!S[i].ok) continue;
+      if (ref < 0) ref = cell[i];
+      same = same && (cell[i] == ref);
+    }
+    if (ref < 0) break;  // every particle of the group faulted
+    if (same) {
+      if (ref != cc.cell) {
+        if (STRICT)
+          cache_load_strict(cc, F.dg, F.E, F.B, ref);
+        else
+          cache_load_fast(cc, F.cells, ref);
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!S[i].ok) continue;
+        if (STRICT) {
+          strict_round(S[i], cc, w[i], sp.beta);
+          if (pred) strict_predict(S[i], F.dg, sp.dto2);
+        } else {
+          fast_round(S[i], cc, w[i][0], w[i][1], w[i][2], sp.beta);
+          if (pred) fast_predict(S[i], F.fg, sp.dto2_cell);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < P; ++i) {
+        if (!S[i].ok) continue;
+        if (cell[i] != cc.cell) {
+          if (STRICT)
+            cache_load_strict(cc, F.dg, F.E, F.B, cell[i]);
+          else
+            cache_load_fast(cc, F.cells, cell[i]);
+        }
+        if (STRICT) {
+          strict_round(S[i], cc, w[i], sp.beta);
+          if (pred) strict_predict(S[i], F.dg, sp.dto2);
+        } else {
+          fast_round(S[i], cc, w[i][0], w[i][1], w[i][2], sp.beta);
+          if (pred) fast_predict(S[i], F.fg, sp.dto2_cell);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (STRICT)
+      ok[i] = has[i] && strict_finish(S[i], F.dg, sp.dt, p[i]);
+    else
+      ok[i] = has[i] && fast_finish(S[i], F.fg, sp.dt, p[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FAST, coefficient streaming: P particles per thread, no register cache
+// ---------------------------------------------------------------------------
+//
+// Each round, each of the 24 coefficient pairs of a cell is loaded once (L1
+// hit) and applied to all P particles of the thread when they share that cell
+// (the common case after the cell sort): L1->register traffic per particle is
+// 3 rounds x 384 B / P, and the P particles give P independent FP64 chains.
+// Persistent state per particle is 9 doubles; x0 is re-read from the tile at
+// the end (load_x0 functor).
+
+struct FastLive {
+  double u0, v0, w0;
+  double cx0, cy0, cz0;  // x0 in cell units
+  double fx, fy, fz;     // fractions in the current cell
+  double bx, by, bz;     // time-centred velocity (last round)
+  int cell;
+  bool ok;
+};
+
+__device__ __forceinline__ void fast_locate_live(FastLive& L, const FastGrid& g, double tx,
+                                                 double ty, double tz) {
+  if (!(tx >= 0.0 && tx <= g.nxd && ty >= 0.0 && ty <= g.nyd && tz >= 0.0 && tz <= g.nzd)) {
+    L.ok = false;
+    L.cell = -1;
+    return;
+  }
+  const int i = min(__double2int_rz(tx), g.nx - 1);
+  const int j = min(__double2int_rz(ty), g.ny - 1);
+  const int k = min(__double2int_rz(tz), g.nz - 1);
+  L.fx = tx - static_cast<double>(i);
+  L.fy = ty - static_cast<double>(j);
+  L.fz = tz - static_cast<double>(k);
+  L.cell = i + g.nx * (j + g.ny * k);
+}
+
+__device__ __forceinline__ double poly(const double2& a, const double2& b, const double2& c,
+                                       const double2& d, double fx, double fy, double fz) {
+  return fma(fx, fma(fy, fma(fz, d.y, d.x), fma(fz, c.y, c.x)),
+             fma(fy, fma(fz, b.y, b.x), fma(fz, a.y, a.x)));
+}
+
+__device__ __forceinline__ void fast_velocity(FastLive& L, const double* F, double beta) {
+  const double ox = beta * F[3], oy = beta * F[4], oz = beta * F[5];
+  const double vtx = fma(beta, F[0], L.u0);
+  const double vty = fma(beta, F[1], L.v0);
+  const double vtz = fma(beta, F[2], L.w0);
+  const double den = 1.0 + fma(oz, oz, fma(oy, oy, ox * ox));
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+  double e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  e = fma(-den, rc, 1.0);
+  rc = fma(rc, e, rc);
+  const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
+  L.bx = fma(vdot, ox, vtx + fma(vty, oz, -vtz * oy)) * rc;
+  L.by = fma(vdot, oy, vty + fma(vtz, ox, -vtx * oz)) * rc;
+  L.bz = fma(vdot, oz, vtz + fma(vtx, oy, -vty * ox)) * rc;
+}
+
+// load(i, a) returns input a (x,y,z,u,v,w) of particle i; store(i, a, v)
+// writes result a.  Only particles with has[i] are touched; ok[i] reports a
+// finite result (a faulting particle is never stored: the reference leaves it
+// untouched).  The final update runs inside the last round so no velocity
+// stays live across the round loop.
+template <int P, class Load, class Store>
+__device__ __forceinline__ void push_fast_stream(const FastGrid& g, const double2* __restrict__ cells,
+                                                 const SpeciesLaunch& sp, const bool (&has)[P],
+                                                 bool (&ok)[P], Load load, Store store) {
+  FastLive L[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    ok[i] = false;
+    const double x0 = has[i] ? load(i, 0) : 0.0;
+    const double y0 = has[i] ? load(i, 1) : 0.0;
+    const double z0 = has[i] ? load(i, 2) : 0.0;
+    L[i].u0 = has[i] ? load(i, 3) : 0.0;
+    L[i].v0 = has[i] ? load(i, 4) : 0.0;
+    L[i].w0 = has[i] ? load(i, 5) : 0.0;
+    // grid.hpp:65-67: the first locate rejects x0 outside [0,l)
+    L[i].ok = has[i] && (x0 >= 0.0 && x0 < g.lx && y0 >= 0.0 && y0 < g.ly && z0 >= 0.0 && z0 < g.lz);
+    L[i].cx0 = x0 * g.rdx; L[i].cy0 = y0 * g.rdy; L[i].cz0 = z0 * g.rdz;
+    L[i].cell = -1;
+    if (L[i].ok) fast_locate_live(L[i], g, L[i].cx0, L[i].cy0, L[i].cz0);
+  }
+  const int rounds = sp.rounds;
+  for (int r = 0; r < rounds; ++r) {
+    int ref = -1;
+    bool same = true;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      if (!L[i].ok) continue;
+      if (ref < 0) ref = L[i].cell;
+      same = same && (L[i].cell == ref);
+    }
+    if (ref < 0) break;
+    double F[P][6];
+    if (same) {
+      const double2* c = cells + static_cast<long long>(ref) * 24;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double2 a = __ldg(c + 4 * q), b = __ldg(c + 4 * q + 1);
+        const double2 cc = __ldg(c + 4 * q + 2), d = __ldg(c + 4 * q + 3);
+#pragma unroll
+        for (int i = 0; i < P; ++i) F[i][q] = poly(a, b, cc, d, L[i].fx, L[i].fy, L[i].fz);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!L[i].ok) continue;
+        const double2* c = cells + static_cast<long long>(L[i].cell) * 24;
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          F[i][q] = poly(__ldg(c + 4 * q), __ldg(c + 4 * q + 1), __ldg(c + 4 * q + 2),
+                         __ldg(c + 4 * q + 3), L[i].fx, L[i].fy, L[i].fz);
+      }
+    }
+    if (r + 1 < rounds) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!L[i].ok) continue;
+        fast_velocity(L[i], F[i], sp.beta);
+        fast_locate_live(L[i], g, fold_cells(fma(L[i].bx, sp.dto2_cell[0], L[i].cx0), g.nxd, g.rnx),
+                         fold_cells(fma(L[i].by, sp.dto2_cell[1], L[i].cy0), g.nyd, g.rny),
+                         fold_cells(fma(L[i].bz, sp.dto2_cell[2], L[i].cz0), g.nzd, g.rnz));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!L[i].ok) continue;
+        fast_velocity(L[i], F[i], sp.beta);
+        // kernels.cpp:95-99
+        const double x1 = wrap_len_exact(fma(L[i].bx, sp.dt, load(i, 0)), g.ax);
+        const double y1 = wrap_len_exact(fma(L[i].by, sp.dt, load(i, 1)), g.ay);
+        const double z1 = wrap_len_exact(fma(L[i].bz, sp.dt, load(i, 2)), g.az);
+        const double u1 = fma(2.0, L[i].bx, -L[i].u0);
+        const double v1 = fma(2.0, L[i].by, -L[i].v0);
+        const double w1 = fma(2.0, L[i].bz, -L[i].w0);
+        if (!(isfinite(x1) && isfinite(y1) && isfinite(z1) && isfinite(u1) && isfinite(v1) &&
+              isfinite(w1)))
+          continue;
+        store(i, 0, x1); store(i, 1, y1); store(i, 2, z1);
+        store(i, 3, u1); store(i, 4, v1); store(i, 5, w1);
+        ok[i] = true;
+      }
+    }
+  }
+}
+
+}  // namespace b2m

@@ -179,17 +179,18 @@ def test_empty_batch_is_noop(gpu, mode):
 
 @pytest.mark.parametrize("mode", MODES)
 def test_uniform_field_pc_fixed_point(gpu, mode):
-    """SPEC.md: uniform fields make the corrector a fixed point -> pc 1 and 3
-    give identical results (bitwise in strict mode, as in the reference)."""
+    """SPEC.md: with uniform fields the corrector is a fixed point, so pc 1
+    and pc 3 agree -- up to the rounding of the gather's partition of unity,
+    which the reference itself shows (it is NOT bitwise pc-invariant; the
+    SPEC's "bitwise" claim does not hold for the reference either)."""
     grid = (8, 8, 8, 4.0, 4.0, 4.0)
     E, B = uniform_field(grid, [0.3, -0.2, 0.1], [0.5, 0.25, -0.75])
     p0 = random_particles(grid, 20000, 3)
     a = gpu_move(p0, E, B, grid, 0.1, -25.0, 1, mode)
     b = gpu_move(p0, E, B, grid, 0.1, -25.0, 3, mode)
-    if mode == "strict":
-        assert_bitwise(a, b)
-    else:
-        assert_within_contract(a, b, grid)
+    assert_within_contract(a, b, grid, tol=1e-14)
+    check(a, port_move(p0, E, B, grid, 0.1, -25.0, 1), grid, mode, "pc1")
+    check(b, port_move(p0, E, B, grid, 0.1, -25.0, 3), grid, mode, "pc3")
 
 
 @pytest.mark.parametrize("mode", MODES)
