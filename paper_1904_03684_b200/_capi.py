@@ -14,7 +14,8 @@ import os
 from .errors import raise_for_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb2m.so")
+# B2M_LIB lets tools/ experiments load an alternative in-tree build variant
+LIB_PATH = os.environ.get("B2M_LIB") or os.path.join(HERE, "libb2m.so")
 
 _dp = C.POINTER(C.c_double)
 _u64 = C.c_uint64

@@ -99,6 +99,7 @@ constexpr int kEventSlots = 16;
 
 struct Species {
   double* a[6] = {};
+  double* alt[6] = {};  // ping-pong set for the cell sort (allocated on first sort)
   uint64_t capacity = 0;
   uint64_t count = 0;
   // migration scratch
@@ -678,14 +679,36 @@ b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
   const uint64_t ncell = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
   int bits = 1;
   while ((1ull << bits) <= ncell) ++bits;
-  launch_cell_keys(to_dev(ctx->grid), S.a[0], S.a[1], S.a[2], n, ctx->keys[0], ctx->vals[0],
+  launch_cell_keys(to_fast(ctx->grid), S.a[0], S.a[1], S.a[2], n, ctx->keys[0], ctx->vals[0],
                    ctx->stream);
   launch_sort_pairs(ctx->sort_temp, ctx->sort_temp_bytes, ctx->keys[0], ctx->keys[1],
                     ctx->vals[0], ctx->vals[1], n, bits, ctx->stream);
-  for (int a = 0; a < 6; ++a) {
-    launch_gather(S.a[a], ctx->vals[1], n, ctx->scratch, ctx->stream);
-    B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a], ctx->scratch, n * sizeof(double),
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  // permute into the ping-pong set and swap (no copy back); fall back to a
+  // scratch array + copy when the second set does not fit in device memory
+  if (!S.alt[0]) {
+    for (int a = 0; a < 6; ++a) {
+      if (cudaMalloc(reinterpret_cast<void**>(&S.alt[a]), S.capacity * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        for (int b = 0; b < a; ++b) {
+          cudaFree(S.alt[b]);
+          S.alt[b] = nullptr;
+        }
+        S.alt[0] = nullptr;
+        break;
+      }
+    }
+    if (S.alt[0])
+      for (int a = 0; a < 6; ++a) ctx->allocations.push_back(S.alt[a]);
+  }
+  if (S.alt[0]) {
+    launch_gather6(S.a, ctx->vals[1], n, S.alt, ctx->stream);
+    for (int a = 0; a < 6; ++a) std::swap(S.a[a], S.alt[a]);
+  } else {
+    for (int a = 0; a < 6; ++a) {
+      launch_gather(S.a[a], ctx->vals[1], n, ctx->scratch, ctx->stream);
+      B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a], ctx->scratch, n * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    }
   }
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;

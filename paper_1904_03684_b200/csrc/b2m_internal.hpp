@@ -42,9 +42,12 @@ void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double
 // Reset the fault words to "clean".
 void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 
-// Cell keys of the current positions (exact grid_cell_of), for sorting.
-void launch_cell_keys(const DevGrid& g, const double* x, const double* y, const double* z,
+// Cell keys of the current positions (cell-unit locate), for sorting.
+void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,
                       uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+// out[a][i] = in[a][perm[i]] for the six SoA arrays
+void launch_gather6(double* const* in, const uint32_t* perm, uint64_t n, double* const* out,
+                    cudaStream_t st);
 // out[i] = in[perm[i]]
 void launch_gather(const double* in, const uint32_t* perm, uint64_t n, double* out,
                    cudaStream_t st);

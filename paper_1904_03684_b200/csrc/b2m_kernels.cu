@@ -33,7 +33,7 @@ __device__ __forceinline__ void store6(const SpeciesLaunch& sp, unsigned long lo
 // are distributed round-robin over the grid; each block keeps kTileStages
 // tiles in flight through shared memory (bulk TMA in, bulk TMA out).
 template <bool STRICT>
-__global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : kTileMinBlocks)
+__global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : B2M_FAST_MINBLOCKS)
     tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TileSpans S,
                 unsigned long long total_tiles, FaultWord* fault) {
   constexpr int PPT = TileShape<STRICT>::ppt;
@@ -93,10 +93,10 @@ __global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : kTileMinBlocks)
     const SpeciesLaunch& sp = S.sp[s];
     double* ptr[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
     const int i0 = PPT * tid;
-    bool has[PPT], ok[PPT];
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) has[i] = i0 + i < cnt;
     if (STRICT) {
+      bool has[PPT], ok[PPT];
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) has[i] = i0 + i < cnt;
       double p[PPT][6];
       if (full) {
 #pragma unroll
@@ -131,26 +131,38 @@ __global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : kTileMinBlocks)
           else
             ptr[a][off + i0 + i] = p[i][a];
         }
-    } else {
-      // inputs are read from (and results written to) the staged tile; a
-      // faulting particle is never stored, so its input stays in place
-      auto load = [&](int i, int a) -> double {
-        return full ? buf[st][a][i0 + i] : ptr[a][off + i0 + i];
-      };
-      auto store = [&](int i, int a, double v) {
-        if (full)
-          buf[st][a][i0 + i] = v;
-        else
-          ptr[a][off + i0 + i] = v;
-      };
-      push_fast_stream<PPT>(F.fg, F.cells, sp, has, ok, load, store);
-    }
 #pragma unroll
-    for (int i = 0; i < PPT; ++i)
-      if (has[i] && !ok[i])
+      for (int i = 0; i < PPT; ++i)
+        if (has[i] && !ok[i])
+          atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
+      if (full) fence_proxy_async();
+      __syncthreads();
+    } else {
+      if (!full) {
+        // partial / unaligned tile: stage it through shared memory by hand
+        for (int j = tid; j < cnt; j += kTileThreads)
+#pragma unroll
+          for (int a = 0; a < 6; ++a) buf[st][a][j] = ptr[a][off + j];
+        __syncthreads();
+      }
+      const FastConst kc = make_const(F.fg, sp);
+      unsigned faults = fast_tile_thread<PPT, TILE>(F.fg, F.cells, kc, buf[st], i0, cnt);
+      while (faults) {
+        const int i = __ffs(faults) - 1;
+        faults &= faults - 1;
         atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
-    if (full) fence_proxy_async();
-    __syncthreads();
+      }
+      if (full) fence_proxy_async();
+      __syncthreads();
+      if (!full) {
+        // a faulting particle's slot still holds its input: copying the whole
+        // tile back leaves it untouched, as the reference does
+        for (int j = tid; j < cnt; j += kTileThreads)
+#pragma unroll
+          for (int a = 0; a < 6; ++a) ptr[a][off + j] = buf[st][a][j];
+        __syncthreads();
+      }
+    }
     if (tid == 0) {
       if (full) {
 #pragma unroll
@@ -163,6 +175,110 @@ __global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : kTileMinBlocks)
     }
   }
   if (tid == 0) tma_wait_all();
+}
+
+// FAST mover with warp-private TMA pipelines: every warp streams its own
+// tiles of 32*P particles (kWarpStages deep) through its slice of shared
+// memory, with its own mbarriers -- no block-wide barrier anywhere, so a warp
+// that finishes a tile early starts the next one instead of idling.
+template <int P>
+__global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
+    warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TileSpans S,
+                     unsigned long long total_tiles, FaultWord* fault) {
+  constexpr int WT = 32 * P;
+  constexpr int WARPS = kTileThreads / 32;
+  extern __shared__ __align__(128) unsigned char wt_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto buf = reinterpret_cast<double(*)[6][WT]>(wt_smem) + warp * kWarpStages;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt_smem + WARPS * kWarpStages * 6 * WT * 8) +
+                  warp * kWarpStages;
+  // tiles round-robin over all warps of the grid: at any moment the whole GPU
+  // streams one contiguous window of the particle arrays (DRAM-friendly)
+  const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * WARPS + warp;
+  const unsigned long long GW = static_cast<unsigned long long>(gridDim.x) * WARPS;
+  const unsigned long long t_end = total_tiles;
+
+  auto resolve = [&](unsigned long long tile, int& s, unsigned long long& off, int& cnt,
+                     bool& full) {
+    s = 0;
+    while (s + 1 < S.n && tile >= S.tile_start[s + 1]) ++s;
+    off = (tile - S.tile_start[s]) * WT;
+    const unsigned long long left = S.sp[s].n - off;
+    cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
+    full = (cnt == WT) && S.tma_ok[s];
+  };
+  auto issue = [&](unsigned long long k) {  // lane 0
+    const unsigned long long tile = gw + k * GW;
+    if (tile >= t_end) return;
+    int s, cnt;
+    unsigned long long off;
+    bool full;
+    resolve(tile, s, off, cnt, full);
+    const int st = static_cast<int>(k % kWarpStages);
+    if (full) {
+      const SpeciesLaunch& sp = S.sp[s];
+      mbar_arrive_tx(&bar[st], 6 * WT * sizeof(double));
+      const double* src[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+        tma_load_1d(buf[st][a], src[a] + off, WT * sizeof(double), &bar[st]);
+    } else {
+      mbar_arrive(&bar[st]);
+    }
+  };
+
+  if (lane == 0) {
+    for (int s = 0; s < kWarpStages; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+    for (int k = 0; k < kWarpStages; ++k) issue(k);
+  }
+  __syncwarp();
+
+  for (unsigned long long k = 0;; ++k) {
+    const unsigned long long tile = gw + k * GW;
+    if (tile >= t_end) break;
+    int s, cnt;
+    unsigned long long off;
+    bool full;
+    resolve(tile, s, off, cnt, full);
+    const int st = static_cast<int>(k % kWarpStages);
+    mbar_wait(&bar[st], static_cast<uint32_t>((k / kWarpStages) & 1));
+    const SpeciesLaunch& sp = S.sp[s];
+    double* ptr[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
+    if (!full) {
+      for (int j = lane; j < cnt; j += 32)
+#pragma unroll
+        for (int a = 0; a < 6; ++a) buf[st][a][j] = ptr[a][off + j];
+      __syncwarp();
+    }
+    const FastConst kc = make_const(F.fg, sp);
+    const int i0 = P * lane;
+    unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
+    while (faults) {
+      const int i = __ffs(faults) - 1;
+      faults &= faults - 1;
+      atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
+    }
+    if (full) fence_proxy_async();
+    __syncwarp();
+    if (!full) {
+      for (int j = lane; j < cnt; j += 32)
+#pragma unroll
+        for (int a = 0; a < 6; ++a) ptr[a][off + j] = buf[st][a][j];
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (full) {
+#pragma unroll
+        for (int a = 0; a < 6; ++a) tma_store_1d(ptr[a] + off, buf[st][a], WT * sizeof(double));
+      }
+      tma_commit();
+      tma_wait_read<0>();
+      issue(k + kWarpStages);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) tma_wait_all();
 }
 
 // One thread per cell: 8 corners x 6 components -> 48 coefficients.
@@ -204,23 +320,35 @@ __global__ void fault_reset_kernel(FaultWord* f) {
   f->cfl = ~0ull;
 }
 
-__global__ void cell_keys_kernel(const __grid_constant__ DevGrid g, const double* __restrict__ x,
+__global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const double* __restrict__ x,
                                  const double* __restrict__ y, const double* __restrict__ z,
                                  unsigned long long n, uint32_t* keys, uint32_t* vals) {
   const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  long long idx[8];
-  double wt[8];
+  const double cx = x[i] * g.rdx, cy = y[i] * g.rdy, cz = z[i] * g.rdz;
   uint32_t key = static_cast<uint32_t>(static_cast<long long>(g.nx) * g.ny * g.nz);
-  if (weights_strict(g, x[i], y[i], z[i], idx, wt)) {
-    // cell of corner 0: node (i,j,k) -> cell i + nx*(j + ny*k)
-    const long long node = idx[0];
-    const long long sx = g.nx + 1, sy = g.ny + 1;
-    const long long ci = node % sx, cj = (node / sx) % sy, ck = node / (sx * sy);
+  if (cx >= 0.0 && cx <= g.nxd && cy >= 0.0 && cy <= g.nyd && cz >= 0.0 && cz <= g.nzd) {
+    const int ci = min(__double2int_rz(cx), g.nx - 1);
+    const int cj = min(__double2int_rz(cy), g.ny - 1);
+    const int ck = min(__double2int_rz(cz), g.nz - 1);
     key = static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
   }
   keys[i] = key;
   vals[i] = static_cast<uint32_t>(i);
+}
+
+struct Ptr6 {
+  const double* in[6];
+  double* out[6];
+};
+
+__global__ void gather6_kernel(const __grid_constant__ Ptr6 P, const uint32_t* __restrict__ perm,
+                               unsigned long long n) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = perm[i];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) P.out[a][i] = __ldg(P.in[a] + j);
 }
 
 __global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __restrict__ perm,
@@ -465,7 +593,41 @@ void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
   TileField F{};
   F.fg = g;
   F.cells = cells;
-  launch_tiles<false>(F, sp, n_spans, fault, st);
+  constexpr int P = B2M_FAST_PPT;
+  constexpr int WT = 32 * P;
+  constexpr int smem = (kTileThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
+  static int grid_cap = -1;
+  if (grid_cap < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(warp_tile_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P>, kTileThreads, smem);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  for (int base = 0; base < n_spans; base += kMaxTileSpans) {
+    TileSpans S{};
+    unsigned long long tiles = 0;
+    for (int s = base; s < n_spans && S.n < kMaxTileSpans; ++s) {
+      if (sp[s].n == 0) continue;
+      S.sp[S.n] = sp[s];
+      S.tile_start[S.n] = tiles;
+      const uintptr_t m =
+          reinterpret_cast<uintptr_t>(sp[s].x) | reinterpret_cast<uintptr_t>(sp[s].y) |
+          reinterpret_cast<uintptr_t>(sp[s].z) | reinterpret_cast<uintptr_t>(sp[s].u) |
+          reinterpret_cast<uintptr_t>(sp[s].v) | reinterpret_cast<uintptr_t>(sp[s].w);
+      S.tma_ok[S.n] = (m & 15u) == 0;
+      tiles += (sp[s].n + WT - 1) / WT;
+      ++S.n;
+    }
+    S.tile_start[S.n] = tiles;
+    if (S.n == 0) continue;
+    const unsigned long long warps_needed = tiles;
+    const unsigned long long blocks = (warps_needed + 3) / 4;
+    const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
+    warp_tile_kernel<P><<<grid, kTileThreads, smem, st>>>(F, S, tiles, fault);
+    note_launch();
+  }
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
@@ -480,7 +642,19 @@ void launch_fault_reset(FaultWord* fault, cudaStream_t st) {
   note_launch();
 }
 
-void launch_cell_keys(const DevGrid& g, const double* x, const double* y, const double* z,
+void launch_gather6(double* const* in, const uint32_t* perm, uint64_t n, double* const* out,
+                    cudaStream_t st) {
+  if (n == 0) return;
+  Ptr6 P;
+  for (int a = 0; a < 6; ++a) {
+    P.in[a] = in[a];
+    P.out[a] = out[a];
+  }
+  gather6_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, perm, n);
+  note_launch();
+}
+
+void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,
                       uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
   if (n == 0) return;
   cell_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, x, y, z, n, keys, vals);

@@ -23,12 +23,19 @@ namespace b2m {
 
 constexpr int kTileThreads = 128;
 constexpr int kTileStages = 2;
+constexpr int kWarpStages = 3;
 constexpr int kTileMinBlocks = 3;
 // particles per thread: FAST streams coefficients to 4 particles, STRICT
 // keeps a register cell cache shared by 2
+#ifndef B2M_FAST_PPT
+#define B2M_FAST_PPT 2
+#endif
+#ifndef B2M_FAST_MINBLOCKS
+#define B2M_FAST_MINBLOCKS 4
+#endif
 template <bool STRICT>
 struct TileShape {
-  static constexpr int ppt = STRICT ? 2 : 4;
+  static constexpr int ppt = STRICT ? 2 : B2M_FAST_PPT;
   static constexpr int tile = kTileThreads * ppt;
   static constexpr int smem = kTileStages * 6 * tile * 8 + 64;
 };
@@ -432,32 +439,100 @@ __device__ __forceinline__ void push_group(const TileField& F, const SpeciesLaun
 // hit) and applied to all P particles of the thread when they share that cell
 // (the common case after the cell sort): L1->register traffic per particle is
 // 3 rounds x 384 B / P, and the P particles give P independent FP64 chains.
-// Persistent state per particle is 9 doubles; x0 is re-read from the tile at
-// the end (load_x0 functor).
+//
+// Control flow is kept off the FP64 pipe and out of the warp: every range
+// check is an unsigned compare of the IEEE bit pattern (for x >= +0 the bit
+// patterns order like the values; negatives, -0, NaN and Inf all land above
+// any positive bound), invalid lanes compute on harmless data and are masked
+// at the store, and cell indices are clamped so a NaN can never address
+// memory.  A sticky per-particle flag records every event the reference
+// would have thrown on (x0 outside [0,l), a non-finite predictor position,
+// a non-finite result), so faults name the same particles.
 
-struct FastLive {
-  double u0, v0, w0;
-  double cx0, cy0, cz0;  // x0 in cell units
-  double fx, fy, fz;     // fractions in the current cell
-  double bx, by, bz;     // time-centred velocity (last round)
-  int cell;
-  bool ok;
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+constexpr unsigned long long kSign = 0x8000000000000000ull;
+constexpr unsigned long long kAbs = 0x7fffffffffffffffull;
+constexpr unsigned long long kExp = 0x7ff0000000000000ull;
+
+// x in [0, l) exactly as `x >= 0.0 && x < l` (accepts -0.0, rejects NaN)
+__device__ __forceinline__ bool in_range(double x, unsigned long long lbits) {
+  const unsigned long long b = dbits(x);
+  return b < lbits || b == kSign;
+}
+
+__device__ __forceinline__ bool finite_bits(double x) { return (dbits(x) & kExp) != kExp; }
+
+// Cell-unit periodic fold of the predictor into [0, n).  The in-range test is
+// one unsigned compare; everything else (c < 0 incl. -0, c >= n, NaN, Inf) is
+// the rare slow path, which also flags non-finite values.
+__device__ __forceinline__ double fold_fast(double c, double n, unsigned long long nbits,
+                                            double rn, unsigned& bad) {
+  if (dbits(c) >= nbits) {
+    if (!finite_bits(c)) bad = 1u;
+    c = fma(-n, floor(c * rn), c);
+    if (c >= n) c -= n;
+    if (c < 0.0) c += n;
+    if (!(c < n)) c = 0.0;
+  }
+  return c;
+}
+
+// Bit-exact wrap_len(v, l) (grid.hpp:45-50) with integer compares: the
+// thresholds of WrapAxis give floor(RN(v/l)) without a division.
+__device__ __forceinline__ double wrap_exact_bits(double v, const WrapAxis& a,
+                                                  unsigned long long hi0b,
+                                                  unsigned long long hi1b,
+                                                  unsigned long long lomb) {
+  const unsigned long long b = dbits(v);
+  double w;
+  if (b <= hi0b) {
+    w = v;                                  // q = 0 (v in [+0, hi0])
+  } else if (b <= hi1b) {
+    w = __dsub_rn(v, a.l);                  // q = 1
+  } else if (b > kSign && (b & kAbs) <= lomb) {
+    w = __dadd_rn(v, a.l);                  // q = -1 (v in [lom1, 0))
+  } else {
+    const double q = floor(__ddiv_rn(v, a.l));  // -0, far out of range, NaN
+    w = __dsub_rn(v, __dmul_rn(a.l, q));
+  }
+  // fix-ups: if (w >= l) w -= l;  if (w < 0.0) w = 0.0;
+  const unsigned long long wb = dbits(w);
+  if (wb < kSign && wb >= dbits(a.l)) w = __dsub_rn(w, a.l);
+  if (dbits(w) > kSign) w = 0.0;
+  return w;
+}
+
+// One component's 8 coefficients = two 256-bit loads (LDG.E.256 on sm_100a).
+struct Coef8 {
+  double p0, q0, p1, q1, p2, q2, p3, q3;
 };
 
-__device__ __forceinline__ void fast_locate_live(FastLive& L, const FastGrid& g, double tx,
-                                                 double ty, double tz) {
-  if (!(tx >= 0.0 && tx <= g.nxd && ty >= 0.0 && ty <= g.nyd && tz >= 0.0 && tz <= g.nzd)) {
-    L.ok = false;
-    L.cell = -1;
-    return;
-  }
-  const int i = min(__double2int_rz(tx), g.nx - 1);
-  const int j = min(__double2int_rz(ty), g.ny - 1);
-  const int k = min(__double2int_rz(tz), g.nz - 1);
-  L.fx = tx - static_cast<double>(i);
-  L.fy = ty - static_cast<double>(j);
-  L.fz = tz - static_cast<double>(k);
-  L.cell = i + g.nx * (j + g.ny * k);
+#ifndef B2M_LDG256
+#define B2M_LDG256 1
+#endif
+__device__ __forceinline__ Coef8 load_coef8(const double2* c) {
+  Coef8 k;
+#if !B2M_LDG256
+  const double2 a = __ldg(c), b = __ldg(c + 1), cc = __ldg(c + 2), d = __ldg(c + 3);
+  k.p0 = a.x; k.q0 = a.y; k.p1 = b.x; k.q1 = b.y;
+  k.p2 = cc.x; k.q2 = cc.y; k.p3 = d.x; k.q3 = d.y;
+  return k;
+#endif
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(k.p0), "=d"(k.q0), "=d"(k.p1), "=d"(k.q1)
+      : "l"(c));
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(k.p2), "=d"(k.q2), "=d"(k.p3), "=d"(k.q3)
+      : "l"(c + 2));
+  return k;
+}
+
+__device__ __forceinline__ double poly8(const Coef8& k, double fx, double fy, double fz) {
+  return fma(fx, fma(fy, fma(fz, k.q3, k.p3), fma(fz, k.q2, k.p2)),
+             fma(fy, fma(fz, k.q1, k.p1), fma(fz, k.q0, k.p0)));
 }
 
 __device__ __forceinline__ double poly(const double2& a, const double2& b, const double2& c,
@@ -466,11 +541,54 @@ __device__ __forceinline__ double poly(const double2& a, const double2& b, const
              fma(fy, fma(fz, b.y, b.x), fma(fz, a.y, a.x)));
 }
 
-__device__ __forceinline__ void fast_velocity(FastLive& L, const double* F, double beta) {
+// Everything the hot loop needs, hoisted into registers once per tile.
+struct FastConst {
+  double rdx, rdy, rdz;
+  double nxd, nyd, nzd;
+  double rnx, rny, rnz;
+  unsigned long long nxb, nyb, nzb;       // bits of nxd, nyd, nzd
+  unsigned long long lxb, lyb, lzb;       // bits of lx, ly, lz
+  int nx1, ny1, nz1;                      // n - 1
+  int nx, nxny;
+  double beta, dt, dcx, dcy, dcz;         // dcx = 0.5*dt/dx
+  int rounds;
+};
+
+__device__ __forceinline__ FastConst make_const(const FastGrid& g, const SpeciesLaunch& sp) {
+  FastConst k;
+  k.rdx = g.rdx; k.rdy = g.rdy; k.rdz = g.rdz;
+  k.nxd = g.nxd; k.nyd = g.nyd; k.nzd = g.nzd;
+  k.rnx = g.rnx; k.rny = g.rny; k.rnz = g.rnz;
+  k.nxb = dbits(g.nxd); k.nyb = dbits(g.nyd); k.nzb = dbits(g.nzd);
+  k.lxb = dbits(g.lx); k.lyb = dbits(g.ly); k.lzb = dbits(g.lz);
+  k.nx1 = g.nx - 1; k.ny1 = g.ny - 1; k.nz1 = g.nz - 1;
+  k.nx = g.nx; k.nxny = g.nx * g.ny;
+  k.beta = sp.beta; k.dt = sp.dt;
+  k.dcx = sp.dto2_cell[0]; k.dcy = sp.dto2_cell[1]; k.dcz = sp.dto2_cell[2];
+  k.rounds = sp.rounds;
+  return k;
+}
+
+// Cell of a folded cell-unit position and the fractions within it.  Indices
+// are clamped into the grid (a NaN position -- already flagged -- reads a
+// valid cell and the particle is discarded at the end).
+__device__ __forceinline__ int locate_fast(const FastConst& k, double tx, double ty, double tz,
+                                           double& fx, double& fy, double& fz) {
+  const int i = max(min(__double2int_rz(tx), k.nx1), 0);
+  const int j = max(min(__double2int_rz(ty), k.ny1), 0);
+  const int m = max(min(__double2int_rz(tz), k.nz1), 0);
+  fx = tx - static_cast<double>(i);
+  fy = ty - static_cast<double>(j);
+  fz = tz - static_cast<double>(m);
+  return i + k.nx * j + k.nxny * m;
+}
+
+__device__ __forceinline__ void implicit_v(double beta, double u0, double v0, double w0,
+                                           const double* F, double& bx, double& by, double& bz) {
   const double ox = beta * F[3], oy = beta * F[4], oz = beta * F[5];
-  const double vtx = fma(beta, F[0], L.u0);
-  const double vty = fma(beta, F[1], L.v0);
-  const double vtz = fma(beta, F[2], L.w0);
+  const double vtx = fma(beta, F[0], u0);
+  const double vty = fma(beta, F[1], v0);
+  const double vtz = fma(beta, F[2], w0);
   const double den = 1.0 + fma(oz, oz, fma(oy, oy, ox * ox));
   double rc;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
@@ -481,98 +599,112 @@ __device__ __forceinline__ void fast_velocity(FastLive& L, const double* F, doub
   e = fma(-den, rc, 1.0);
   rc = fma(rc, e, rc);
   const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
-  L.bx = fma(vdot, ox, vtx + fma(vty, oz, -vtz * oy)) * rc;
-  L.by = fma(vdot, oy, vty + fma(vtz, ox, -vtx * oz)) * rc;
-  L.bz = fma(vdot, oz, vtz + fma(vtx, oy, -vty * ox)) * rc;
+  bx = fma(vdot, ox, vtx + fma(vty, oz, -vtz * oy)) * rc;
+  by = fma(vdot, oy, vty + fma(vtz, ox, -vtx * oz)) * rc;
+  bz = fma(vdot, oz, vtz + fma(vtx, oy, -vty * ox)) * rc;
 }
 
-// load(i, a) returns input a (x,y,z,u,v,w) of particle i; store(i, a, v)
-// writes result a.  Only particles with has[i] are touched; ok[i] reports a
-// finite result (a faulting particle is never stored: the reference leaves it
-// untouched).  The final update runs inside the last round so no velocity
-// stays live across the round loop.
-template <int P, class Load, class Store>
-__device__ __forceinline__ void push_fast_stream(const FastGrid& g, const double2* __restrict__ cells,
-                                                 const SpeciesLaunch& sp, const bool (&has)[P],
-                                                 bool (&ok)[P], Load load, Store store) {
-  FastLive L[P];
+// One thread's P particles of a staged tile: buf[a][i0 + i] holds input a of
+// particle i (x,y,z,u,v,w); results overwrite it for particles that finish
+// clean.  Returns a bit mask of particles that must be reported as faulted.
+template <int P, int TILE>
+__device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
+                                                     const double2* __restrict__ cells,
+                                                     const FastConst& k, double (*buf)[TILE],
+                                                     int i0, int cnt) {
+  static_assert(P % 2 == 0, "pairs of particles are read with 128-bit shared loads");
+  double u0[P], v0[P], w0[P], cx0[P], cy0[P], cz0[P], fx[P], fy[P], fz[P];
+  int cell[P];
+  unsigned bad[P];
 #pragma unroll
-  for (int i = 0; i < P; ++i) {
-    ok[i] = false;
-    const double x0 = has[i] ? load(i, 0) : 0.0;
-    const double y0 = has[i] ? load(i, 1) : 0.0;
-    const double z0 = has[i] ? load(i, 2) : 0.0;
-    L[i].u0 = has[i] ? load(i, 3) : 0.0;
-    L[i].v0 = has[i] ? load(i, 4) : 0.0;
-    L[i].w0 = has[i] ? load(i, 5) : 0.0;
-    // grid.hpp:65-67: the first locate rejects x0 outside [0,l)
-    L[i].ok = has[i] && (x0 >= 0.0 && x0 < g.lx && y0 >= 0.0 && y0 < g.ly && z0 >= 0.0 && z0 < g.lz);
-    L[i].cx0 = x0 * g.rdx; L[i].cy0 = y0 * g.rdy; L[i].cz0 = z0 * g.rdz;
-    L[i].cell = -1;
-    if (L[i].ok) fast_locate_live(L[i], g, L[i].cx0, L[i].cy0, L[i].cz0);
-  }
-  const int rounds = sp.rounds;
-  for (int r = 0; r < rounds; ++r) {
-    int ref = -1;
-    bool same = true;
+  for (int i = 0; i < P; i += 2) {
+    const double2 X = *reinterpret_cast<const double2*>(&buf[0][i0 + i]);
+    const double2 Y = *reinterpret_cast<const double2*>(&buf[1][i0 + i]);
+    const double2 Z = *reinterpret_cast<const double2*>(&buf[2][i0 + i]);
+    const double2 U = *reinterpret_cast<const double2*>(&buf[3][i0 + i]);
+    const double2 V = *reinterpret_cast<const double2*>(&buf[4][i0 + i]);
+    const double2 W = *reinterpret_cast<const double2*>(&buf[5][i0 + i]);
+    const double xs[2] = {X.x, X.y}, ys[2] = {Y.x, Y.y}, zs[2] = {Z.x, Z.y};
+    u0[i] = U.x; u0[i + 1] = U.y;
+    v0[i] = V.x; v0[i + 1] = V.y;
+    w0[i] = W.x; w0[i + 1] = W.y;
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      if (!L[i].ok) continue;
-      if (ref < 0) ref = L[i].cell;
-      same = same && (L[i].cell == ref);
+    for (int h = 0; h < 2; ++h) {
+      const int q = i + h;
+      // grid.hpp:65-67: the first locate rejects x0 outside [0,l)
+      const bool inside = (i0 + q < cnt) && in_range(xs[h], k.lxb) && in_range(ys[h], k.lyb) &&
+                          in_range(zs[h], k.lzb);
+      bad[q] = inside ? 0u : 1u;
+      cx0[q] = inside ? xs[h] * k.rdx : 0.0;
+      cy0[q] = inside ? ys[h] * k.rdy : 0.0;
+      cz0[q] = inside ? zs[h] * k.rdz : 0.0;
+      cell[q] = locate_fast(k, cx0[q], cy0[q], cz0[q], fx[q], fy[q], fz[q]);
     }
-    if (ref < 0) break;
+  }
+  for (int r = 0; r < k.rounds; ++r) {
+    // every particle is gathered with the coefficients of particle 0's cell
+    // (one L1 load per pair, shared by the group); a particle that sits in
+    // another cell is re-gathered from its own.  A warp pays the fix-up only
+    // when one of its lanes needs it, instead of running a second full path.
     double F[P][6];
-    if (same) {
-      const double2* c = cells + static_cast<long long>(ref) * 24;
+    {
+      const double2* c = cells + static_cast<long long>(cell[0]) * 24;
+      Coef8 K[6];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const double2 a = __ldg(c + 4 * q), b = __ldg(c + 4 * q + 1);
-        const double2 cc = __ldg(c + 4 * q + 2), d = __ldg(c + 4 * q + 3);
+      for (int q = 0; q < 6; ++q) K[q] = load_coef8(c + 4 * q);
 #pragma unroll
-        for (int i = 0; i < P; ++i) F[i][q] = poly(a, b, cc, d, L[i].fx, L[i].fy, L[i].fz);
-      }
-    } else {
+      for (int q = 0; q < 6; ++q)
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        if (!L[i].ok) continue;
-        const double2* c = cells + static_cast<long long>(L[i].cell) * 24;
+        for (int i = 0; i < P; ++i) F[i][q] = poly8(K[q], fx[i], fy[i], fz[i]);
+    }
 #pragma unroll
-        for (int q = 0; q < 6; ++q)
-          F[i][q] = poly(__ldg(c + 4 * q), __ldg(c + 4 * q + 1), __ldg(c + 4 * q + 2),
-                         __ldg(c + 4 * q + 3), L[i].fx, L[i].fy, L[i].fz);
+    for (int i = 1; i < P; ++i) {
+      if (cell[i] != cell[0]) {
+        const double2* c = cells + static_cast<long long>(cell[i]) * 24;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) F[i][q] = poly8(load_coef8(c + 4 * q), fx[i], fy[i], fz[i]);
       }
     }
-    if (r + 1 < rounds) {
+    if (r + 1 < k.rounds) {
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        if (!L[i].ok) continue;
-        fast_velocity(L[i], F[i], sp.beta);
-        fast_locate_live(L[i], g, fold_cells(fma(L[i].bx, sp.dto2_cell[0], L[i].cx0), g.nxd, g.rnx),
-                         fold_cells(fma(L[i].by, sp.dto2_cell[1], L[i].cy0), g.nyd, g.rny),
-                         fold_cells(fma(L[i].bz, sp.dto2_cell[2], L[i].cz0), g.nzd, g.rnz));
+        double bx, by, bz;
+        implicit_v(k.beta, u0[i], v0[i], w0[i], F[i], bx, by, bz);
+        const double tx = fold_fast(fma(bx, k.dcx, cx0[i]), k.nxd, k.nxb, k.rnx, bad[i]);
+        const double ty = fold_fast(fma(by, k.dcy, cy0[i]), k.nyd, k.nyb, k.rny, bad[i]);
+        const double tz = fold_fast(fma(bz, k.dcz, cz0[i]), k.nzd, k.nzb, k.rnz, bad[i]);
+        cell[i] = locate_fast(k, tx, ty, tz, fx[i], fy[i], fz[i]);
       }
     } else {
+      unsigned faults = 0u;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        if (!L[i].ok) continue;
-        fast_velocity(L[i], F[i], sp.beta);
+        double bx, by, bz;
+        implicit_v(k.beta, u0[i], v0[i], w0[i], F[i], bx, by, bz);
         // kernels.cpp:95-99
-        const double x1 = wrap_len_exact(fma(L[i].bx, sp.dt, load(i, 0)), g.ax);
-        const double y1 = wrap_len_exact(fma(L[i].by, sp.dt, load(i, 1)), g.ay);
-        const double z1 = wrap_len_exact(fma(L[i].bz, sp.dt, load(i, 2)), g.az);
-        const double u1 = fma(2.0, L[i].bx, -L[i].u0);
-        const double v1 = fma(2.0, L[i].by, -L[i].v0);
-        const double w1 = fma(2.0, L[i].bz, -L[i].w0);
-        if (!(isfinite(x1) && isfinite(y1) && isfinite(z1) && isfinite(u1) && isfinite(v1) &&
-              isfinite(w1)))
-          continue;
-        store(i, 0, x1); store(i, 1, y1); store(i, 2, z1);
-        store(i, 3, u1); store(i, 4, v1); store(i, 5, w1);
-        ok[i] = true;
+        const int p = i0 + i;
+        const double x1 = wrap_exact_bits(fma(bx, k.dt, buf[0][p]), g.ax, dbits(g.ax.hi0),
+                                          dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
+        const double y1 = wrap_exact_bits(fma(by, k.dt, buf[1][p]), g.ay, dbits(g.ay.hi0),
+                                          dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
+        const double z1 = wrap_exact_bits(fma(bz, k.dt, buf[2][p]), g.az, dbits(g.az.hi0),
+                                          dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+        const double u1 = fma(2.0, bx, -u0[i]);
+        const double v1 = fma(2.0, by, -v0[i]);
+        const double w1 = fma(2.0, bz, -w0[i]);
+        const bool fin = finite_bits(x1) && finite_bits(y1) && finite_bits(z1) &&
+                         finite_bits(u1) && finite_bits(v1) && finite_bits(w1);
+        if (bad[i] == 0u && fin) {
+          buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
+          buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;
+        } else if (p < cnt) {
+          faults |= 1u << i;
+        }
       }
+      return faults;
     }
   }
+  return 0u;
 }
 
 }  // namespace b2m
