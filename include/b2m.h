@@ -224,6 +224,12 @@ b2m_status b2m_gem_counts(const b2m_grid* g, int ppc, uint64_t* counts4);
 b2m_status b2m_gem_species_params(const b2m_grid* g, int ppc, double* qom4, double* qpp4);
 b2m_status b2m_gem_fill_species(const b2m_grid* g, int ppc, uint64_t seed, int s,
                                 double* const* host6, int threads);
+/* Background species s (0 or 1) particles [m0, m1) of the reference's
+ * (k,j,i,p) emission order, written to host6[a][0 .. m1-m0): the counter RNG
+ * jumps straight to particle m0, so a rank can generate just its slab. */
+b2m_status b2m_gem_fill_species_range(const b2m_grid* g, int ppc, uint64_t seed, int s,
+                                      uint64_t m0, uint64_t m1, double* const* host6,
+                                      int threads);
 b2m_status b2m_gem_field(const b2m_grid* g, double* E, double* B);
 /* Test/bench field fixture with nonzero E (test_offload.cpp:60-71):
  * E=(0.01 sin y, 0, 0.02), B=(tanh((y-ly/2)/0.5), 0.05 sin x, 0). */

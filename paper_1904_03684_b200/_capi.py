@@ -92,6 +92,8 @@ SIGNATURES = {
     "b2m_gem_species_params": (_st, [C.POINTER(b2m_grid), C.c_int, _dp, _dp]),
     "b2m_gem_fill_species": (_st, [C.POINTER(b2m_grid), C.c_int, _u64, C.c_int, C.POINTER(_dp),
                                    C.c_int]),
+    "b2m_gem_fill_species_range": (_st, [C.POINTER(b2m_grid), C.c_int, _u64, C.c_int, _u64, _u64,
+                                         C.POINTER(_dp), C.c_int]),
     "b2m_gem_field": (_st, [C.POINTER(b2m_grid), _dp, _dp]),
     "b2m_gem_like_field": (_st, [C.POINTER(b2m_grid), _dp, _dp]),
 }

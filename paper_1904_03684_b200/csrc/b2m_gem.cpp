@@ -129,9 +129,10 @@ uint64_t sheet_count(const b2m_grid& g, int ppc) {  // init.cpp:54-58
       std::llround(double(ppc) * double(int64_t(g.nx) * g.ny * g.nz) * integral / g.ly));
 }
 
-// Background species, particles [m0, m1) in (k,j,i,p) order.
+// Background species, particles [m0, m1) in (k,j,i,p) order, written at
+// out[a][m - base].
 void fill_background(const b2m_grid& g, int ppc, const SpeciesDef& d, const Stream& rs,
-                     uint64_t m0, uint64_t m1, double* const* out) {
+                     uint64_t m0, uint64_t m1, double* const* out, uint64_t base = 0) {
   for (uint64_t m = m0; m < m1; ++m) {
     uint64_t cell = m / uint64_t(ppc);
     const int i = int(cell % uint64_t(g.nx));
@@ -168,12 +169,13 @@ void fill_background(const b2m_grid& g, int ppc, const SpeciesDef& d, const Stre
         have = true;
       }
     }
-    out[0][m] = x;
-    out[1][m] = y;
-    out[2][m] = z;
-    out[3][m] = d.u0[0] + d.uth[0] * nrm[0];
-    out[4][m] = d.u0[1] + d.uth[1] * nrm[1];
-    out[5][m] = d.u0[2] + d.uth[2] * nrm[2];
+    const uint64_t o = m - base;
+    out[0][o] = x;
+    out[1][o] = y;
+    out[2][o] = z;
+    out[3][o] = d.u0[0] + d.uth[0] * nrm[0];
+    out[4][o] = d.u0[1] + d.uth[1] * nrm[1];
+    out[5][o] = d.u0[2] + d.uth[2] * nrm[2];
   }
 }
 
@@ -266,6 +268,30 @@ b2m_status b2m_gem_fill_species(const b2m_grid* g, int ppc, uint64_t seed, int s
   for (int t = 0; t < threads; ++t) {
     const uint64_t lo = std::min(n, chunk * uint64_t(t)), hi = std::min(n, lo + chunk);
     pool.emplace_back([&, lo, hi] { fill_background(*g, ppc, d, rs, lo, hi, host6); });
+  }
+  for (auto& th : pool) th.join();
+  return B2M_OK;
+}
+
+b2m_status b2m_gem_fill_species_range(const b2m_grid* g, int ppc, uint64_t seed, int s,
+                                      uint64_t m0, uint64_t m1, double* const* host6,
+                                      int threads) {
+  if (!valid(g, ppc) || !host6 || s < 0 || s > 1 || m1 < m0)
+    return gem_fail(B2M_CONFIG_ERROR, "gem: range fill needs a background species and m0 <= m1");
+  const uint64_t n = uint64_t(ppc) * uint64_t(g->nx) * g->ny * g->nz;
+  if (m1 > n) return gem_fail(B2M_CONFIG_ERROR, "gem: range beyond the species");
+  const SpeciesDef d = species_def(*g, ppc, s);
+  const Stream rs(seed, uint64_t(s));
+  const uint64_t len = m1 - m0;
+  if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
+  threads = int(std::min<uint64_t>(uint64_t(threads), std::max<uint64_t>(1, len / 4096)));
+  std::vector<std::thread> pool;
+  const uint64_t chunk = (len + uint64_t(threads) - 1) / uint64_t(threads);
+  for (int t = 0; t < threads; ++t) {
+    const uint64_t lo = m0 + std::min(len, chunk * uint64_t(t));
+    const uint64_t hi = std::min(m1, lo + chunk);
+    if (lo >= hi) continue;
+    pool.emplace_back([&, lo, hi] { fill_background(*g, ppc, d, rs, lo, hi, host6, m0); });
   }
   for (auto& th : pool) th.join();
   return B2M_OK;

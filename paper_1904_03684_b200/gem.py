@@ -65,6 +65,50 @@ def init_gem_species(grid: Grid, ppc: int, seed: int = DEFAULT_SEED, pinned: boo
     return [batches[s] for s in species]
 
 
+def init_gem_slab(grid: Grid, ppc: int, rank: int, world: int, seed: int = DEFAULT_SEED,
+                  pinned: bool = True, threads: int = 0):
+    """This rank's share of the reference GEM state: exactly the particles
+    ``Simulation::distribute`` hands to worker ``rank`` (owner_of(y) == rank,
+    runtime.cpp:150-166), in the reference's emission order.  Background
+    species are generated only for the k-planes' j-rows around the slab (the
+    counter RNG jumps ahead); the sheet species, whose count does not grow
+    with the domain, are generated whole and filtered."""
+    from .partition import decompose, owner_of
+    sub = decompose(grid, world)[rank]
+    counts = gem_counts(grid, ppc)
+    qom, qpp = gem_species_params(grid, ppc)
+    g = grid.to_c()
+    row = grid.nx * ppc                       # particles per (k, j) row
+    j0, j1 = max(sub.j_lo - 1, 0), min(sub.j_hi + 1, grid.ny)
+    out = []
+    for s in range(4):
+        if s < 2:
+            # rows that can hold this rank's particles: the slab +- 1 row, and
+            # for rank 0 also the top row (y rounding up to ly wraps to 0)
+            rows = [(j0, j1)]
+            if rank == 0 and j1 < grid.ny:
+                rows.append((grid.ny - 1, grid.ny))
+            parts = []
+            for k in range(grid.nz):
+                for ja, jb in rows:
+                    m0 = (k * grid.ny + ja) * row
+                    m1 = (k * grid.ny + jb) * row
+                    arrs = [np.empty(m1 - m0) for _ in range(6)]
+                    _capi.check(_capi.lib().b2m_gem_fill_species_range(
+                        C.byref(g), ppc, seed, s, m0, m1, _capi.ptr6(arrs), threads))
+                    keep = owner_of(arrs[1], grid, world) == rank
+                    parts.append([a[keep] for a in arrs])
+            p6 = [np.concatenate([p[a] for p in parts]) for a in range(6)]
+        else:
+            full = init_gem_species(grid, ppc, seed, species=(s,))[0]
+            keep = owner_of(full.span()[1], grid, world) == rank
+            p6 = [a[keep] for a in full.span()]
+        b = ParticleBatch(s, float(qom[s]), float(qpp[s]), len(p6[0]), pinned=pinned)
+        b.assign(p6)
+        out.append(b)
+    return out
+
+
 def gem_field(grid: Grid) -> FieldMesh:
     """Harris-sheet B with the psi perturbation, E = 0 (init.cpp:72-86)."""
     f = FieldMesh(grid)

@@ -1,0 +1,349 @@
+"""Partition layer: y-slab domain decomposition across GPUs (one process per
+GPU) with NCCL particle migration -- the B200 equivalent of the reference's
+multi-worker ``Simulation`` (runtime.cpp:22-76, :211-289).
+
+* ``decompose`` / ``owner_of`` are the reference's slab rules
+  (runtime.cpp:22-44), with the same ConfigError texts.
+* ``SlabWorld`` drives one rank: the mover kernel is fused with the owner scan
+  (``b2m_move_migrate``), leavers go to the prev/next outboxes, counts then
+  payloads are exchanged with ``torch.distributed`` point-to-point ops (NCCL
+  over NVLink on GPUs), arrivals fill the holes the leavers left
+  (``b2m_inbox_append``), and an all-reduce checks particle-count conservation
+  (runtime.cpp:264-269).  A particle that lands farther than one slab away
+  raises CflViolation (runtime.cpp:55-59).
+* The field is replicated: rank 0's field is broadcast each cycle
+  (runtime.cpp:143 keeps a full copy per worker).
+
+The exchange code only needs a *store* with the DeviceStore migration methods
+and a torch device, so the same protocol runs over gloo with a host test
+double (tests/test_partition.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CflViolation, ConfigError, EngineFault
+
+
+@dataclass(frozen=True)
+class Subdomain:
+    """One worker's y-slab [j_lo, j_hi) with periodic neighbours (runtime.hpp:13-20)."""
+    worker_id: int
+    j_lo: int
+    j_hi: int
+    prev: int
+    next: int
+
+
+def decompose(grid, workers: int):
+    """Equal slabs along y (runtime.cpp:22-37)."""
+    if workers < 1:
+        raise ConfigError("workers: must be >= 1")
+    if grid.ny % workers != 0:
+        raise ConfigError(f"workers: {workers} does not divide ny={grid.ny}")
+    slab = grid.ny // workers
+    if slab < 2:
+        raise ConfigError(f"workers: slab would be {slab} cells; each slab needs at least 2")
+    return [Subdomain(w, w * slab, (w + 1) * slab, (w + workers - 1) % workers, (w + 1) % workers)
+            for w in range(workers)]
+
+
+def owner_of(y, grid, workers: int):
+    """Owner worker of wrapped y coordinate(s) (runtime.cpp:39-44):
+    j = int(y/dy) (truncation), clamped to [0, ny-1], then j / slab.
+    Vectorised over numpy arrays."""
+    y = np.asarray(y, dtype=np.float64)
+    j = np.trunc(y / grid.dy)
+    j = np.where(np.isnan(j), 0, j)
+    j = np.clip(j, 0, grid.ny - 1).astype(np.int64)
+    return j // (grid.ny // workers)
+
+
+class _CudaArray:
+    """Zero-copy torch view of a libb2m device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, stream: int = 0):
+        # no "stream" entry: the producer (b2m_sync) has already completed
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 2,
+                                         "strides": None}
+
+
+class DeviceMigration:
+    """Migration methods of a GPU DeviceStore (C ABI b2m_slab_config /
+    b2m_move_migrate / b2m_outbox / b2m_inbox_append)."""
+
+    def __init__(self, store, rank: int, world: int):
+        from . import _capi
+        self._capi = _capi
+        self.store = store
+        _capi.check(_capi.lib().b2m_slab_config(store.h, rank, world))
+
+    def move_migrate(self, s: int, mp):
+        self._capi.check(self._capi.lib().b2m_move_migrate(self.store.h, s, C.byref(mp.to_c())))
+
+    def outbox(self, s: int, direction: int):
+        import torch
+        p = C.c_void_p()
+        n = C.c_uint64()
+        self._capi.check(self._capi.lib().b2m_outbox(self.store.h, s, direction, C.byref(p),
+                                                     C.byref(n)))
+        if n.value == 0:
+            return torch.empty((0, 6), dtype=torch.float64, device="cuda")
+        return torch.as_tensor(_CudaArray(p.value, (n.value, 6)), device="cuda")
+
+    def inbox_append(self, s: int, recs):
+        n = int(recs.shape[0])
+        ptr = recs.data_ptr() if n else 0
+        self._capi.check(self._capi.lib().b2m_inbox_append(self.store.h, s, C.c_void_p(ptr), n))
+
+    def sync(self):
+        self.store.sync()
+
+    def count(self, s: int) -> int:
+        return self.store.count(s)
+
+
+class SlabWorld:
+    """One rank of the slab-partitioned mover.
+
+    ``store`` provides move_migrate / outbox / inbox_append / sync / count
+    (DeviceMigration on GPUs); ``dist`` is torch.distributed (initialised);
+    ``device`` the torch device of the exchanged tensors."""
+
+    def __init__(self, grid, store, n_species: int, dist, device):
+        self.grid = grid
+        self.store = store
+        self.ns = n_species
+        self.dist = dist
+        self.device = device
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.subs = decompose(grid, self.world)
+        me = self.subs[self.rank]
+        self.prev, self.next = me.prev, me.next
+        self.total = None
+        self.last_exchange = {}
+
+    def _count_all(self) -> int:
+        return sum(self.store.count(s) for s in range(self.ns))
+
+    def set_total(self) -> int:
+        """Global particle count (the conservation reference, runtime.cpp:150)."""
+        import torch
+        t = torch.tensor([self._count_all()], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t)
+        self.total = int(t.item())
+        return self.total
+
+    def _exchange(self, send_prev, send_next):
+        """Send (n,6) float64 tensors to prev/next, return what arrives from
+        prev and from next.  Counts first, then payloads, both as batched P2P
+        (grouped ncclSend/ncclRecv on NCCL).  With two ranks prev == next and
+        both directions travel in one message each way."""
+        import torch
+        dist = self.dist
+        dev = self.device
+        if self.world == 1:
+            return send_next, send_prev   # periodic self-neighbour (never used: no leavers)
+        if self.world == 2:
+            other = self.prev
+            out = torch.cat([send_prev, send_next], dim=0) if send_next.shape[0] else send_prev
+            cnt_out = torch.tensor([out.shape[0]], dtype=torch.int64, device=dev)
+            cnt_in = torch.zeros(1, dtype=torch.int64, device=dev)
+            ops = [dist.P2POp(dist.isend, cnt_out, other), dist.P2POp(dist.irecv, cnt_in, other)]
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+            n_in = int(cnt_in.item())
+            buf = torch.empty((n_in, 6), dtype=torch.float64, device=dev)
+            ops = []
+            if out.shape[0]:
+                ops.append(dist.P2POp(dist.isend, out.contiguous(), other))
+            if n_in:
+                ops.append(dist.P2POp(dist.irecv, buf, other))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+            return buf, torch.empty((0, 6), dtype=torch.float64, device=dev)
+        cnt_out = torch.tensor([send_prev.shape[0], send_next.shape[0]], dtype=torch.int64,
+                               device=dev)
+        c_from_prev = torch.zeros(1, dtype=torch.int64, device=dev)
+        c_from_next = torch.zeros(1, dtype=torch.int64, device=dev)
+        ops = [dist.P2POp(dist.isend, cnt_out[0:1].clone(), self.prev),
+               dist.P2POp(dist.isend, cnt_out[1:2].clone(), self.next),
+               dist.P2POp(dist.irecv, c_from_prev, self.prev),
+               dist.P2POp(dist.irecv, c_from_next, self.next)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        n_prev, n_next = int(c_from_prev.item()), int(c_from_next.item())
+        from_prev = torch.empty((n_prev, 6), dtype=torch.float64, device=dev)
+        from_next = torch.empty((n_next, 6), dtype=torch.float64, device=dev)
+        ops = []
+        if send_prev.shape[0]:
+            ops.append(dist.P2POp(dist.isend, send_prev.contiguous(), self.prev))
+        if send_next.shape[0]:
+            ops.append(dist.P2POp(dist.isend, send_next.contiguous(), self.next))
+        if n_prev:
+            ops.append(dist.P2POp(dist.irecv, from_prev, self.prev))
+        if n_next:
+            ops.append(dist.P2POp(dist.irecv, from_next, self.next))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return from_prev, from_next
+
+    def step(self, mps, check_counts: bool = True):
+        """One mover cycle over all species with migration
+        (runtime.cpp:227-244 mover + exchange, :264-269 count check).
+
+        A fault on any rank (NumericalFault, CflViolation, ...) must not
+        deadlock its peers inside the exchange (the reference drops the
+        faulting worker from the barrier, runtime.cpp:283-288): the faulting
+        rank keeps running the protocol with empty outboxes, and the fault
+        flag rides on the count all-reduce, after which every rank raises --
+        the faulting one its typed error, the others EngineFault."""
+        import torch
+        st = self.store
+        err = None
+        try:
+            for s in range(self.ns):
+                st.move_migrate(s, mps[s])
+            st.sync()   # NumericalFault / CflViolation, as the reference raises them
+        except Exception as e:  # noqa: BLE001 - re-raised after the collective below
+            err = e
+        empty = torch.empty((0, 6), dtype=torch.float64, device=self.device)
+        moved = 0
+        for s in range(self.ns):
+            if err is None:
+                try:
+                    send_prev, send_next = st.outbox(s, 0), st.outbox(s, 1)
+                except Exception as e:  # noqa: BLE001
+                    err, send_prev, send_next = e, empty, empty
+            else:
+                send_prev, send_next = empty, empty
+            from_prev, from_next = self._exchange(send_prev, send_next)
+            inbox = torch.cat([from_prev, from_next], dim=0) if from_next.shape[0] else from_prev
+            if err is None:
+                try:
+                    st.inbox_append(s, inbox.contiguous())
+                except Exception as e:  # noqa: BLE001
+                    err = e
+            moved += int(send_prev.shape[0] + send_next.shape[0])
+        self.last_exchange = {"sent": moved}
+        t = torch.tensor([self._count_all() if err is None else 0, 1 if err is not None else 0],
+                         dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t)
+        n, n_faulted = int(t[0].item()), int(t[1].item())
+        if err is not None:
+            raise err
+        if n_faulted:
+            raise EngineFault(f"simulation aborted: {n_faulted} peer rank(s) faulted in this cycle")
+        if check_counts and self.total is not None and n != self.total:
+            raise EngineFault(f"particle count drifted: {n} vs {self.total}")
+        return moved
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU benchmark (bench.py --gpus N under torchrun)
+# ---------------------------------------------------------------------------
+
+def bench_world(args) -> int:
+    """Weak scaling: grid (64, 64*N, 32), L = (25.6, 12.8*N, 6.4), 216 ppc, so
+    every rank owns a C2-sized slab (64x64x32 cells, ~56.6M background
+    particles; the Harris sheet species sit on the middle ranks).  A timed
+    step = mover + migration (NCCL P2P) + count all-reduce on every rank;
+    the time is the max over ranks of CUDA-event time."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _capi, gem
+    from .engine import DeviceStore
+    from .mover import Grid, MoverParams
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    grid = Grid.make(64, 64 * world, 32, 25.6, 12.8 * world, 6.4)
+    ppc = 216
+    sub = decompose(grid, world)[rank]
+    # this rank's slab of the reference GEM state (bit-identical generator,
+    # filtered by owner_of like Simulation::distribute, runtime.cpp:150-166)
+    batches = gem.init_gem_slab(grid, ppc, rank, world)
+    field = gem.gem_field(grid)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    caps = [int(b.count() * 1.05) + 65536 for b in batches]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    store = DeviceStore(grid, caps, args.mode, device=local)
+    store.set_stream(stream.cuda_stream)
+    store.upload_field(field)
+    for s, b in enumerate(batches):
+        store.upload(s, b.span())
+        store.sort(s)
+    mig = DeviceMigration(store, rank, world)
+    sw = SlabWorld(grid, mig, len(batches), dist, torch.device("cuda", local))
+    sw.set_total()
+    # field replication: rank 0 broadcasts its device field every cycle
+    nodes = grid.nodes()
+    fE = torch.empty(3 * nodes, dtype=torch.float64, device="cuda")
+    fB = torch.empty(3 * nodes, dtype=torch.float64, device="cuda")
+    if rank == 0:
+        fE.copy_(torch.from_numpy(field.E.ravel()))
+        fB.copy_(torch.from_numpy(field.B.ravel()))
+    step_no = [0]
+
+    def step():
+        if args.resort and step_no[0] % args.resort == 0:
+            for s in range(len(batches)):
+                store.sort(s)
+        dist.broadcast(fE, 0)
+        dist.broadcast(fB, 0)
+        store.upload_field_device(fE.data_ptr(), fB.data_ptr())
+        sw.step(mps)
+        step_no[0] += 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    l0 = _capi.lib().b2m_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    moved = 0
+    for _ in range(args.steps):
+        step()
+        moved += sw.last_exchange["sent"]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item()) / args.steps
+    n_local = torch.tensor([sum(store.count(s) for s in range(len(batches)))], dtype=torch.int64,
+                           device="cuda")
+    dist.all_reduce(n_local)
+    n_total = int(n_local.item())
+    launches = _capi.lib().b2m_launch_count() - l0
+    if rank == 0:
+        line = {"metric": "MPA/s in mover", "value": n_total / (ms_max * 1e-3) / 1e6,
+                "unit": "MPA/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic GEM state (reference init_gem generator), per-rank C2 slab",
+                "config": {"workload": f"GEM 64x{64 * world}x32, 216 ppc, y-slabs of 64 cells",
+                           "particles": n_total, "mode": args.mode,
+                           "cell_sort": f"every {args.resort} steps" if args.resort else "once",
+                           "parallelism": f"y-slab x{world}, NCCL P2P migration + field broadcast",
+                           "migrated_per_step_rank0": moved / max(1, args.steps)},
+                "gpu_launches": int(launches), "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
