@@ -13,6 +13,9 @@ Two checkers are exposed through ctypes:
 * ``ref``   -- ``_ref/libminipic_ref.so``, the UNMODIFIED reference library
   compiled from its own sources by ``Makefile`` (only where /root/reference is
   present; the built .so travels to the GPU box with the repo snapshot).
+* ``ref_b200`` -- ``_ref/libminipic_b200.so``: the same reference library
+  with the B200 engine plug-in (integration/) linked in, so the reference's
+  own Simulation can be checked against its own CPU engine.
 
 Parity of ``port`` against ``ref`` is pinned by tests/test_oracle.py and by the
 golden vectors under tests/golden/ that the reference generated.
@@ -28,6 +31,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle_port.so")
 REF_SO = os.path.join(HERE, "_ref", "libminipic_ref.so")
+# the reference library with the B200 engine plugged in (integration/Makefile)
+B200_SO = os.path.join(HERE, "_ref", "libminipic_b200.so")
 REF_SRC = "/root/reference/proj/src/kernels.cpp"
 
 _dp = C.POINTER(C.c_double)
@@ -151,6 +156,7 @@ def port_gem_species(grid, ppc: int, seed: int = 12345, species=(0, 1, 2, 3)):
 # unmodified reference library
 # --------------------------------------------------------------------------
 _ref = None
+_ref_b200 = None
 
 
 def ref_available() -> bool:
@@ -164,36 +170,52 @@ def ref() -> C.CDLL:
             if not os.path.exists(REF_SRC):
                 raise FileNotFoundError("reference library not built and sources absent")
             build()
-        lib = C.CDLL(REF_SO)
-        eb = [C.c_char_p, C.c_int]
-        g6 = [C.c_int] * 3 + [C.c_double] * 3
-        lib.ref_move_batch.argtypes = [_dp] * 6 + [_u64, _dp, _dp] + g6 + \
-            [C.c_double, C.c_double, C.c_int] + eb
-        lib.ref_move_batch_mt.argtypes = [_dp] * 6 + [_u64, _dp, _dp] + g6 + \
-            [C.c_double, C.c_double, C.c_int, C.c_int] + eb
-        lib.ref_wrap_len.argtypes = [C.c_double, C.c_double, _dp]
-        lib.ref_grid_cell_of.argtypes = [C.c_double] * 3 + g6 + [C.POINTER(C.c_int), _dp] + eb
-        lib.ref_trilinear_weights.argtypes = [C.c_double] * 3 + g6 + \
-            [C.POINTER(C.c_int64), _dp] + eb
-        lib.ref_implicit_velocity.argtypes = [_dp, _dp, _dp, C.c_double, C.c_double, _dp]
-        lib.ref_gem_species.argtypes = g6 + [C.c_int, _dp, _dp, C.POINTER(_u64)] + eb
-        lib.ref_init_gem.argtypes = g6 + [C.c_int, _u64, C.POINTER(_dp), _dp, _dp] + eb
-        lib.ref_sim_create.argtypes = g6 + [C.c_int, _u64, C.c_int, C.c_int, C.c_int,
-                                            C.c_double, C.c_int, C.c_int, C.POINTER(_dp),
-                                            C.POINTER(_u64), _dp, _dp,
-                                            C.POINTER(C.c_void_p)] + eb
-        lib.ref_sim_run.argtypes = [C.c_void_p, C.c_int] + eb
-        lib.ref_sim_species_count.argtypes = [C.c_void_p, C.c_int, C.POINTER(_u64)]
-        lib.ref_sim_gather.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp)] + eb
-        lib.ref_sim_mean_mover_s.argtypes = [C.c_void_p, _dp]
-        lib.ref_sim_destroy.argtypes = [C.c_void_p]
-        lib.ref_sim_destroy.restype = None
-        lib.ref_mpa.argtypes = [_u64, C.c_double, _dp] + eb
-        lib.ref_aggregate_runs.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp] + eb
-        lib.ref_decompose.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] + eb
-        lib.ref_owner_of.argtypes = [C.c_double] + g6 + [C.c_int]
-        _ref = lib
+        _ref = _bind_ref(C.CDLL(REF_SO))
     return _ref
+
+
+def b200_integration_available() -> bool:
+    return os.path.exists(B200_SO)
+
+
+def ref_b200() -> C.CDLL:
+    """The unmodified reference Simulation with libb2m's pic::Engine plugged
+    in (integration/minipic_b200_engine.cpp); B2M_ENGINE=1 selects it."""
+    global _ref_b200
+    if _ref_b200 is None:
+        _ref_b200 = _bind_ref(C.CDLL(B200_SO))
+    return _ref_b200
+
+
+def _bind_ref(lib: C.CDLL) -> C.CDLL:
+    eb = [C.c_char_p, C.c_int]
+    g6 = [C.c_int] * 3 + [C.c_double] * 3
+    lib.ref_move_batch.argtypes = [_dp] * 6 + [_u64, _dp, _dp] + g6 + \
+        [C.c_double, C.c_double, C.c_int] + eb
+    lib.ref_move_batch_mt.argtypes = [_dp] * 6 + [_u64, _dp, _dp] + g6 + \
+        [C.c_double, C.c_double, C.c_int, C.c_int] + eb
+    lib.ref_wrap_len.argtypes = [C.c_double, C.c_double, _dp]
+    lib.ref_grid_cell_of.argtypes = [C.c_double] * 3 + g6 + [C.POINTER(C.c_int), _dp] + eb
+    lib.ref_trilinear_weights.argtypes = [C.c_double] * 3 + g6 + \
+        [C.POINTER(C.c_int64), _dp] + eb
+    lib.ref_implicit_velocity.argtypes = [_dp, _dp, _dp, C.c_double, C.c_double, _dp]
+    lib.ref_gem_species.argtypes = g6 + [C.c_int, _dp, _dp, C.POINTER(_u64)] + eb
+    lib.ref_init_gem.argtypes = g6 + [C.c_int, _u64, C.POINTER(_dp), _dp, _dp] + eb
+    lib.ref_sim_create.argtypes = g6 + [C.c_int, _u64, C.c_int, C.c_int, C.c_int,
+                                        C.c_double, C.c_int, C.c_int, C.POINTER(_dp),
+                                        C.POINTER(_u64), _dp, _dp,
+                                        C.POINTER(C.c_void_p)] + eb
+    lib.ref_sim_run.argtypes = [C.c_void_p, C.c_int] + eb
+    lib.ref_sim_species_count.argtypes = [C.c_void_p, C.c_int, C.POINTER(_u64)]
+    lib.ref_sim_gather.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp)] + eb
+    lib.ref_sim_mean_mover_s.argtypes = [C.c_void_p, _dp]
+    lib.ref_sim_destroy.argtypes = [C.c_void_p]
+    lib.ref_sim_destroy.restype = None
+    lib.ref_mpa.argtypes = [_u64, C.c_double, _dp] + eb
+    lib.ref_aggregate_runs.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp] + eb
+    lib.ref_decompose.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] + eb
+    lib.ref_owner_of.argtypes = [C.c_double] + g6 + [C.c_int]
+    return lib
 
 
 def _errbuf():
@@ -282,8 +304,9 @@ class RefSimulation:
     ENGINES = {"cpu": 0, "naive": 1, "pinned": 2, "prefetch": 3}
 
     def __init__(self, grid, ppc, workers=1, engine="cpu", pc=3, dt=0.1, field_passes=100,
-                 seed=12345, inject=None):
-        lib = ref()
+                 seed=12345, inject=None, lib=None):
+        lib = lib or ref()
+        self.lib = lib
         buf = _errbuf()
         h = C.c_void_p()
         if inject is None:
@@ -303,25 +326,28 @@ class RefSimulation:
 
     def run(self, cycles: int) -> None:
         buf = _errbuf()
-        _check(ref().ref_sim_run(self.h, cycles, buf, 512), buf)
+        _check(self.lib.ref_sim_run(self.h, cycles, buf, 512), buf)
 
     def gather(self, s: int):
         n = _u64()
-        ref().ref_sim_species_count(self.h, s, C.byref(n))
+        self.lib.ref_sim_species_count(self.h, s, C.byref(n))
         out = [np.empty(n.value) for _ in range(6)]
         buf = _errbuf()
-        _check(ref().ref_sim_gather(self.h, s, (_dp * 6)(*[_ptr(a) for a in out]), buf, 512),
+        _check(self.lib.ref_sim_gather(self.h, s, (_dp * 6)(*[_ptr(a) for a in out]), buf, 512),
                buf)
         return out
 
     def mean_mover_s(self) -> float:
         out = C.c_double()
-        ref().ref_sim_mean_mover_s(self.h, C.byref(out))
+        self.lib.ref_sim_mean_mover_s(self.h, C.byref(out))
         return out.value
 
     def __del__(self):
         if getattr(self, "h", None):
-            ref().ref_sim_destroy(self.h)
+            try:
+                self.lib.ref_sim_destroy(self.h)
+            except Exception:
+                pass
             self.h = None
 
 
