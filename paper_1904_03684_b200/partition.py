@@ -130,6 +130,9 @@ class SlabWorld:
         self.prev, self.next = me.prev, me.next
         self.total = None
         self.last_exchange = {}
+        # gloo has no CUDA point-to-point: stage device tensors through host
+        backend = getattr(dist, "get_backend", lambda: "")()
+        self.stage_host = (str(backend) == "gloo" and getattr(device, "type", "") == "cuda")
 
     def _count_all(self) -> int:
         return sum(self.store.count(s) for s in range(self.ns))
@@ -138,18 +141,31 @@ class SlabWorld:
         """Global particle count (the conservation reference, runtime.cpp:150)."""
         import torch
         t = torch.tensor([self._count_all()], dtype=torch.int64, device=self.device)
-        self.dist.all_reduce(t)
+        self._all_reduce(t)
         self.total = int(t.item())
         return self.total
 
     def _exchange(self, send_prev, send_next):
+        if self.stage_host:
+            a, b = self._exchange_on(send_prev.cpu(), send_next.cpu(), "cpu")
+            return a.to(self.device), b.to(self.device)
+        return self._exchange_on(send_prev, send_next, self.device)
+
+    def _all_reduce(self, t, op=None):
+        if self.stage_host:
+            h = t.cpu()
+            self.dist.all_reduce(h) if op is None else self.dist.all_reduce(h, op=op)
+            t.copy_(h.to(t.device))
+        else:
+            self.dist.all_reduce(t) if op is None else self.dist.all_reduce(t, op=op)
+
+    def _exchange_on(self, send_prev, send_next, dev):
         """Send (n,6) float64 tensors to prev/next, return what arrives from
         prev and from next.  Counts first, then payloads, both as batched P2P
         (grouped ncclSend/ncclRecv on NCCL).  With two ranks prev == next and
         both directions travel in one message each way."""
         import torch
         dist = self.dist
-        dev = self.device
         if self.world == 1:
             return send_next, send_prev   # periodic self-neighbour (never used: no leavers)
         if self.world == 2:
@@ -238,7 +254,7 @@ class SlabWorld:
         self.last_exchange = {"sent": moved}
         t = torch.tensor([self._count_all() if err is None else 0, 1 if err is not None else 0],
                          dtype=torch.int64, device=self.device)
-        self.dist.all_reduce(t)
+        self._all_reduce(t)
         n, n_faulted = int(t[0].item()), int(t[1].item())
         if err is not None:
             raise err
@@ -266,9 +282,15 @@ def bench_world(args) -> int:
     from .engine import DeviceStore
     from .mover import Grid, MoverParams
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # B2M_DIST_BACKEND=gloo lets several ranks share fewer GPUs for functional
+    # checks (host-staged exchange); the benchmark itself uses NCCL
+    backend = os.environ.get("B2M_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     rank, world = dist.get_rank(), dist.get_world_size()
     grid = Grid.make(64, 64 * world, 32, 25.6, 12.8 * world, 6.4)
     ppc = 216
@@ -303,8 +325,14 @@ def bench_world(args) -> int:
         if args.resort and step_no[0] % args.resort == 0:
             for s in range(len(batches)):
                 store.sort(s)
-        dist.broadcast(fE, 0)
-        dist.broadcast(fB, 0)
+        if backend == "nccl":
+            dist.broadcast(fE, 0)
+            dist.broadcast(fB, 0)
+        else:
+            for t in (fE, fB):
+                h = t.cpu()
+                dist.broadcast(h, 0)
+                t.copy_(h.to(t.device))
         store.upload_field_device(fE.data_ptr(), fB.data_ptr())
         sw.step(mps)
         step_no[0] += 1
@@ -324,11 +352,11 @@ def bench_world(args) -> int:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sw._all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item()) / args.steps
     n_local = torch.tensor([sum(store.count(s) for s in range(len(batches)))], dtype=torch.int64,
                            device="cuda")
-    dist.all_reduce(n_local)
+    sw._all_reduce(n_local)
     n_total = int(n_local.item())
     launches = _capi.lib().b2m_launch_count() - l0
     if rank == 0:
@@ -340,7 +368,8 @@ def bench_world(args) -> int:
                 "config": {"workload": f"GEM 64x{64 * world}x32, 216 ppc, y-slabs of 64 cells",
                            "particles": n_total, "mode": args.mode,
                            "cell_sort": f"every {args.resort} steps" if args.resort else "once",
-                           "parallelism": f"y-slab x{world}, NCCL P2P migration + field broadcast",
+                           "parallelism": f"y-slab x{world}, {backend} P2P migration + field "
+                                          "broadcast",
                            "migrated_per_step_rank0": moved / max(1, args.steps)},
                 "gpu_launches": int(launches), "e2e": None, "cpu_baseline": None}
         print(json.dumps(line), flush=True)
