@@ -98,9 +98,12 @@ namespace {
 constexpr int kEventSlots = 16;
 
 struct Species {
+  // the six SoA arrays live in one [6][stride] block (stride = capacity
+  // rounded up to 32), so a tile of all six is a single 2-D TMA box
   double* a[6] = {};
   double* alt[6] = {};  // ping-pong set for the cell sort (allocated on first sort)
   uint64_t capacity = 0;
+  uint64_t stride = 0;
   uint64_t count = 0;
   // migration scratch
   uint8_t* flags = nullptr;
@@ -216,6 +219,8 @@ SpeciesLaunch make_launch(b2m_ctx* ctx, int s, const b2m_mover_params& mp, uint6
   L.dto2_cell[2] = L.dto2 / ctx->grid.dz;
   L.rounds = mp.pc_iterations;
   L.species = s;
+  L.col0 = offset;
+  L.stride = S.stride;
   return L;
 }
 
@@ -366,8 +371,10 @@ b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const ui
   for (int s = 0; s < n_species; ++s) {
     Species& S = ctx->sp[static_cast<size_t>(s)];
     S.capacity = capacity[s];
-    for (int a = 0; a < 6; ++a)
-      if ((st = dalloc(ctx, &S.a[a], S.capacity, "species arrays")) != B2M_OK) return bail(st);
+    S.stride = (S.capacity + 31) / 32 * 32;
+    double* blk = nullptr;
+    if ((st = dalloc(ctx, &blk, 6 * S.stride, "species arrays")) != B2M_OK) return bail(st);
+    for (int a = 0; a < 6; ++a) S.a[a] = blk + a * S.stride;
   }
   launch_fault_reset(ctx->fault, ctx->stream);
   if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
@@ -576,7 +583,8 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   if (ctx->mode == B2M_MODE_STRICT)
     launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
   else
-    launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream);
+    if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
+      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }
@@ -602,8 +610,9 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
   if (ctx->mode == B2M_MODE_STRICT)
     launch_move_strict_batch(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
                              ctx->stream);
-  else
-    launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault, ctx->stream);
+  else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault,
+                             ctx->stream))
+    return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }
@@ -653,8 +662,8 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
       const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
       if (ctx->mode == B2M_MODE_STRICT)
         launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
-      else
-        launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream);
+      else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
+        return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       B2M_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], ctx->stream));
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->down, ev[2 * c + 1], 0));
       for (int a = 0; a < 6; ++a)
@@ -686,19 +695,13 @@ b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
   // permute into the ping-pong set and swap (no copy back); fall back to a
   // scratch array + copy when the second set does not fit in device memory
   if (!S.alt[0]) {
-    for (int a = 0; a < 6; ++a) {
-      if (cudaMalloc(reinterpret_cast<void**>(&S.alt[a]), S.capacity * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        for (int b = 0; b < a; ++b) {
-          cudaFree(S.alt[b]);
-          S.alt[b] = nullptr;
-        }
-        S.alt[0] = nullptr;
-        break;
-      }
+    double* blk = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&blk), 6 * S.stride * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+    } else {
+      ctx->allocations.push_back(blk);
+      for (int a = 0; a < 6; ++a) S.alt[a] = blk + a * S.stride;
     }
-    if (S.alt[0])
-      for (int a = 0; a < 6; ++a) ctx->allocations.push_back(S.alt[a]);
   }
   if (S.alt[0]) {
     launch_gather6(S.a, ctx->vals[1], n, S.alt, ctx->stream);
@@ -935,6 +938,7 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
   SpeciesLaunch L{};
   L.x = S.a[0]; L.y = S.a[1]; L.z = S.a[2];
   L.u = S.a[3]; L.v = S.a[4]; L.w = S.a[5];
+  L.stride = S.stride;
   L.n = old_n;
   L.species = s;
   if (S.migrate_pending) {

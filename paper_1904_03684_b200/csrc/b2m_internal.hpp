@@ -33,8 +33,9 @@ void launch_move_strict(const DevGrid& g, const double* E, const double* B,
 void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B,
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                               cudaStream_t st);
-// FAST mover on a batch of species spans (one launch).
-void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+// FAST mover on a batch of species spans (one launch).  Returns false when a
+// TMA tensor map cannot be built (driver entry point missing, >2^31 columns).
+bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st);
 // Node AoS E/B -> per-cell polynomial coefficients (48 doubles per cell).
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,

@@ -10,6 +10,7 @@
 //   scatter_out / fill    outbox compaction and hole filling
 //                         (merge_incoming, runtime.cpp:64-76)
 #include <cub/cub.cuh>
+#include <cudaTypedefs.h>
 
 #include "b2m_internal.hpp"
 #include "b2m_tile.cuh"
@@ -179,11 +180,12 @@ __global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : B2M_FAST_MINBLOCKS)
 
 // FAST mover with warp-private TMA pipelines: every warp streams its own
 // tiles of 32*P particles (kWarpStages deep) through its slice of shared
-// memory, with its own mbarriers -- no block-wide barrier anywhere, so a warp
-// that finishes a tile early starts the next one instead of idling.
+// memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
+// tensor-map box per tile carries all six SoA arrays in (and one out); the
+// TMA unit zero-fills / clips partial tiles, so there is a single code path.
 template <int P>
 __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
-    warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TileSpans S,
+    warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
                      unsigned long long total_tiles, FaultWord* fault) {
   constexpr int WT = 32 * P;
   constexpr int WARPS = kTileThreads / 32;
@@ -196,35 +198,21 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
   // streams one contiguous window of the particle arrays (DRAM-friendly)
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * WARPS + warp;
   const unsigned long long GW = static_cast<unsigned long long>(gridDim.x) * WARPS;
-  const unsigned long long t_end = total_tiles;
+  const uint64_t stream_pol = policy_evict_first();
 
-  auto resolve = [&](unsigned long long tile, int& s, unsigned long long& off, int& cnt,
-                     bool& full) {
-    s = 0;
+  auto species_of = [&](unsigned long long tile) {
+    int s = 0;
     while (s + 1 < S.n && tile >= S.tile_start[s + 1]) ++s;
-    off = (tile - S.tile_start[s]) * WT;
-    const unsigned long long left = S.sp[s].n - off;
-    cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
-    full = (cnt == WT) && S.tma_ok[s];
+    return s;
   };
   auto issue = [&](unsigned long long k) {  // lane 0
     const unsigned long long tile = gw + k * GW;
-    if (tile >= t_end) return;
-    int s, cnt;
-    unsigned long long off;
-    bool full;
-    resolve(tile, s, off, cnt, full);
+    if (tile >= total_tiles) return;
+    const int s = species_of(tile);
     const int st = static_cast<int>(k % kWarpStages);
-    if (full) {
-      const SpeciesLaunch& sp = S.sp[s];
-      mbar_arrive_tx(&bar[st], 6 * WT * sizeof(double));
-      const double* src[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-        tma_load_1d(buf[st][a], src[a] + off, WT * sizeof(double), &bar[st]);
-    } else {
-      mbar_arrive(&bar[st]);
-    }
+    const int c0 = static_cast<int>(S.sp[s].col0 + (tile - S.tile_start[s]) * WT);
+    mbar_arrive_tx(&bar[st], 6 * WT * sizeof(double));
+    tma_load_2d(buf[st], &S.tmap[s], c0, 0, &bar[st], stream_pol);
   };
 
   if (lane == 0) {
@@ -236,21 +224,14 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
 
   for (unsigned long long k = 0;; ++k) {
     const unsigned long long tile = gw + k * GW;
-    if (tile >= t_end) break;
-    int s, cnt;
-    unsigned long long off;
-    bool full;
-    resolve(tile, s, off, cnt, full);
+    if (tile >= total_tiles) break;
+    const int s = species_of(tile);
+    const SpeciesLaunch& sp = S.sp[s];
+    const unsigned long long off = (tile - S.tile_start[s]) * WT;
+    const unsigned long long left = sp.n - off;
+    const int cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
     const int st = static_cast<int>(k % kWarpStages);
     mbar_wait(&bar[st], static_cast<uint32_t>((k / kWarpStages) & 1));
-    const SpeciesLaunch& sp = S.sp[s];
-    double* ptr[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
-    if (!full) {
-      for (int j = lane; j < cnt; j += 32)
-#pragma unroll
-        for (int a = 0; a < 6; ++a) buf[st][a][j] = ptr[a][off + j];
-      __syncwarp();
-    }
     const FastConst kc = make_const(F.fg, sp);
     const int i0 = P * lane;
     unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
@@ -259,19 +240,10 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
       faults &= faults - 1;
       atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
     }
-    if (full) fence_proxy_async();
+    fence_proxy_async();
     __syncwarp();
-    if (!full) {
-      for (int j = lane; j < cnt; j += 32)
-#pragma unroll
-        for (int a = 0; a < 6; ++a) ptr[a][off + j] = buf[st][a][j];
-      __syncwarp();
-    }
     if (lane == 0) {
-      if (full) {
-#pragma unroll
-        for (int a = 0; a < 6; ++a) tma_store_1d(ptr[a] + off, buf[st][a], WT * sizeof(double));
-      }
+      tma_store_2d(&S.tmap[s], static_cast<int>(sp.col0 + off), 0, buf[st], stream_pol);
       tma_commit();
       tma_wait_read<0>();
       issue(k + kWarpStages);
@@ -588,7 +560,38 @@ void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B
   launch_tiles<true>(F, sp, n_spans, fault, st);
 }
 
-void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool encode_species_map(CUtensorMap* map, const SpeciesLaunch& sp, int box_cols) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  // the species block starts at x - col0; rows are the six arrays
+  const double* base = sp.x - sp.col0;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(sp.col0 + sp.n), 6};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(sp.stride * sizeof(double))};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 6};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st) {
   TileField F{};
   F.fg = g;
@@ -606,28 +609,25 @@ void launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   for (int base = 0; base < n_spans; base += kMaxTileSpans) {
-    TileSpans S{};
+    TensorSpans S{};
     unsigned long long tiles = 0;
     for (int s = base; s < n_spans && S.n < kMaxTileSpans; ++s) {
       if (sp[s].n == 0) continue;
+      if (sp[s].col0 + sp[s].n > 0x7fffffffull) return false;  // 32-bit TMA coordinates
       S.sp[S.n] = sp[s];
+      if (!encode_species_map(&S.tmap[S.n], sp[s], WT)) return false;
       S.tile_start[S.n] = tiles;
-      const uintptr_t m =
-          reinterpret_cast<uintptr_t>(sp[s].x) | reinterpret_cast<uintptr_t>(sp[s].y) |
-          reinterpret_cast<uintptr_t>(sp[s].z) | reinterpret_cast<uintptr_t>(sp[s].u) |
-          reinterpret_cast<uintptr_t>(sp[s].v) | reinterpret_cast<uintptr_t>(sp[s].w);
-      S.tma_ok[S.n] = (m & 15u) == 0;
       tiles += (sp[s].n + WT - 1) / WT;
       ++S.n;
     }
     S.tile_start[S.n] = tiles;
     if (S.n == 0) continue;
-    const unsigned long long warps_needed = tiles;
-    const unsigned long long blocks = (warps_needed + 3) / 4;
+    const unsigned long long blocks = (tiles + 3) / 4;
     const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
     warp_tile_kernel<P><<<grid, kTileThreads, smem, st>>>(F, S, tiles, fault);
     note_launch();
   }
+  return true;
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,

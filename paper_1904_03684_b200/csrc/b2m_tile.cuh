@@ -17,6 +17,8 @@
 // Partial tail tiles (and unaligned spans) use plain loads/stores.
 #pragma once
 
+#include <cuda.h>
+
 #include "b2m_mover.cuh"
 
 namespace b2m {
@@ -45,6 +47,16 @@ struct TileSpans {
   SpeciesLaunch sp[kMaxTileSpans];
   unsigned long long tile_start[kMaxTileSpans + 1];
   int tma_ok[kMaxTileSpans];
+  int n;
+};
+
+// FAST launch: per span a 2-D tensor map over the species' [6][stride]
+// block (dims {col0 + n, 6}), so one TMA box moves all six arrays of a tile
+// and the hardware clips partial tiles.
+struct alignas(64) TensorSpans {
+  CUtensorMap tmap[kMaxTileSpans];
+  SpeciesLaunch sp[kMaxTileSpans];
+  unsigned long long tile_start[kMaxTileSpans + 1];
   int n;
 };
 
@@ -83,6 +95,56 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+
+// L2 eviction priorities: the particle stream (2.9 GB per cycle at C2) is
+// evict-first so it does not sweep the 50 MB coefficient table, which is
+// evict-last (createpolicy, PTX ISA 7.4+).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void tma_load_1d_hint(void* smem_dst, const void* gmem_src,
+                                                 uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_1d_hint(void* gmem_dst, const void* smem_src,
+                                                  uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                   gmem_dst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1,
+                                             const void* smem_src, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(smem_src)), "l"(pol)
       : "memory");
 }
 
@@ -513,8 +575,21 @@ struct Coef8 {
 #ifndef B2M_LDG256
 #define B2M_LDG256 1
 #endif
+#ifndef B2M_L2HINT
+#define B2M_L2HINT 1
+#endif
 __device__ __forceinline__ Coef8 load_coef8(const double2* c) {
   Coef8 k;
+#if B2M_L2HINT && B2M_LDG256
+  const uint64_t pol = policy_evict_last();
+  asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(k.p0), "=d"(k.q0), "=d"(k.p1), "=d"(k.q1)
+      : "l"(c), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(k.p2), "=d"(k.q2), "=d"(k.p3), "=d"(k.q3)
+      : "l"(c + 2), "l"(pol));
+  return k;
+#endif
 #if !B2M_LDG256
   const double2 a = __ldg(c), b = __ldg(c + 1), cc = __ldg(c + 2), d = __ldg(c + 3);
   k.p0 = a.x; k.q0 = a.y; k.p1 = b.x; k.q1 = b.y;
@@ -583,6 +658,9 @@ __device__ __forceinline__ int locate_fast(const FastConst& k, double tx, double
   return i + k.nx * j + k.nxny * m;
 }
 
+// Implicit velocity (kernels.cpp:83-90), FMA form: vt = v0 + beta*E,
+// W = beta*B, vbar = (vt + vt x W + (vt.W) W) / (1 + |W|^2).  The reciprocal
+// is the MUFU.RCP64H seed (~2^-23) refined by two Newton steps (~2^-92).
 __device__ __forceinline__ void implicit_v(double beta, double u0, double v0, double w0,
                                            const double* F, double& bx, double& by, double& bz) {
   const double ox = beta * F[3], oy = beta * F[4], oz = beta * F[5];
@@ -596,12 +674,21 @@ __device__ __forceinline__ void implicit_v(double beta, double u0, double v0, do
   rc = fma(rc, e, rc);
   e = fma(-den, rc, 1.0);
   rc = fma(rc, e, rc);
-  e = fma(-den, rc, 1.0);
-  rc = fma(rc, e, rc);
   const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
-  bx = fma(vdot, ox, vtx + fma(vty, oz, -vtz * oy)) * rc;
-  by = fma(vdot, oy, vty + fma(vtz, ox, -vtx * oz)) * rc;
-  bz = fma(vdot, oz, vtz + fma(vtx, oy, -vty * ox)) * rc;
+  bx = fma(vdot, ox, fma(vty, oz, fma(-vtz, oy, vtx))) * rc;
+  by = fma(vdot, oy, fma(vtz, ox, fma(-vtx, oz, vty))) * rc;
+  bz = fma(vdot, oz, fma(vtx, oy, fma(-vty, ox, vtz))) * rc;
+}
+
+// Fold of all three predictor coordinates at once: one combined (integer)
+// range test, the slow path only for the rare lane that crossed a boundary.
+__device__ __forceinline__ void fold3(double& tx, double& ty, double& tz, const FastConst& k,
+                                      unsigned& bad) {
+  if ((dbits(tx) >= k.nxb) | (dbits(ty) >= k.nyb) | (dbits(tz) >= k.nzb)) {
+    tx = fold_fast(tx, k.nxd, k.nxb, k.rnx, bad);
+    ty = fold_fast(ty, k.nyd, k.nyb, k.rny, bad);
+    tz = fold_fast(tz, k.nzd, k.nzb, k.rnz, bad);
+  }
 }
 
 // One thread's P particles of a staged tile: buf[a][i0 + i] holds input a of
@@ -641,12 +728,53 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
       cell[q] = locate_fast(k, cx0[q], cy0[q], cz0[q], fx[q], fy[q], fz[q]);
     }
   }
+#ifndef B2M_FAST_CACHE
+#define B2M_FAST_CACHE 0
+#endif
+#if B2M_FAST_CACHE
+  // Register cell cache: the 48 coefficients of one cell stay in registers
+  // across the predictor rounds and are shared by the P particles; it is
+  // refilled only when fewer than half of the live particles sit in it.
+  Coef8 K[6];
+  int kcell = -1;
+#endif
   for (int r = 0; r < k.rounds; ++r) {
+    double F[P][6];
+#if B2M_FAST_CACHE
+    {
+      int hits = 0;
+#pragma unroll
+      for (int i = 0; i < P; ++i) hits += (cell[i] == kcell) ? 1 : 0;
+      if (2 * hits < P) {
+        kcell = cell[0];
+        const double2* c = cells + static_cast<long long>(kcell) * 24;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) K[q] = load_coef8(c + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int i = 0; i < P; ++i) F[i][q] = poly8(K[q], fx[i], fy[i], fz[i]);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      if (cell[i] != kcell) {
+        const double2* c = cells + static_cast<long long>(cell[i]) * 24;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) F[i][q] = poly8(load_coef8(c + 4 * q), fx[i], fy[i], fz[i]);
+      }
+    }
+#elif defined(B2M_DIAG_NOGATHER)
+    // DIAGNOSTIC BUILD ONLY (tools/build_variants.sh): no field loads at all
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int i = 0; i < P; ++i) F[i][q] = fma(fx[i], fy[i], fz[i] * (0.001 * q));
+#else
     // every particle is gathered with the coefficients of particle 0's cell
     // (one L1 load per pair, shared by the group); a particle that sits in
     // another cell is re-gathered from its own.  A warp pays the fix-up only
     // when one of its lanes needs it, instead of running a second full path.
-    double F[P][6];
     {
       const double2* c = cells + static_cast<long long>(cell[0]) * 24;
       Coef8 K[6];
@@ -665,14 +793,16 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
         for (int q = 0; q < 6; ++q) F[i][q] = poly8(load_coef8(c + 4 * q), fx[i], fy[i], fz[i]);
       }
     }
+#endif
     if (r + 1 < k.rounds) {
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         double bx, by, bz;
         implicit_v(k.beta, u0[i], v0[i], w0[i], F[i], bx, by, bz);
-        const double tx = fold_fast(fma(bx, k.dcx, cx0[i]), k.nxd, k.nxb, k.rnx, bad[i]);
-        const double ty = fold_fast(fma(by, k.dcy, cy0[i]), k.nyd, k.nyb, k.rny, bad[i]);
-        const double tz = fold_fast(fma(bz, k.dcz, cz0[i]), k.nzd, k.nzb, k.rnz, bad[i]);
+        double tx = fma(bx, k.dcx, cx0[i]);
+        double ty = fma(by, k.dcy, cy0[i]);
+        double tz = fma(bz, k.dcz, cz0[i]);
+        fold3(tx, ty, tz, k, bad[i]);
         cell[i] = locate_fast(k, tx, ty, tz, fx[i], fy[i], fz[i]);
       }
     } else {
@@ -683,12 +813,20 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
         implicit_v(k.beta, u0[i], v0[i], w0[i], F[i], bx, by, bz);
         // kernels.cpp:95-99
         const int p = i0 + i;
-        const double x1 = wrap_exact_bits(fma(bx, k.dt, buf[0][p]), g.ax, dbits(g.ax.hi0),
-                                          dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
-        const double y1 = wrap_exact_bits(fma(by, k.dt, buf[1][p]), g.ay, dbits(g.ay.hi0),
-                                          dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
-        const double z1 = wrap_exact_bits(fma(bz, k.dt, buf[2][p]), g.az, dbits(g.az.hi0),
-                                          dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+        double x1 = fma(bx, k.dt, buf[0][p]);
+        double y1 = fma(by, k.dt, buf[1][p]);
+        double z1 = fma(bz, k.dt, buf[2][p]);
+        // common case: every coordinate stayed in [+0, hi0] -> wrap_len is the
+        // identity; otherwise the exact per-axis wrap
+        if ((dbits(x1) > dbits(g.ax.hi0)) | (dbits(y1) > dbits(g.ay.hi0)) |
+            (dbits(z1) > dbits(g.az.hi0))) {
+          x1 = wrap_exact_bits(x1, g.ax, dbits(g.ax.hi0), dbits(g.ax.hi1),
+                               dbits(g.ax.lom1) & kAbs);
+          y1 = wrap_exact_bits(y1, g.ay, dbits(g.ay.hi0), dbits(g.ay.hi1),
+                               dbits(g.ay.lom1) & kAbs);
+          z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1),
+                               dbits(g.az.lom1) & kAbs);
+        }
         const double u1 = fma(2.0, bx, -u0[i]);
         const double v1 = fma(2.0, by, -v0[i]);
         const double w1 = fma(2.0, bz, -w0[i]);
