@@ -233,12 +233,27 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
     const int st = static_cast<int>(k % kWarpStages);
     mbar_wait(&bar[st], static_cast<uint32_t>((k / kWarpStages) & 1));
     const FastConst kc = make_const(F.fg, sp);
-    const int i0 = P * lane;
-    unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
-    while (faults) {
-      const int i = __ffs(faults) - 1;
-      faults &= faults - 1;
-      atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
+    if (B2M_FAST_SEQ) {
+      // particles lane + 32*j, j < P, one after the other, sharing the
+      // register cell cache (consecutive particles of a cell-ordered species
+      // mostly share a cell, so the cache is usually filled once per tile);
+      // consecutive lanes read consecutive shared-memory words
+      Coef8 K[6];
+      int kcell = -1;
+#pragma unroll 1
+      for (int j = 0; j < P; ++j) {
+        const int p = lane + 32 * j;
+        if (fast_tile_thread_p1<WT>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell))
+          atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+      }
+    } else {
+      const int i0 = P * lane;
+      unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
+      while (faults) {
+        const int i = __ffs(faults) - 1;
+        faults &= faults - 1;
+        atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
+      }
     }
     fence_proxy_async();
     __syncwarp();
@@ -599,6 +614,7 @@ bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
   constexpr int P = B2M_FAST_PPT;
   constexpr int WT = 32 * P;
   constexpr int smem = (kTileThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
+  static_assert(smem <= 227 * 1024, "warp tiles exceed shared memory");
   static int grid_cap = -1;
   if (grid_cap < 0) {
     int dev = 0, sms = 0, per_sm = 0;

@@ -29,11 +29,17 @@ constexpr int kWarpStages = 3;
 constexpr int kTileMinBlocks = 3;
 // particles per thread: FAST streams coefficients to 4 particles, STRICT
 // keeps a register cell cache shared by 2
+// FAST kernel shape (tuned on B200, tools/sweep.py): each lane moves 4
+// particles one after the other with a register cell cache (SEQ), 3 blocks
+// of 128 threads per SM.  SEQ=0 selects the older pair-sharing variant.
 #ifndef B2M_FAST_PPT
-#define B2M_FAST_PPT 2
+#define B2M_FAST_PPT 4
+#endif
+#ifndef B2M_FAST_SEQ
+#define B2M_FAST_SEQ 1
 #endif
 #ifndef B2M_FAST_MINBLOCKS
-#define B2M_FAST_MINBLOCKS 4
+#define B2M_FAST_MINBLOCKS 3
 #endif
 template <bool STRICT>
 struct TileShape {
@@ -699,7 +705,7 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
                                                      const double2* __restrict__ cells,
                                                      const FastConst& k, double (*buf)[TILE],
                                                      int i0, int cnt) {
-  static_assert(P % 2 == 0, "pairs of particles are read with 128-bit shared loads");
+  static_assert(P % 2 == 0 || P == 1, "pairs of particles are read with 128-bit shared loads");
   double u0[P], v0[P], w0[P], cx0[P], cy0[P], cz0[P], fx[P], fy[P], fz[P];
   int cell[P];
   unsigned bad[P];
@@ -843,6 +849,74 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
     }
   }
   return 0u;
+}
+
+// ---------------------------------------------------------------------------
+// FAST, one particle per thread with a register cell cache
+// ---------------------------------------------------------------------------
+//
+// The 48 coefficients of the particle's cell stay in registers for all
+// predictor rounds and are reloaded only when the predictor position moves to
+// another cell (~2 % of rounds in GEM).  The reload branch contains loads
+// only, so a warp whose lanes disagree never runs two evaluation paths, and
+// performance does not depend on particles sharing cells (no cell sort
+// needed).  L1->register traffic: 384 B per particle per cycle.
+template <int TILE>
+__device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
+                                                        const double2* __restrict__ cells,
+                                                        const FastConst& k, double (*buf)[TILE],
+                                                        int p, int cnt, Coef8 (&K)[6],
+                                                        int& kcell) {
+  const double x0 = buf[0][p], y0 = buf[1][p], z0 = buf[2][p];
+  const double u0 = buf[3][p], v0 = buf[4][p], w0 = buf[5][p];
+  const bool inside = (p < cnt) && in_range(x0, k.lxb) && in_range(y0, k.lyb) && in_range(z0, k.lzb);
+  unsigned bad = inside ? 0u : 1u;
+  const double cx0 = inside ? x0 * k.rdx : 0.0;
+  const double cy0 = inside ? y0 * k.rdy : 0.0;
+  const double cz0 = inside ? z0 * k.rdz : 0.0;
+  double fx, fy, fz;
+  int cell = locate_fast(k, cx0, cy0, cz0, fx, fy, fz);
+  double bx = u0, by = v0, bz = w0;
+  for (int r = 0; r < k.rounds; ++r) {
+    if (cell != kcell) {  // rare: the predictor left the cached cell
+      const double2* c = cells + static_cast<long long>(cell) * 24;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) K[q] = load_coef8(c + 4 * q);
+      kcell = cell;
+    }
+    double F[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) F[q] = poly8(K[q], fx, fy, fz);
+    implicit_v(k.beta, u0, v0, w0, F, bx, by, bz);
+    if (r + 1 < k.rounds) {
+      double tx = fma(bx, k.dcx, cx0);
+      double ty = fma(by, k.dcy, cy0);
+      double tz = fma(bz, k.dcz, cz0);
+      fold3(tx, ty, tz, k, bad);
+      cell = locate_fast(k, tx, ty, tz, fx, fy, fz);
+    }
+  }
+  // kernels.cpp:95-99
+  double x1 = fma(bx, k.dt, x0);
+  double y1 = fma(by, k.dt, y0);
+  double z1 = fma(bz, k.dt, z0);
+  if ((dbits(x1) > dbits(g.ax.hi0)) | (dbits(y1) > dbits(g.ay.hi0)) |
+      (dbits(z1) > dbits(g.az.hi0))) {
+    x1 = wrap_exact_bits(x1, g.ax, dbits(g.ax.hi0), dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
+    y1 = wrap_exact_bits(y1, g.ay, dbits(g.ay.hi0), dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
+    z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+  }
+  const double u1 = fma(2.0, bx, -u0);
+  const double v1 = fma(2.0, by, -v0);
+  const double w1 = fma(2.0, bz, -w0);
+  const bool fin = finite_bits(x1) && finite_bits(y1) && finite_bits(z1) && finite_bits(u1) &&
+                   finite_bits(v1) && finite_bits(w1);
+  if (bad == 0u && fin) {
+    buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
+    buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;
+    return 0u;
+  }
+  return p < cnt ? 1u : 0u;
 }
 
 }  // namespace b2m
