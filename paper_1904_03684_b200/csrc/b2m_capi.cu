@@ -580,11 +580,13 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   Species& S = ctx->sp[static_cast<size_t>(s)];
   if (offset + n > S.count) return fail(B2M_INVALID_ARGUMENT, "move range beyond species count");
   const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
-  if (ctx->mode == B2M_MODE_STRICT)
-    launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
-  else
-    if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
+  if (ctx->mode == B2M_MODE_STRICT) {
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+                                  ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+  } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream)) {
+    return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+  }
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }
@@ -607,10 +609,11 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
     if ((st = check_params(&mp[s])) != B2M_OK) return st;
     L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
   }
-  if (ctx->mode == B2M_MODE_STRICT)
-    launch_move_strict_batch(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
-                             ctx->stream);
-  else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault,
+  if (ctx->mode == B2M_MODE_STRICT) {
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
+                                  ctx->stream))
+      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+  } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault,
                              ctx->stream))
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaGetLastError());
@@ -660,9 +663,11 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
       B2M_CUDA(ctx, cudaEventRecord(ev[2 * c], ctx->up));
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev[2 * c], 0));
       const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
-      if (ctx->mode == B2M_MODE_STRICT)
-        launch_move_strict(to_dev(ctx->grid), ctx->dE, ctx->dB, L, ctx->fault, ctx->stream);
-      else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
+      if (ctx->mode == B2M_MODE_STRICT) {
+        if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+                                      ctx->stream))
+          return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+      } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
         return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       B2M_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], ctx->stream));
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->down, ev[2 * c + 1], 0));
@@ -890,9 +895,20 @@ b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
     return B2M_OK;
   }
   const int nb = flag_blocks(S.count);
-  launch_move_flag(ctx->mode == B2M_MODE_STRICT, to_dev(ctx->grid), ctx->dE, ctx->dB,
-                   to_fast(ctx->grid), ctx->cells, L, ctx->sl, S.flags, S.blk, ctx->fault,
-                   ctx->stream);
+  if (ctx->mode == B2M_MODE_STRICT) {
+    uint8_t* fl[1] = {S.flags};
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+                                  ctx->stream, &ctx->sl, fl))
+      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+    launch_count_flags(S.flags, S.count, S.blk, ctx->stream);
+  } else {
+    // the production mover writes the flags itself; a light kernel counts them
+    uint8_t* fl[1] = {S.flags};
+    if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream, &ctx->sl,
+                          fl))
+      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+    launch_count_flags(S.flags, S.count, S.blk, ctx->stream);
+  }
   launch_scan_blocks(ctx->scan_temp, ctx->scan_temp_bytes, S.blk, nb, S.totals, ctx->stream);
   launch_scatter_out(L, S.flags, S.blk, S.out[0], S.out[1], S.cap_out, S.holes, ctx->stream);
   B2M_CUDA(ctx, cudaMemcpyAsync(S.totals_h, S.totals, 3 * sizeof(unsigned long long),

@@ -35,8 +35,15 @@ void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B
                               cudaStream_t st);
 // FAST mover on a batch of species spans (one launch).  Returns false when a
 // TMA tensor map cannot be built (driver entry point missing, >2^31 columns).
+struct SlabLaunch;
 bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
-                      int n_spans, FaultWord* fault, cudaStream_t st);
+                      int n_spans, FaultWord* fault, cudaStream_t st,
+                      const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr);
+// STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
+bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st, const SlabLaunch* sl = nullptr,
+                              uint8_t* const* flags = nullptr);
 // Node AoS E/B -> per-cell polynomial coefficients (48 doubles per cell).
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
                            double2* cells, cudaStream_t st);
@@ -73,6 +80,8 @@ void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const dou
                       const SlabLaunch& sl, uint8_t* flags, uint32_t* blk, FaultWord* fault,
                       cudaStream_t st);
 int flag_blocks(uint64_t n);
+// per-block (prev, next, any) counts of an existing flag array
+void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStream_t st);
 // In-place exclusive scan of the 3-wide per-block counts; totals[3] written.
 size_t scan_temp_bytes(int n_blocks);
 void launch_scan_blocks(void* temp, size_t temp_bytes, uint32_t* blk, int n_blocks,

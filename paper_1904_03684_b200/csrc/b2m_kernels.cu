@@ -178,15 +178,24 @@ __global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : B2M_FAST_MINBLOCKS)
   if (tid == 0) tma_wait_all();
 }
 
+// owner_of (runtime.cpp:39-44) with the reference's IEEE division.
+__device__ __forceinline__ int owner_of_slab(double y, const SlabLaunch& sl) {
+  int j = __double2int_rz(__ddiv_rn(y, sl.dy));
+  if (j >= sl.ny) j = sl.ny - 1;
+  if (j < 0) j = 0;
+  return j / sl.slab;
+}
+
 // FAST mover with warp-private TMA pipelines: every warp streams its own
 // tiles of 32*P particles (kWarpStages deep) through its slice of shared
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
 // tensor-map box per tile carries all six SoA arrays in (and one out); the
 // TMA unit zero-fills / clips partial tiles, so there is a single code path.
-template <int P>
+template <int P, bool STRICT>
 __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
     warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
-                     unsigned long long total_tiles, FaultWord* fault) {
+                     const __grid_constant__ SlabLaunch sl, unsigned long long total_tiles,
+                     FaultWord* fault) {
   constexpr int WT = 32 * P;
   constexpr int WARPS = kTileThreads / 32;
   extern __shared__ __align__(128) unsigned char wt_smem[];
@@ -232,21 +241,66 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
     const int cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
     const int st = static_cast<int>(k % kWarpStages);
     mbar_wait(&bar[st], static_cast<uint32_t>((k / kWarpStages) & 1));
-    const FastConst kc = make_const(F.fg, sp);
-    if (B2M_FAST_SEQ) {
+    if (STRICT) {
+      CellCache cc;
+      cc.cell = -1;
+      uint8_t* flags = S.flags[s];
+#pragma unroll 1
+      for (int j = 0; j < P; ++j) {
+        const int p = lane + 32 * j;
+        const unsigned bad = strict_tile_thread_p1<WT>(F.dg, F.E, F.B, sp, buf[st], p, cnt, cc);
+        if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (flags && p < cnt) {
+          int flag = 0;
+          if (!bad) {
+            const int dest = owner_of_slab(buf[st][1][p], sl);
+            if (dest != sl.rank) {
+              if (dest == sl.prev)
+                flag = 1;
+              else if (dest == sl.next)
+                flag = 2;
+              else
+                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+            }
+          }
+          flags[off + p] = static_cast<uint8_t>(flag);
+        }
+      }
+    } else if (B2M_FAST_SEQ) {
+      const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
       // register cell cache (consecutive particles of a cell-ordered species
       // mostly share a cell, so the cache is usually filled once per tile);
       // consecutive lanes read consecutive shared-memory words
       Coef8 K[6];
       int kcell = -1;
+      uint8_t* flags = S.flags[s];
 #pragma unroll 1
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        if (fast_tile_thread_p1<WT>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell))
-          atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        const unsigned bad = fast_tile_thread_p1<WT>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell);
+        if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (flags && p < cnt) {
+          // migration scan fused into the mover (partition_outgoing,
+          // runtime.cpp:46-62): 0 stay, 1 prev, 2 next; a non-neighbour
+          // destination records a CflViolation
+          int flag = 0;
+          if (!bad) {
+            const int dest = owner_of_slab(buf[st][1][p], sl);
+            if (dest != sl.rank) {
+              if (dest == sl.prev)
+                flag = 1;
+              else if (dest == sl.next)
+                flag = 2;
+              else
+                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+            }
+          }
+          flags[off + p] = static_cast<uint8_t>(flag);
+        }
       }
     } else {
+      const FastConst kc = make_const(F.fg, sp);
       const int i0 = P * lane;
       unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
       while (faults) {
@@ -386,6 +440,24 @@ __global__ void __launch_bounds__(kFlagThreads)
     }
     flags[i] = static_cast<uint8_t>(flag);
   }
+  const int c_prev = __syncthreads_count(flag == 1);
+  const int c_next = __syncthreads_count(flag == 2);
+  const int c_any = __syncthreads_count(flag != 0);
+  if (threadIdx.x == 0) {
+    blk[blockIdx.x] = static_cast<uint32_t>(c_prev);
+    blk[n_blocks + blockIdx.x] = static_cast<uint32_t>(c_next);
+    blk[2 * n_blocks + blockIdx.x] = static_cast<uint32_t>(c_any);
+  }
+}
+
+// Per-block counts (prev, next, any) of the flags the mover wrote, for the
+// scan that orders the outboxes (same layout as move_flag_kernel's).
+__global__ void __launch_bounds__(kFlagThreads)
+    count_flags_kernel(const uint8_t* __restrict__ flags, unsigned long long n,
+                       uint32_t* __restrict__ blk, unsigned n_blocks) {
+  const unsigned long long i =
+      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
+  const int flag = i < n ? flags[i] : 0;
   const int c_prev = __syncthreads_count(flag == 1);
   const int c_next = __syncthreads_count(flag == 2);
   const int c_any = __syncthreads_count(flag != 0);
@@ -606,11 +678,9 @@ bool encode_species_map(CUtensorMap* map, const SpeciesLaunch& sp, int box_cols)
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
-                      int n_spans, FaultWord* fault, cudaStream_t st) {
-  TileField F{};
-  F.fg = g;
-  F.cells = cells;
+template <bool STRICT>
+bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                       cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
   constexpr int P = B2M_FAST_PPT;
   constexpr int WT = 32 * P;
   constexpr int smem = (kTileThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
@@ -620,8 +690,10 @@ bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(warp_tile_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P>, kTileThreads, smem);
+    cudaFuncSetAttribute(warp_tile_kernel<P, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT>,
+                                                  kTileThreads, smem);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   for (int base = 0; base < n_spans; base += kMaxTileSpans) {
@@ -631,6 +703,7 @@ bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
       if (sp[s].n == 0) continue;
       if (sp[s].col0 + sp[s].n > 0x7fffffffull) return false;  // 32-bit TMA coordinates
       S.sp[S.n] = sp[s];
+      S.flags[S.n] = flags ? flags[s] : nullptr;
       if (!encode_species_map(&S.tmap[S.n], sp[s], WT)) return false;
       S.tile_start[S.n] = tiles;
       tiles += (sp[s].n + WT - 1) / WT;
@@ -640,10 +713,30 @@ bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaun
     if (S.n == 0) continue;
     const unsigned long long blocks = (tiles + 3) / 4;
     const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
-    warp_tile_kernel<P><<<grid, kTileThreads, smem, st>>>(F, S, tiles, fault);
+    warp_tile_kernel<P, STRICT><<<grid, kTileThreads, smem, st>>>(F, S, sl ? *sl : SlabLaunch{},
+                                                                   tiles, fault);
     note_launch();
   }
   return true;
+}
+
+bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+                      int n_spans, FaultWord* fault, cudaStream_t st, const SlabLaunch* sl,
+                      uint8_t* const* flags) {
+  TileField F{};
+  F.fg = g;
+  F.cells = cells;
+  return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags);
+}
+
+bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
+  TileField F{};
+  F.dg = g;
+  F.E = E;
+  F.B = B;
+  return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags);
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
@@ -704,6 +797,13 @@ void launch_sort_pairs(void* temp, size_t temp_bytes, const uint32_t* kin, uint3
 }
 
 int flag_blocks(uint64_t n) { return static_cast<int>(grid_for(n, kFlagThreads)); }
+
+void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStream_t st) {
+  const unsigned nb = static_cast<unsigned>(flag_blocks(n));
+  if (nb == 0) return;
+  count_flags_kernel<<<nb, kFlagThreads, 0, st>>>(flags, n, blk, nb);
+  note_launch();
+}
 
 void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const double* B,
                       const FastGrid& fg, const double2* cells, const SpeciesLaunch& sp,

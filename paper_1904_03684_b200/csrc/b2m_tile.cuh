@@ -63,6 +63,7 @@ struct alignas(64) TensorSpans {
   CUtensorMap tmap[kMaxTileSpans];
   SpeciesLaunch sp[kMaxTileSpans];
   unsigned long long tile_start[kMaxTileSpans + 1];
+  uint8_t* flags[kMaxTileSpans];  // migration: per-particle destination flag (or null)
   int n;
 };
 
@@ -917,6 +918,42 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
     return 0u;
   }
   return p < cnt ? 1u : 0u;
+}
+
+// ---------------------------------------------------------------------------
+// STRICT, one particle per thread at a time with a register node cache
+// ---------------------------------------------------------------------------
+//
+// Bit-identical to the reference: every round locates with IEEE divisions,
+// computes the 8 weights and accumulates the corners in the reference's
+// order with separate roundings.  The 8 corner nodes' E and B (48 doubles)
+// stay in registers while the particle -- and the lane's next particles --
+// remain in the same cell: a bitwise-identical reuse of values the reference
+// would re-read.
+template <int TILE>
+__device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g,
+                                                          const double* __restrict__ E,
+                                                          const double* __restrict__ B,
+                                                          const SpeciesLaunch& sp,
+                                                          double (*buf)[TILE], int p, int cnt,
+                                                          CellCache& cc) {
+  if (p >= cnt) return 0u;
+  PState P;
+  const double in[6] = {buf[0][p], buf[1][p], buf[2][p], buf[3][p], buf[4][p], buf[5][p]};
+  begin(P, in);
+  for (int r = 0; r < sp.rounds; ++r) {
+    double wt[8];
+    const int cell = strict_locate(P, g, wt);
+    if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
+    if (cell != cc.cell) cache_load_strict(cc, g, E, B, cell);
+    strict_round(P, cc, wt, sp.beta);
+    if (r + 1 < sp.rounds) strict_predict(P, g, sp.dto2);
+  }
+  double out[6];
+  if (!strict_finish(P, g, sp.dt, out)) return 1u;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) buf[a][p] = out[a];
+  return 0u;
 }
 
 }  // namespace b2m
