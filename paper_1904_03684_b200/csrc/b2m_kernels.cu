@@ -191,13 +191,18 @@ __device__ __forceinline__ int owner_of_slab(double y, const SlabLaunch& sl) {
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
 // tensor-map box per tile carries all six SoA arrays in (and one out); the
 // TMA unit zero-fills / clips partial tiles, so there is a single code path.
+#ifdef B2M_MAXNREG
+#define B2M_WARP_BOUNDS __maxnreg__(B2M_MAXNREG)
+#else
+#define B2M_WARP_BOUNDS __launch_bounds__(kWarpThreads, B2M_FAST_MINBLOCKS)
+#endif
 template <int P, bool STRICT>
-__global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
+__global__ void B2M_WARP_BOUNDS
     warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
                      const __grid_constant__ SlabLaunch sl, unsigned long long total_tiles,
                      FaultWord* fault) {
   constexpr int WT = 32 * P;
-  constexpr int WARPS = kTileThreads / 32;
+  constexpr int WARPS = kWarpThreads / 32;
   extern __shared__ __align__(128) unsigned char wt_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto buf = reinterpret_cast<double(*)[6][WT]>(wt_smem) + warp * kWarpStages;
@@ -278,7 +283,11 @@ __global__ void __launch_bounds__(kTileThreads, B2M_FAST_MINBLOCKS)
 #pragma unroll 1
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        const unsigned bad = fast_tile_thread_p1<WT>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell);
+        // pc_iterations = 3 (the reference default) gets a fully unrolled body
+        const unsigned bad =
+            kc.rounds == 3
+                ? fast_tile_thread_p1<WT, 3>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell)
+                : fast_tile_thread_p1<WT, 0>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           // migration scan fused into the mover (partition_outgoing,
@@ -683,7 +692,7 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
                        cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
   constexpr int P = B2M_FAST_PPT;
   constexpr int WT = 32 * P;
-  constexpr int smem = (kTileThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
+  constexpr int smem = (kWarpThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
   static_assert(smem <= 227 * 1024, "warp tiles exceed shared memory");
   static int grid_cap = -1;
   if (grid_cap < 0) {
@@ -693,7 +702,7 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     cudaFuncSetAttribute(warp_tile_kernel<P, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT>,
-                                                  kTileThreads, smem);
+                                                  kWarpThreads, smem);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   for (int base = 0; base < n_spans; base += kMaxTileSpans) {
@@ -711,9 +720,10 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     }
     S.tile_start[S.n] = tiles;
     if (S.n == 0) continue;
-    const unsigned long long blocks = (tiles + 3) / 4;
+    constexpr unsigned long long WPB = kWarpThreads / 32;
+    const unsigned long long blocks = (tiles + WPB - 1) / WPB;
     const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
-    warp_tile_kernel<P, STRICT><<<grid, kTileThreads, smem, st>>>(F, S, sl ? *sl : SlabLaunch{},
+    warp_tile_kernel<P, STRICT><<<grid, kWarpThreads, smem, st>>>(F, S, sl ? *sl : SlabLaunch{},
                                                                    tiles, fault);
     note_launch();
   }

@@ -23,9 +23,16 @@
 
 namespace b2m {
 
-constexpr int kTileThreads = 128;
+#ifndef B2M_TPB
+#define B2M_TPB 128
+#endif
+#ifndef B2M_WARP_STAGES
+#define B2M_WARP_STAGES 3
+#endif
+constexpr int kTileThreads = 128;        // block-tile (STRICT legacy) kernel
+constexpr int kWarpThreads = B2M_TPB;     // warp-tile kernels
 constexpr int kTileStages = 2;
-constexpr int kWarpStages = 3;
+constexpr int kWarpStages = B2M_WARP_STAGES;
 constexpr int kTileMinBlocks = 3;
 // particles per thread: FAST streams coefficients to 4 particles, STRICT
 // keeps a register cell cache shared by 2
@@ -862,7 +869,7 @@ __device__ __forceinline__ unsigned fast_tile_thread(const FastGrid& g,
 // only, so a warp whose lanes disagree never runs two evaluation paths, and
 // performance does not depend on particles sharing cells (no cell sort
 // needed).  L1->register traffic: 384 B per particle per cycle.
-template <int TILE>
+template <int TILE, int ROUNDS = 0>
 __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
                                                         const double2* __restrict__ cells,
                                                         const FastConst& k, double (*buf)[TILE],
@@ -878,7 +885,9 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
   double fx, fy, fz;
   int cell = locate_fast(k, cx0, cy0, cz0, fx, fy, fz);
   double bx = u0, by = v0, bz = w0;
-  for (int r = 0; r < k.rounds; ++r) {
+  const int rounds = ROUNDS > 0 ? ROUNDS : k.rounds;
+#pragma unroll
+  for (int r = 0; r < rounds; ++r) {
     if (cell != kcell) {  // rare: the predictor left the cached cell
       const double2* c = cells + static_cast<long long>(cell) * 24;
 #pragma unroll
@@ -889,7 +898,7 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
 #pragma unroll
     for (int q = 0; q < 6; ++q) F[q] = poly8(K[q], fx, fy, fz);
     implicit_v(k.beta, u0, v0, w0, F, bx, by, bz);
-    if (r + 1 < k.rounds) {
+    if (r + 1 < rounds) {
       double tx = fma(bx, k.dcx, cx0);
       double ty = fma(by, k.dcy, cy0);
       double tz = fma(bz, k.dcz, cz0);
