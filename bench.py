@@ -105,6 +105,23 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": r}
 
 
+def measured_traffic(mode: str):
+    """dram__bytes_read + dram__bytes_write of the mover launch at C2 from the
+    committed `ncu --set full` capture (profiles/r01_c2_bench.json), per launch."""
+    p = os.path.join(ROOT, "profiles", "r01_c2_bench.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    want = "0>(" if mode == "fast" else "1>("
+    for k in d.get("kernels", []):
+        if "warp_tile_kernel" in k["kernel"] and want in k["kernel"]:
+            rd, wr = k["dram__bytes_read.sum"], k["dram__bytes_write.sum"]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            return float(rd[0]) * scale[rd[1]] + float(wr[0]) * scale[wr[1]]
+    return None
+
+
 def host_info():
     model = "unknown"
     try:
@@ -352,7 +369,10 @@ def run_ours(args):
                    "parallelism": "single GPU"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": args.traffic,
+                     "frac": achieved / peak,
+                     "traffic": args.traffic if args.traffic is not None
+                                else measured_traffic(args.mode),
+                     "traffic_source": "ncu --set full, profiles/r01_c2_bench.json",
                      "kernel": "warp_tile_kernel (FAST)" if args.mode == "fast"
                                else "tile_kernel<STRICT>",
                      "kernel_ms": kernel_ms, "bytes_per_launch": alg_bytes,
