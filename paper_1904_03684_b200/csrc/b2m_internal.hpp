@@ -27,12 +27,6 @@ FastGrid to_fast(const b2m_grid& g);
 // ---- launchers (b2m_kernels.cu) -------------------------------------------
 // All launches are asynchronous on `st`.
 
-// STRICT mover on one species span.  field = node AoS E (3*nodes) and B.
-void launch_move_strict(const DevGrid& g, const double* E, const double* B,
-                        const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st);
-void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B,
-                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                              cudaStream_t st);
 // FAST mover on a batch of species spans (one launch).  Returns false when a
 // TMA tensor map cannot be built (driver entry point missing, >2^31 columns).
 struct SlabLaunch;
@@ -73,12 +67,8 @@ struct SlabLaunch {
   int ny;
 };
 
-// FAST or STRICT mover fused with the owner_of scan: writes flags[i]
-// (0 stay, 1 prev, 2 next) and per-block counts blk[3*b + {0:prev,1:next,2:any}].
-void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const double* B,
-                      const FastGrid& fg, const double2* cells, const SpeciesLaunch& sp,
-                      const SlabLaunch& sl, uint8_t* flags, uint32_t* blk, FaultWord* fault,
-                      cudaStream_t st);
+// The movers above, given `sl` and `flags`, also run the owner_of scan and
+// write flags[i] (0 stay, 1 prev, 2 next).
 int flag_blocks(uint64_t n);
 // per-block (prev, next, any) counts of an existing flag array
 void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStream_t st);

@@ -1,13 +1,14 @@
 // b2m_kernels.cu — sm_100a kernels and their launchers.
 //
-//   move_strict_kernel    bit-exact reference mover (kernels.cpp:52-104)
-//   move_fast_kernel      production mover, several species per launch
+//   warp_tile_kernel<PPT, STRICT>  the mover (b2m_tile.cuh): FAST (FMA,
+//                         1e-12 contract) or STRICT (bit-identical to
+//                         kernels.cpp:52-104); optionally fused with the
+//                         y-slab owner scan (partition_outgoing,
+//                         runtime.cpp:46-62) writing migration flags
 //   field_to_cells_kernel node-layout E/B (field_mesh.hpp:13-60) -> per-cell
 //                         trilinear polynomial for the FAST gather
-//   cell_keys / gather    the optional cell-sort pass
-//   move_flag_kernel      mover fused with the y-slab owner scan
-//                         (partition_outgoing, runtime.cpp:46-62)
-//   scatter_out / fill    outbox compaction and hole filling
+//   cell_keys / gather6   the optional cell-sort pass (+ CUB radix sort)
+//   count_flags / scatter_out / fill_*   outbox compaction and hole filling
 //                         (merge_incoming, runtime.cpp:64-76)
 #include <cub/cub.cuh>
 #include <cudaTypedefs.h>
@@ -28,154 +29,6 @@ __device__ __forceinline__ void store6(const SpeciesLaunch& sp, unsigned long lo
                                        const double* p) {
   sp.x[i] = p[0]; sp.y[i] = p[1]; sp.z[i] = p[2];
   sp.u[i] = p[3]; sp.v[i] = p[4]; sp.w[i] = p[5];
-}
-
-// Persistent TMA-staged mover (b2m_tile.cuh).  Tiles of PPT*128 particles
-// are distributed round-robin over the grid; each block keeps kTileStages
-// tiles in flight through shared memory (bulk TMA in, bulk TMA out).
-template <bool STRICT>
-__global__ void __launch_bounds__(kTileThreads, STRICT ? 2 : B2M_FAST_MINBLOCKS)
-    tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TileSpans S,
-                unsigned long long total_tiles, FaultWord* fault) {
-  constexpr int PPT = TileShape<STRICT>::ppt;
-  constexpr int TILE = TileShape<STRICT>::tile;
-  extern __shared__ __align__(128) unsigned char tile_smem[];
-  auto buf = reinterpret_cast<double(*)[6][TILE]>(tile_smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tile_smem + kTileStages * 6 * TILE * 8);
-  const int tid = threadIdx.x;
-  const unsigned long long G = gridDim.x;
-
-  auto resolve = [&](unsigned long long tile, int& s, unsigned long long& off, int& cnt,
-                     bool& full) {
-    s = 0;
-    while (s + 1 < S.n && tile >= S.tile_start[s + 1]) ++s;
-    off = (tile - S.tile_start[s]) * TILE;
-    const unsigned long long left = S.sp[s].n - off;
-    cnt = left < static_cast<unsigned long long>(TILE) ? static_cast<int>(left) : TILE;
-    full = (cnt == TILE) && S.tma_ok[s];
-  };
-  auto issue = [&](unsigned long long k) {  // thread 0
-    const unsigned long long tile = blockIdx.x + k * G;
-    if (tile >= total_tiles) return;
-    int s, cnt;
-    unsigned long long off;
-    bool full;
-    resolve(tile, s, off, cnt, full);
-    const int st = static_cast<int>(k % kTileStages);
-    if (full) {
-      const SpeciesLaunch& sp = S.sp[s];
-      mbar_arrive_tx(&bar[st], 6 * TILE * sizeof(double));
-      const double* src[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-        tma_load_1d(buf[st][a], src[a] + off, TILE * sizeof(double), &bar[st]);
-    } else {
-      mbar_arrive(&bar[st]);
-    }
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < kTileStages; ++s) mbar_init(&bar[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < kTileStages; ++k) issue(k);
-
-  for (unsigned long long k = 0;; ++k) {
-    const unsigned long long tile = blockIdx.x + k * G;
-    if (tile >= total_tiles) break;
-    int s, cnt;
-    unsigned long long off;
-    bool full;
-    resolve(tile, s, off, cnt, full);
-    const int st = static_cast<int>(k % kTileStages);
-    mbar_wait(&bar[st], static_cast<uint32_t>((k / kTileStages) & 1));
-    const SpeciesLaunch& sp = S.sp[s];
-    double* ptr[6] = {sp.x, sp.y, sp.z, sp.u, sp.v, sp.w};
-    const int i0 = PPT * tid;
-    if (STRICT) {
-      bool has[PPT], ok[PPT];
-#pragma unroll
-      for (int i = 0; i < PPT; ++i) has[i] = i0 + i < cnt;
-      double p[PPT][6];
-      if (full) {
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-#pragma unroll
-          for (int i = 0; i < PPT; i += 2) {
-            const double2 v = *reinterpret_cast<const double2*>(&buf[st][a][i0 + i]);
-            p[i][a] = v.x;
-            p[i + 1][a] = v.y;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int i = 0; i < PPT; ++i) p[i][a] = has[i] ? ptr[a][off + i0 + i] : 0.0;
-      }
-      if (has[0]) {
-        push_group<true, PPT>(F, sp, p, has, ok);
-      } else {
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) ok[i] = false;
-      }
-      // a faulting particle keeps its input (the reference leaves it untouched)
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) {
-          if (!(has[i] && ok[i])) continue;
-          if (full)
-            buf[st][a][i0 + i] = p[i][a];
-          else
-            ptr[a][off + i0 + i] = p[i][a];
-        }
-#pragma unroll
-      for (int i = 0; i < PPT; ++i)
-        if (has[i] && !ok[i])
-          atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
-      if (full) fence_proxy_async();
-      __syncthreads();
-    } else {
-      if (!full) {
-        // partial / unaligned tile: stage it through shared memory by hand
-        for (int j = tid; j < cnt; j += kTileThreads)
-#pragma unroll
-          for (int a = 0; a < 6; ++a) buf[st][a][j] = ptr[a][off + j];
-        __syncthreads();
-      }
-      const FastConst kc = make_const(F.fg, sp);
-      unsigned faults = fast_tile_thread<PPT, TILE>(F.fg, F.cells, kc, buf[st], i0, cnt);
-      while (faults) {
-        const int i = __ffs(faults) - 1;
-        faults &= faults - 1;
-        atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
-      }
-      if (full) fence_proxy_async();
-      __syncthreads();
-      if (!full) {
-        // a faulting particle's slot still holds its input: copying the whole
-        // tile back leaves it untouched, as the reference does
-        for (int j = tid; j < cnt; j += kTileThreads)
-#pragma unroll
-          for (int a = 0; a < 6; ++a) ptr[a][off + j] = buf[st][a][j];
-        __syncthreads();
-      }
-    }
-    if (tid == 0) {
-      if (full) {
-#pragma unroll
-        for (int a = 0; a < 6; ++a) tma_store_1d(ptr[a] + off, buf[st][a], TILE * sizeof(double));
-      }
-      tma_commit();
-      // refill the buffer just consumed once its bulk store has read it
-      tma_wait_read<0>();
-      issue(k + kTileStages);
-    }
-  }
-  if (tid == 0) tma_wait_all();
 }
 
 // owner_of (runtime.cpp:39-44) with the reference's IEEE division.
@@ -271,7 +124,7 @@ __global__ void B2M_WARP_BOUNDS
           flags[off + p] = static_cast<uint8_t>(flag);
         }
       }
-    } else if (B2M_FAST_SEQ) {
+    } else {
       const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
       // register cell cache (consecutive particles of a cell-ordered species
@@ -307,15 +160,6 @@ __global__ void B2M_WARP_BOUNDS
           }
           flags[off + p] = static_cast<uint8_t>(flag);
         }
-      }
-    } else {
-      const FastConst kc = make_const(F.fg, sp);
-      const int i0 = P * lane;
-      unsigned faults = fast_tile_thread<P, WT>(F.fg, F.cells, kc, buf[st], i0, cnt);
-      while (faults) {
-        const int i = __ffs(faults) - 1;
-        faults &= faults - 1;
-        atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + i0 + i));
       }
     }
     fence_proxy_async();
@@ -411,56 +255,8 @@ __global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __r
 
 constexpr int kFlagThreads = 256;
 
-// owner_of (runtime.cpp:39-44) with the reference's IEEE division.
-__device__ __forceinline__ int owner_of_dev(double y, const SlabLaunch& sl) {
-  int j = __double2int_rz(__ddiv_rn(y, sl.dy));
-  if (j >= sl.ny) j = sl.ny - 1;
-  if (j < 0) j = 0;
-  return j / sl.slab;
-}
-
-__global__ void __launch_bounds__(kFlagThreads)
-    move_flag_kernel(int strict, const __grid_constant__ DevGrid dg, const double* __restrict__ E,
-                     const double* __restrict__ B, const __grid_constant__ FastGrid fg,
-                     const double2* __restrict__ cells, const __grid_constant__ SpeciesLaunch sp,
-                     const __grid_constant__ SlabLaunch sl, uint8_t* __restrict__ flags,
-                     uint32_t* __restrict__ blk, unsigned n_blocks, FaultWord* fault) {
-  const unsigned long long i =
-      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
-  int flag = 0;
-  if (i < sp.n) {
-    double p[6];
-    load6(sp, i, p);
-    const bool ok = strict ? push_strict(dg, E, B, sp.beta, sp.dt, sp.dto2, sp.rounds, p)
-                           : push_fast(fg, cells, sp.beta, sp.dt, sp.dto2_cell, sp.rounds, p);
-    if (ok) {
-      store6(sp, i, p);
-      const int dest = owner_of_dev(p[1], sl);
-      if (dest != sl.rank) {
-        if (dest == sl.prev)
-          flag = 1;
-        else if (dest == sl.next)
-          flag = 2;
-        else
-          atomicMin(&fault->cfl, fault_key(sp.species, sp.base + i));
-      }
-    } else {
-      atomicMin(&fault->numerical, fault_key(sp.species, sp.base + i));
-    }
-    flags[i] = static_cast<uint8_t>(flag);
-  }
-  const int c_prev = __syncthreads_count(flag == 1);
-  const int c_next = __syncthreads_count(flag == 2);
-  const int c_any = __syncthreads_count(flag != 0);
-  if (threadIdx.x == 0) {
-    blk[blockIdx.x] = static_cast<uint32_t>(c_prev);
-    blk[n_blocks + blockIdx.x] = static_cast<uint32_t>(c_next);
-    blk[2 * n_blocks + blockIdx.x] = static_cast<uint32_t>(c_any);
-  }
-}
-
 // Per-block counts (prev, next, any) of the flags the mover wrote, for the
-// scan that orders the outboxes (same layout as move_flag_kernel's).
+// scan that orders the outboxes.
 __global__ void __launch_bounds__(kFlagThreads)
     count_flags_kernel(const uint8_t* __restrict__ flags, unsigned long long n,
                        uint32_t* __restrict__ blk, unsigned n_blocks) {
@@ -589,72 +385,6 @@ unsigned grid_for(uint64_t n, int threads) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-
-namespace {
-
-template <bool STRICT>
-int tile_grid(unsigned long long total_tiles) {
-  static int blocks_per_sm = -1, sms = 0;
-  if (blocks_per_sm < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(tile_kernel<STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TileShape<STRICT>::smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tile_kernel<STRICT>,
-                                                  kTileThreads, TileShape<STRICT>::smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const unsigned long long g = static_cast<unsigned long long>(sms) * blocks_per_sm;
-  return static_cast<int>(total_tiles < g ? total_tiles : g);
-}
-
-template <bool STRICT>
-void launch_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                  cudaStream_t st) {
-  for (int base = 0; base < n_spans; base += kMaxTileSpans) {
-    TileSpans S{};
-    unsigned long long tiles = 0;
-    for (int s = base; s < n_spans && S.n < kMaxTileSpans; ++s) {
-      if (sp[s].n == 0) continue;
-      S.sp[S.n] = sp[s];
-      S.tile_start[S.n] = tiles;
-      const uintptr_t m =
-          reinterpret_cast<uintptr_t>(sp[s].x) | reinterpret_cast<uintptr_t>(sp[s].y) |
-          reinterpret_cast<uintptr_t>(sp[s].z) | reinterpret_cast<uintptr_t>(sp[s].u) |
-          reinterpret_cast<uintptr_t>(sp[s].v) | reinterpret_cast<uintptr_t>(sp[s].w);
-      S.tma_ok[S.n] = (m & 15u) == 0;
-      tiles += (sp[s].n + TileShape<STRICT>::tile - 1) / TileShape<STRICT>::tile;
-      ++S.n;
-    }
-    S.tile_start[S.n] = tiles;
-    if (S.n == 0) continue;
-    tile_kernel<STRICT><<<tile_grid<STRICT>(tiles), kTileThreads, TileShape<STRICT>::smem, st>>>(
-        F, S, tiles, fault);
-    note_launch();
-  }
-}
-
-}  // namespace
-
-void launch_move_strict(const DevGrid& g, const double* E, const double* B,
-                        const SpeciesLaunch& sp, FaultWord* fault, cudaStream_t st) {
-  TileField F{};
-  F.dg = g;
-  F.E = E;
-  F.B = B;
-  launch_tiles<true>(F, &sp, 1, fault, st);
-}
-
-void launch_move_strict_batch(const DevGrid& g, const double* E, const double* B,
-                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                              cudaStream_t st) {
-  TileField F{};
-  F.dg = g;
-  F.E = E;
-  F.B = B;
-  launch_tiles<true>(F, sp, n_spans, fault, st);
-}
 
 namespace {
 
@@ -812,17 +542,6 @@ void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStr
   const unsigned nb = static_cast<unsigned>(flag_blocks(n));
   if (nb == 0) return;
   count_flags_kernel<<<nb, kFlagThreads, 0, st>>>(flags, n, blk, nb);
-  note_launch();
-}
-
-void launch_move_flag(bool strict, const DevGrid& dg, const double* E, const double* B,
-                      const FastGrid& fg, const double2* cells, const SpeciesLaunch& sp,
-                      const SlabLaunch& sl, uint8_t* flags, uint32_t* blk, FaultWord* fault,
-                      cudaStream_t st) {
-  const unsigned nb = static_cast<unsigned>(flag_blocks(sp.n));
-  if (nb == 0) return;
-  move_flag_kernel<<<nb, kFlagThreads, 0, st>>>(strict ? 1 : 0, dg, E, B, fg, cells, sp, sl,
-                                                 flags, blk, nb, fault);
   note_launch();
 }
 
