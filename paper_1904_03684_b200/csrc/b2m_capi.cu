@@ -117,6 +117,11 @@ struct Species {
   uint64_t n_holes = 0;
   uint64_t pre_count = 0;  // count before the last migration step
   bool migrate_pending = false;
+  // FAST: the field as per-cell polynomials pre-scaled by this species' beta
+  // (qom*dt/2), rebuilt when the field or beta changes
+  double2* cells = nullptr;
+  double cells_beta = 0.0;
+  uint64_t cells_gen = 0;
 };
 
 }  // namespace
@@ -129,8 +134,8 @@ struct b2m_ctx {
   uint64_t n_nodes = 0;
   double* dE = nullptr;
   double* dB = nullptr;
-  double2* cells = nullptr;
   bool field_ready = false;
+  uint64_t field_gen = 0;  // bumped by every field upload
   FaultWord* fault = nullptr;
   FaultWord* fault_h = nullptr;
   cudaStream_t own = nullptr;
@@ -207,6 +212,7 @@ SpeciesLaunch make_launch(b2m_ctx* ctx, int s, const b2m_mover_params& mp, uint6
                           uint64_t n) {
   SpeciesLaunch L{};
   Species& S = ctx->sp[static_cast<size_t>(s)];
+  if (ctx->mode == B2M_MODE_FAST) L.cells = S.cells;  // built by ensure_tables
   L.x = S.a[0] + offset; L.y = S.a[1] + offset; L.z = S.a[2] + offset;
   L.u = S.a[3] + offset; L.v = S.a[4] + offset; L.w = S.a[5] + offset;
   L.n = n;
@@ -222,6 +228,28 @@ SpeciesLaunch make_launch(b2m_ctx* ctx, int s, const b2m_mover_params& mp, uint6
   L.col0 = offset;
   L.stride = S.stride;
   return L;
+}
+
+// FAST: (re)build, in one launch, the beta-scaled cell tables of the given
+// species whose field or beta changed since their last build.
+void ensure_tables(b2m_ctx* ctx, const int* species, const b2m_mover_params* mp, int n) {
+  if (ctx->mode != B2M_MODE_FAST) return;
+  std::vector<double2*> tables;
+  std::vector<double> scale;
+  for (int m = 0; m < n; ++m) {
+    Species& S = ctx->sp[static_cast<size_t>(species[m])];
+    if (S.cells_gen == ctx->field_gen &&
+        std::memcmp(&S.cells_beta, &mp[m].beta, sizeof(double)) == 0)
+      continue;
+    tables.push_back(S.cells);
+    scale.push_back(mp[m].beta);
+    S.cells_gen = ctx->field_gen;
+    S.cells_beta = mp[m].beta;
+  }
+  if (!tables.empty())
+    launch_field_to_cells(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
+                          scale.data(), tables.data(), static_cast<int>(tables.size()),
+                          ctx->stream);
 }
 
 b2m_status check_params(const b2m_mover_params* mp) {
@@ -360,8 +388,6 @@ b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const ui
   b2m_status st;
   if ((st = dalloc(ctx, &ctx->dE, 3 * nodes, "field E")) != B2M_OK) return bail(st);
   if ((st = dalloc(ctx, &ctx->dB, 3 * nodes, "field B")) != B2M_OK) return bail(st);
-  if ((st = dalloc(ctx, &ctx->cells, ncell * (kCellDoubles / 2), "field cells")) != B2M_OK)
-    return bail(st);
   if ((st = dalloc(ctx, &ctx->fault, 1, "fault word")) != B2M_OK) return bail(st);
   if (cudaMallocHost(&ctx->fault_h, sizeof(FaultWord)) != cudaSuccess) {
     cudaGetLastError();
@@ -375,6 +401,8 @@ b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const ui
     double* blk = nullptr;
     if ((st = dalloc(ctx, &blk, 6 * S.stride, "species arrays")) != B2M_OK) return bail(st);
     for (int a = 0; a < 6; ++a) S.a[a] = blk + a * S.stride;
+    if ((st = dalloc(ctx, &S.cells, ncell * (kCellDoubles / 2), "field cells")) != B2M_OK)
+      return bail(st);
   }
   launch_fault_reset(ctx->fault, ctx->stream);
   if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
@@ -448,10 +476,9 @@ b2m_status b2m_host_free(void* ptr) {
   return B2M_OK;
 }
 
+// A new field: the FAST per-species tables are rebuilt on their next move.
 static b2m_status relayout(b2m_ctx* ctx) {
-  launch_field_to_cells(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB, ctx->cells,
-                        ctx->stream);
-  B2M_CUDA(ctx, cudaGetLastError());
+  ++ctx->field_gen;
   ctx->field_ready = true;
   return B2M_OK;
 }
@@ -579,12 +606,13 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
   Species& S = ctx->sp[static_cast<size_t>(s)];
   if (offset + n > S.count) return fail(B2M_INVALID_ARGUMENT, "move range beyond species count");
+  ensure_tables(ctx, &s, mp, 1);
   const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
   if (ctx->mode == B2M_MODE_STRICT) {
     if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-  } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream)) {
+  } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream)) {
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   }
   B2M_CUDA(ctx, cudaGetLastError());
@@ -605,15 +633,19 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
   if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
   const int ns = static_cast<int>(ctx->sp.size());
   std::vector<SpeciesLaunch> L;
+  std::vector<int> all(static_cast<size_t>(ns));
   for (int s = 0; s < ns; ++s) {
     if ((st = check_params(&mp[s])) != B2M_OK) return st;
-    L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
+    all[static_cast<size_t>(s)] = s;
   }
+  ensure_tables(ctx, all.data(), mp, ns);
+  for (int s = 0; s < ns; ++s)
+    L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
   if (ctx->mode == B2M_MODE_STRICT) {
     if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-  } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, L.data(), ns, ctx->fault,
+  } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault,
                              ctx->stream))
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaGetLastError());
@@ -650,6 +682,9 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
   cudaEvent_t* ev = ctx->pipe_ev.data();
   B2M_CUDA(ctx, cudaEventRecord(ev[2 * n_chunks], ctx->stream));
   B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->up, ev[2 * n_chunks], 0));
+  std::vector<int> all(static_cast<size_t>(n_species));
+  for (int s = 0; s < n_species; ++s) all[static_cast<size_t>(s)] = s;
+  ensure_tables(ctx, all.data(), mp, n_species);
   size_t c = 0;
   for (int s = 0; s < n_species; ++s) {
     Species& S = ctx->sp[static_cast<size_t>(s)];
@@ -667,7 +702,7 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
         if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
                                       ctx->stream))
           return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-      } else if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream))
+      } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream))
         return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       B2M_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], ctx->stream));
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->down, ev[2 * c + 1], 0));
@@ -887,6 +922,7 @@ b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
   if (!ctx->slab_on) return fail(B2M_CONFIG_ERROR, "move_migrate: call b2m_slab_config first");
   if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
   Species& S = ctx->sp[static_cast<size_t>(s)];
+  ensure_tables(ctx, &s, mp, 1);
   const SpeciesLaunch L = make_launch(ctx, s, *mp, 0, S.count);
   S.pre_count = S.count;
   S.migrate_pending = true;
@@ -904,7 +940,7 @@ b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
   } else {
     // the production mover writes the flags itself; a light kernel counts them
     uint8_t* fl[1] = {S.flags};
-    if (!launch_move_fast(to_fast(ctx->grid), ctx->cells, &L, 1, ctx->fault, ctx->stream, &ctx->sl,
+    if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, &ctx->sl,
                           fl))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
     launch_count_flags(S.flags, S.count, S.blk, ctx->stream);

@@ -30,7 +30,7 @@ FastGrid to_fast(const b2m_grid& g);
 // FAST mover on a batch of species spans (one launch).  Returns false when a
 // TMA tensor map cannot be built (driver entry point missing, >2^31 columns).
 struct SlabLaunch;
-bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
+bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st,
                       const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
@@ -38,9 +38,13 @@ bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                               cudaStream_t st, const SlabLaunch* sl = nullptr,
                               uint8_t* const* flags = nullptr);
-// Node AoS E/B -> per-cell polynomial coefficients (48 doubles per cell).
+// Node AoS E/B -> per-cell polynomial coefficients of (scale[m]*E,
+// scale[m]*B) into tables[m] (48 doubles per cell), one field read per
+// kMaxTables tables.
+constexpr int kMaxTables = 8;
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
-                           double2* cells, cudaStream_t st);
+                           const double* scale, double2* const* tables, int n_tables,
+                           cudaStream_t st);
 // Reset the fault words to "clean".
 void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 

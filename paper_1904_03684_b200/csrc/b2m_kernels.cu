@@ -85,7 +85,8 @@ __global__ void B2M_WARP_BOUNDS
   if (lane == 0) {
     for (int s = 0; s < kWarpStages; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
-    for (int k = 0; k < kWarpStages; ++k) issue(k);
+    for (int k = 0; k < kWarpStages; ++k) issue(k);  // stages 0..S-1 (tile S-1 is refilled
+                                                     // into stage S-1 only after tile 0)
   }
   __syncwarp();
 
@@ -139,8 +140,8 @@ __global__ void B2M_WARP_BOUNDS
         // pc_iterations = 3 (the reference default) gets a fully unrolled body
         const unsigned bad =
             kc.rounds == 3
-                ? fast_tile_thread_p1<WT, 3>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell)
-                : fast_tile_thread_p1<WT, 0>(F.fg, F.cells, kc, buf[st], p, cnt, K, kcell);
+                ? fast_tile_thread_p1<WT, 3>(F.fg, sp.cells, kc, buf[st], p, cnt, K, kcell)
+                : fast_tile_thread_p1<WT, 0>(F.fg, sp.cells, kc, buf[st], p, cnt, K, kcell);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           // migration scan fused into the mover (partition_outgoing,
@@ -167,45 +168,57 @@ __global__ void B2M_WARP_BOUNDS
     if (lane == 0) {
       tma_store_2d(&S.tmap[s], static_cast<int>(sp.col0 + off), 0, buf[st], stream_pol);
       tma_commit();
-      tma_wait_read<0>();
-      issue(k + kWarpStages);
+      // refill the stage of tile k-1, whose store was issued a whole tile ago
+      // (its shared-memory read is long done): no wait on the store just issued
+      if (k > 0) {
+        tma_wait_read<1>();
+        issue(k - 1 + kWarpStages);
+      }
     }
     __syncwarp();
   }
   if (lane == 0) tma_wait_all();
 }
 
-// One thread per cell: 8 corners x 6 components -> 48 coefficients.
+// Per-cell trilinear polynomials of (beta*E, beta*B) for up to kMaxTables
+// species at once (one read of the field).  Thread = (cell, component q):
+// the 8 corner values -> 4 {P, Q} pairs (b2m_mover.cuh, kCellDoubles), so
+// consecutive threads write consecutive 64-byte pieces of the tables.
+struct CellTables {
+  double2* out[kMaxTables];
+  double scale[kMaxTables];
+  int n;
+};
+
 __global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __restrict__ E,
-                                      const double* __restrict__ B, double2* __restrict__ cells) {
-  const long long cell = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+                                      const double* __restrict__ B,
+                                      const __grid_constant__ CellTables T) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long ncell = static_cast<long long>(nx) * ny * nz;
-  if (cell >= ncell) return;
+  if (t >= 6 * ncell) return;
+  const long long cell = t / 6;
+  const int q = static_cast<int>(t % 6);
   const int i = static_cast<int>(cell % nx);
   const int j = static_cast<int>((cell / nx) % ny);
   const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
   const long long sx = nx + 1, sy = ny + 1;
-  long long node[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int di = c & 1, dj = (c >> 1) & 1, dk = (c >> 2) & 1;
-    node[c] = (i + di) + sx * ((j + dj) + sy * (k + dk));
-  }
-  double2* out = cells + cell * (kCellDoubles / 2);
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    const double* F = q < 3 ? E : B;
-    const int a = q % 3;
-    // f<di dj dk>
-    const double f000 = F[3 * node[0] + a], f100 = F[3 * node[1] + a];
-    const double f010 = F[3 * node[2] + a], f110 = F[3 * node[3] + a];
-    const double f001 = F[3 * node[4] + a], f101 = F[3 * node[5] + a];
-    const double f011 = F[3 * node[6] + a], f111 = F[3 * node[7] + a];
-    const double d00 = f001 - f000, d10 = f101 - f100, d01 = f011 - f010, d11 = f111 - f110;
-    out[4 * q + 0] = make_double2(f000, d00);
-    out[4 * q + 1] = make_double2(f010 - f000, d01 - d00);
-    out[4 * q + 2] = make_double2(f100 - f000, d10 - d00);
-    out[4 * q + 3] = make_double2((f110 - f100) - (f010 - f000), (d11 - d10) - (d01 - d00));
+  const double* F = (q < 3 ? E : B) + q % 3;
+  auto f = [&](int di, int dj, int dk) {
+    return __ldg(F + 3 * ((i + di) + sx * ((j + dj) + sy * (k + dk))));
+  };
+  // f<di dj dk>
+  const double f000 = f(0, 0, 0), f100 = f(1, 0, 0), f010 = f(0, 1, 0), f110 = f(1, 1, 0);
+  const double f001 = f(0, 0, 1), f101 = f(1, 0, 1), f011 = f(0, 1, 1), f111 = f(1, 1, 1);
+  for (int m = 0; m < T.n; ++m) {
+    const double c = T.scale[m];
+    const double g000 = c * f000, g100 = c * f100, g010 = c * f010, g110 = c * f110;
+    const double g001 = c * f001, g101 = c * f101, g011 = c * f011, g111 = c * f111;
+    const double d00 = g001 - g000, d10 = g101 - g100, d01 = g011 - g010, d11 = g111 - g110;
+    double2* out = T.out[m] + cell * (kCellDoubles / 2) + 4 * q;
+    out[0] = make_double2(g000, d00);
+    out[1] = make_double2(g010 - g000, d01 - d00);
+    out[2] = make_double2(g100 - g000, d10 - d00);
+    out[3] = make_double2((g110 - g100) - (g010 - g000), (d11 - d10) - (d01 - d00));
   }
 }
 
@@ -460,12 +473,10 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
   return true;
 }
 
-bool launch_move_fast(const FastGrid& g, const double2* cells, const SpeciesLaunch* sp,
-                      int n_spans, FaultWord* fault, cudaStream_t st, const SlabLaunch* sl,
-                      uint8_t* const* flags) {
+bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                      cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
   TileField F{};
   F.fg = g;
-  F.cells = cells;
   return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags);
 }
 
@@ -480,10 +491,18 @@ bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
-                           double2* cells, cudaStream_t st) {
+                           const double* scale, double2* const* tables, int n_tables,
+                           cudaStream_t st) {
   const long long ncell = static_cast<long long>(nx) * ny * nz;
-  field_to_cells_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(nx, ny, nz, E, B, cells);
-  note_launch();
+  for (int base = 0; base < n_tables; base += kMaxTables) {
+    CellTables T{};
+    for (T.n = 0; T.n < kMaxTables && base + T.n < n_tables; ++T.n) {
+      T.out[T.n] = tables[base + T.n];
+      T.scale[T.n] = scale[base + T.n];
+    }
+    field_to_cells_kernel<<<grid_for(6 * ncell, 192), 192, 0, st>>>(nx, ny, nz, E, B, T);
+    note_launch();
+  }
 }
 
 void launch_fault_reset(FaultWord* fault, cudaStream_t st) {

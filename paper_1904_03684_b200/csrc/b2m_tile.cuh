@@ -126,7 +126,6 @@ __device__ __forceinline__ void fence_proxy_async() {
 struct TileField {
   FastGrid fg;
   DevGrid dg;
-  const double2* cells;  // FAST
   const double* E;       // STRICT
   const double* B;
 };
@@ -242,7 +241,7 @@ struct FastConst {
   unsigned long long lxb, lyb, lzb;       // bits of lx, ly, lz
   int nx1, ny1, nz1;                      // n - 1
   int nx, nxny;
-  double beta, dt, dcx, dcy, dcz;         // dcx = 0.5*dt/dx
+  double dt, dcx, dcy, dcz;               // dcx = 0.5*dt/dx
   int rounds;
 };
 
@@ -255,7 +254,7 @@ __device__ __forceinline__ FastConst make_const(const FastGrid& g, const Species
   k.lxb = dbits(g.lx); k.lyb = dbits(g.ly); k.lzb = dbits(g.lz);
   k.nx1 = g.nx - 1; k.ny1 = g.ny - 1; k.nz1 = g.nz - 1;
   k.nx = g.nx; k.nxny = g.nx * g.ny;
-  k.beta = sp.beta; k.dt = sp.dt;
+  k.dt = sp.dt;
   k.dcx = sp.dto2_cell[0]; k.dcy = sp.dto2_cell[1]; k.dcz = sp.dto2_cell[2];
   k.rounds = sp.rounds;
   return k;
@@ -275,22 +274,21 @@ __device__ __forceinline__ int locate_fast(const FastConst& k, double tx, double
   return i + k.nx * j + k.nxny * m;
 }
 
-// Implicit velocity (kernels.cpp:83-90), FMA form: vt = v0 + beta*E,
+// Implicit velocity (kernels.cpp:83-90), FMA form, from the gathered
+// F = (beta*E, beta*B) (the cell table is pre-scaled): vt = v0 + beta*E,
 // W = beta*B, vbar = (vt + vt x W + (vt.W) W) / (1 + |W|^2).  The reciprocal
-// is the MUFU.RCP64H seed (~2^-23) refined by two Newton steps (~2^-92).
-__device__ __forceinline__ void implicit_v(double beta, double u0, double v0, double w0,
-                                           const double* F, double& bx, double& by, double& bz) {
-  const double ox = beta * F[3], oy = beta * F[4], oz = beta * F[5];
-  const double vtx = fma(beta, F[0], u0);
-  const double vty = fma(beta, F[1], v0);
-  const double vtz = fma(beta, F[2], w0);
+// is the MUFU.RCP64H seed (~2^-23) refined by one third-order step (~2^-66).
+__device__ __forceinline__ void implicit_v(double u0, double v0, double w0, const double* F,
+                                           double& bx, double& by, double& bz) {
+  const double ox = F[3], oy = F[4], oz = F[5];
+  const double vtx = u0 + F[0];
+  const double vty = v0 + F[1];
+  const double vtz = w0 + F[2];
   const double den = 1.0 + fma(oz, oz, fma(oy, oy, ox * ox));
   double rc;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
-  double e = fma(-den, rc, 1.0);
-  rc = fma(rc, e, rc);
-  e = fma(-den, rc, 1.0);
-  rc = fma(rc, e, rc);
+  const double e = fma(-den, rc, 1.0);
+  rc = fma(rc, fma(e, e, e), rc);  // rc * (1 + e + e^2)
   const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
   bx = fma(vdot, ox, fma(vty, oz, fma(-vtz, oy, vtx))) * rc;
   by = fma(vdot, oy, fma(vtz, ox, fma(-vtx, oz, vty))) * rc;
@@ -343,7 +341,7 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
     double F[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) F[q] = poly8(K[q], fx, fy, fz);
-    implicit_v(k.beta, u0, v0, w0, F, bx, by, bz);
+    implicit_v(u0, v0, w0, F, bx, by, bz);
     if (r + 1 < rounds) {
       double tx = fma(bx, k.dcx, cx0);
       double ty = fma(by, k.dcy, cy0);
