@@ -67,39 +67,40 @@ __global__ void B2M_WARP_BOUNDS
   const unsigned long long GW = static_cast<unsigned long long>(gridDim.x) * WARPS;
   const uint64_t stream_pol = policy_evict_first();
 
-  auto species_of = [&](unsigned long long tile) {
-    int s = 0;
+  // Tiles are visited in increasing order, so the span index only advances.
+  auto advance_span = [&](int& s, unsigned long long tile) {
     while (s + 1 < S.n && tile >= S.tile_start[s + 1]) ++s;
-    return s;
   };
-  auto issue = [&](unsigned long long k) {  // lane 0
-    const unsigned long long tile = gw + k * GW;
-    if (tile >= total_tiles) return;
-    const int s = species_of(tile);
-    const int st = static_cast<int>(k % kWarpStages);
-    const int c0 = static_cast<int>(S.sp[s].col0 + (tile - S.tile_start[s]) * WT);
-    mbar_arrive_tx(&bar[st], 6 * WT * sizeof(double));
-    tma_load_2d(buf[st], &S.tmap[s], c0, 0, &bar[st], stream_pol);
+  // lane 0's load cursor: the next tile to load, its span and ring stage
+  unsigned long long ld_tile = gw;
+  int ld_span = 0, ld_stage = 0;
+  auto issue = [&]() {  // lane 0
+    if (ld_tile >= total_tiles) return;
+    advance_span(ld_span, ld_tile);
+    const int c0 =
+        static_cast<int>(S.sp[ld_span].col0 + (ld_tile - S.tile_start[ld_span]) * WT);
+    mbar_arrive_tx(&bar[ld_stage], 6 * WT * sizeof(double));
+    tma_load_2d(buf[ld_stage], &S.tmap[ld_span], c0, 0, &bar[ld_stage], stream_pol);
+    ld_tile += GW;
+    ld_stage = ld_stage + 1 == kWarpStages ? 0 : ld_stage + 1;
   };
 
   if (lane == 0) {
     for (int s = 0; s < kWarpStages; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
-    for (int k = 0; k < kWarpStages; ++k) issue(k);  // stages 0..S-1 (tile S-1 is refilled
-                                                     // into stage S-1 only after tile 0)
+    for (int k = 0; k < kWarpStages; ++k) issue();  // fill every stage
   }
   __syncwarp();
 
-  for (unsigned long long k = 0;; ++k) {
-    const unsigned long long tile = gw + k * GW;
-    if (tile >= total_tiles) break;
-    const int s = species_of(tile);
+  int s = 0, st = 0;
+  uint32_t phase = 0;
+  for (unsigned long long tile = gw, k = 0; tile < total_tiles; tile += GW, ++k) {
+    advance_span(s, tile);
     const SpeciesLaunch& sp = S.sp[s];
     const unsigned long long off = (tile - S.tile_start[s]) * WT;
     const unsigned long long left = sp.n - off;
     const int cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
-    const int st = static_cast<int>(k % kWarpStages);
-    mbar_wait(&bar[st], static_cast<uint32_t>((k / kWarpStages) & 1));
+    mbar_wait(&bar[st], phase);
     if (STRICT) {
       CellCache cc;
       cc.cell = -1;
@@ -172,10 +173,14 @@ __global__ void B2M_WARP_BOUNDS
       // (its shared-memory read is long done): no wait on the store just issued
       if (k > 0) {
         tma_wait_read<1>();
-        issue(k - 1 + kWarpStages);
+        issue();  // tile k-1+stages into the stage of tile k-1
       }
     }
     __syncwarp();
+    if (++st == kWarpStages) {
+      st = 0;
+      phase ^= 1u;
+    }
   }
   if (lane == 0) tma_wait_all();
 }
