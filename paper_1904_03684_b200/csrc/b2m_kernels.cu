@@ -44,6 +44,10 @@ __device__ __forceinline__ int owner_of_slab(double y, const SlabLaunch& sl) {
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
 // tensor-map box per tile carries all six SoA arrays in (and one out); the
 // TMA unit zero-fills / clips partial tiles, so there is a single code path.
+#ifndef B2M_J_UNROLL
+#define B2M_J_UNROLL 1
+#endif
+constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
 #ifdef B2M_MAXNREG
 #define B2M_WARP_BOUNDS __maxnreg__(B2M_MAXNREG)
 #else
@@ -135,7 +139,7 @@ __global__ void B2M_WARP_BOUNDS
       Coef8 K[6];
       int kcell = -1;
       uint8_t* flags = S.flags[s];
-#pragma unroll 1
+#pragma unroll (kJUnroll)
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
         // pc_iterations = 3 (the reference default) gets a fully unrolled body
