@@ -312,6 +312,27 @@ def run_ours(args):
         strict_value = n_total / (a.elapsed_time(b) / 3 * 1e-3) / 1e6
         store.sync()
         store.set_mode(args.mode)
+
+    # Moment deposition (deposit_moments, kernels.cpp:147-183)
+    # of the resident state after the timed steps, rho + J for all species
+    moments = None
+    if args.moments:
+        store.moments_zero(False)
+        for s, b in enumerate(batches):
+            store.deposit(s, b.q_per_particle)  # warm-up
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        store.moments_zero(False)
+        a.record()
+        for s, b in enumerate(batches):
+            store.deposit(s, b.q_per_particle)
+        b_.record()
+        torch.cuda.synchronize()
+        store.sync()
+        dep_ms = a.elapsed_time(b_)
+        moments = {"value": n_total / (dep_ms * 1e-3) / 1e6, "unit": "MPA/s", "ms": dep_ms,
+                   "what": "deposit_moments rho+J, all species, device-resident state after "
+                           "the timed steps (cell-sorted every --resort steps)",
+                   "hbm_frac": 48 * n_total / (dep_ms * 1e-3) / 1e9 / load_peaks()[0]}
     store.close()
 
     peak, peak_src = load_peaks()
@@ -382,6 +403,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "strict_value": strict_value,
+        "moments": moments,
         "init_s": t_init,
     }
     print(json.dumps(line), flush=True)
@@ -401,6 +423,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--strict-too", type=int, default=1)
+    ap.add_argument("--moments", type=int, default=1)
     ap.add_argument("--field", default="gem", choices=["gem", "gem+E"],
                     help="gem: the reference's init_gem field (E=0, static B) that its own "
                          "benchmark moves particles in; gem+E: add the gem_like_field E")

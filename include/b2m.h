@@ -184,6 +184,28 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
  * runtime.cpp:64-76). */
 b2m_status b2m_sort_species(b2m_ctx* ctx, int s);
 
+/* ---- moments (deposit_moments, kernels.cpp:147-183; MomentMesh
+ * kernels.hpp:54-69) -------------------------------------------------------
+ * The context owns one device moment mesh of nx*ny*nz periodic nodes (index
+ * i + nx*(j + ny*k)): rho, jx, jy, jz and, with pressure, pxx, pxy, pxz, pyy,
+ * pyz, pzz.  b2m_moments_zero (re)allocates it for `with_pressure` and zeroes
+ * it (MomentMesh::make / zero); b2m_deposit adds species s's particles with
+ * charge q_per_particle each (asynchronous; a particle outside the domain is
+ * reported by b2m_sync as B2M_DOMAIN_ERROR, the reference's grid_cell_of
+ * DomainError); b2m_moments_download copies the 4 (or 10) arrays to host
+ * out[0..] and synchronizes.  Sums are in a different order than the
+ * reference's particle order: equal to rounding. */
+b2m_status b2m_moments_zero(b2m_ctx* ctx, int with_pressure);
+b2m_status b2m_deposit(b2m_ctx* ctx, int s, double q_per_particle);
+b2m_status b2m_moments_download(b2m_ctx* ctx, double* const* out, int n_arrays);
+/* One-shot pic::deposit_moments for host arrays: ADDS the n particles'
+ * moments into out[0..3] (+ out[4..9] with pressure), nx*ny*nz each.
+ * B2M_DOMAIN_ERROR (nothing added) if a particle lies outside the domain. */
+b2m_status b2m_deposit_moments_host(const b2m_grid* g, const double* x, const double* y,
+                                    const double* z, const double* u, const double* v,
+                                    const double* w, uint64_t n, double q_per_particle,
+                                    int with_pressure, double* const* out);
+
 /* Wait for all enqueued work (CommandQueue::synchronize,
  * command_queue.cpp:45-49).  Returns B2M_NUMERICAL_FAULT with the species and
  * particle index of the first recorded fault (message text as

@@ -87,6 +87,9 @@ def port() -> C.CDLL:
         lib.or_fill_species_g.restype = None
         lib.or_fill_species_g.argtypes = [C.c_int] * 3 + [C.c_double] * 3 + \
             [C.c_int, C.c_int, _u64, C.c_double, _dp, _dp, _u64, _u64] + [_dp] * 6
+        lib.or_deposit_moments_g.restype = C.c_int64
+        lib.or_deposit_moments_g.argtypes = [_dp] * 6 + [_u64] + [C.c_int] * 3 + \
+            [C.c_double] * 3 + [C.c_double, C.c_int, C.POINTER(_dp)]
         lib.or_sheet_count_g.restype = _u64
         lib.or_sheet_count_g.argtypes = [C.c_int] * 3 + [C.c_double] * 4 + [C.c_int]
         _port = lib
@@ -100,6 +103,18 @@ def port_move_batch(p6, E, B, grid, dt, qom, pc) -> int:
     n = len(p6[0])
     return int(port().or_move_batch_g(*[_ptr(a) for a in p6], n, _ptr(E), _ptr(B),
                                       nx, ny, nz, lx, ly, lz, dt, qom, pc))
+
+
+def port_deposit_moments(p6, grid, qp: float, with_pressure: bool = False):
+    """The C restatement of deposit_moments; returns [rho, jx, jy, jz (, p..)]
+    or raises OracleError(DomainError) naming the first particle outside."""
+    out = [np.zeros(grid[0] * grid[1] * grid[2]) for _ in range(10 if with_pressure else 4)]
+    ptrs = (_dp * 10)(*[_ptr(a) for a in out] + [None] * (10 - len(out)))
+    bad = port().or_deposit_moments_g(*[_ptr(np.ascontiguousarray(a)) for a in p6], len(p6[0]),
+                                      *grid, qp, int(with_pressure), ptrs)
+    if bad >= 0:
+        raise OracleError(2, f"particle {bad} outside the domain")
+    return out
 
 
 def port_wrap_len(v: float, l: float) -> float:
@@ -215,6 +230,8 @@ def _bind_ref(lib: C.CDLL) -> C.CDLL:
     lib.ref_aggregate_runs.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp] + eb
     lib.ref_decompose.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] + eb
     lib.ref_owner_of.argtypes = [C.c_double] + g6 + [C.c_int]
+    lib.ref_deposit_moments.argtypes = [_dp] * 6 + [_u64] + g6 + [C.c_double, C.c_int,
+                                                                   C.POINTER(_dp)] + eb
     return lib
 
 
@@ -239,6 +256,26 @@ def ref_move_batch(p6, E, B, grid, dt, qom, pc, threads: int = 0) -> None:
         st = ref().ref_move_batch(*[_ptr(a) for a in p6], n, _ptr(E), _ptr(B), *grid,
                                   dt, qom, pc, buf, 512)
     _check(st, buf)
+
+
+MOMENT_NAMES = ("rho", "jx", "jy", "jz", "pxx", "pxy", "pxz", "pyy", "pyz", "pzz")
+
+
+def _moment_arrays(grid, with_pressure):
+    nx, ny, nz = grid[:3]
+    return [np.zeros(nx * ny * nz) for _ in range(10 if with_pressure else 4)]
+
+
+def ref_deposit_moments(p6, grid, qp: float, with_pressure: bool = False):
+    """pic::deposit_moments (kernels.cpp:147-183) of six float64 arrays onto
+    a fresh MomentMesh; returns [rho, jx, jy, jz (, pxx .. pzz)]."""
+    out = _moment_arrays(grid, with_pressure)
+    ptrs = (_dp * 10)(*[_ptr(a) for a in out] + [None] * (10 - len(out)))
+    buf = _errbuf()
+    st = ref().ref_deposit_moments(*[_ptr(np.ascontiguousarray(a)) for a in p6], len(p6[0]),
+                                   *grid, qp, int(with_pressure), ptrs, buf, 512)
+    _check(st, buf)
+    return out
 
 
 def ref_wrap_len(v: float, l: float) -> float:

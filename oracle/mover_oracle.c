@@ -162,6 +162,54 @@ int64_t or_move_batch_g(double* x, double* y, double* z, double* u, double* v, d
 
 /* ---- GEM input generation (init.cpp, rng.hpp) ---------------------------- */
 
+/* kernels.cpp:147-183 deposit_moments: every particle scatters
+ * wq = ((q/V * wx) * wy) * wz onto the 8 corners of its cell, corner order
+ * c = di + 2dj + 4dk, the upper corners wrapping onto node 0 (periodic, nodes
+ * == cells, index i + nx*(j + ny*k), kernels.hpp:63-65); rho += wq,
+ * j += wq*u, and (with_pressure) p_ab += (wq*u_a)*u_b, in particle order.
+ * out[0..3] = rho, jx, jy, jz; out[4..9] = pxx, pxy, pxz, pyy, pyz, pzz.
+ * Returns -1, or the index of the first particle outside the domain (the
+ * reference's grid_cell_of throws DomainError there). */
+int64_t or_deposit_moments_g(const double* x, const double* y, const double* z, const double* u,
+                             const double* v, const double* w, uint64_t n, int nx, int ny,
+                             int nz, double lx, double ly, double lz, double qp,
+                             int with_pressure, double* const* out) {
+  or_grid g;
+  or_grid_make(&g, nx, ny, nz, lx, ly, lz);
+  const double inv_vol = 1.0 / (g.dx * g.dy * g.dz);
+  for (uint64_t p = 0; p < n; ++p) {
+    int c[3];
+    double f[3];
+    if (or_grid_cell_of(&g, x[p], y[p], z[p], c, f) != 0) return (int64_t)p;
+    const double wx[2] = {1.0 - f[0], f[0]};
+    const double wy[2] = {1.0 - f[1], f[1]};
+    const double wz[2] = {1.0 - f[2], f[2]};
+    const int ii[2] = {c[0], c[0] + 1 == nx ? 0 : c[0] + 1};
+    const int jj[2] = {c[1], c[1] + 1 == ny ? 0 : c[1] + 1};
+    const int kk[2] = {c[2], c[2] + 1 == nz ? 0 : c[2] + 1};
+    const double ux = u[p], uy = v[p], uz = w[p];
+    const double qv = qp * inv_vol;
+    for (int corner = 0; corner < 8; ++corner) {
+      const int di = corner & 1, dj = (corner >> 1) & 1, dk = (corner >> 2) & 1;
+      const double wq = qv * wx[di] * wy[dj] * wz[dk];
+      const int64_t idx = (int64_t)ii[di] + (int64_t)nx * ((int64_t)jj[dj] + (int64_t)ny * kk[dk]);
+      out[0][idx] += wq;
+      out[1][idx] += wq * ux;
+      out[2][idx] += wq * uy;
+      out[3][idx] += wq * uz;
+      if (with_pressure) {
+        out[4][idx] += wq * ux * ux;
+        out[5][idx] += wq * ux * uy;
+        out[6][idx] += wq * ux * uz;
+        out[7][idx] += wq * uy * uy;
+        out[8][idx] += wq * uy * uz;
+        out[9][idx] += wq * uz * uz;
+      }
+    }
+  }
+  return -1;
+}
+
 /* rng.hpp:12-56 CounterRng: splitmix64 stream keyed by (seed, stream). */
 typedef struct {
   uint64_t state;

@@ -147,6 +147,25 @@ int ref_move_batch_mt(double* x, double* y, double* z, double* u, double* v, dou
   SHIM_CATCH
 }
 
+// pic::deposit_moments (kernels.cpp:147-183) on a ParticleBatch built from the
+// six arrays; out[0..3] rho,jx,jy,jz (+ out[4..9] pressure) are ACCUMULATED.
+int ref_deposit_moments(const double* x, const double* y, const double* z, const double* u,
+                        const double* v, const double* w, std::uint64_t n, int nx, int ny,
+                        int nz, double lx, double ly, double lz, double qp, int with_pressure,
+                        double* const* out, char* err, int errlen) {
+  SHIM_TRY
+  const Grid g = Grid::make(nx, ny, nz, lx, ly, lz);
+  ParticleBatch b(0, 1.0, qp, std::size_t(n));
+  for (std::uint64_t i = 0; i < n; ++i) b.append(x[i], y[i], z[i], u[i], v[i], w[i]);
+  MomentMesh m = MomentMesh::make(g, with_pressure != 0);
+  deposit_moments(b, g, m);
+  const std::vector<double>* arr[10] = {&m.rho, &m.jx, &m.jy, &m.jz, &m.pxx,
+                                        &m.pxy, &m.pxz, &m.pyy, &m.pyz, &m.pzz};
+  for (int a = 0; a < (with_pressure ? 10 : 4); ++a)
+    for (std::size_t i = 0; i < arr[a]->size(); ++i) out[a][i] += (*arr[a])[i];
+  SHIM_CATCH
+}
+
 int ref_wrap_len(double v, double l, double* out) {
   *out = wrap_len(v, l);
   return kOk;

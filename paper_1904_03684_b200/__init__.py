@@ -7,8 +7,9 @@ include/b2m.h).
 """
 from .errors import (AllocError, CflViolation, ConfigError, DomainError, EngineFault,
                      MetricError, MinipicError, NumericalFault)
-from .mover import FieldMesh, Grid, MoverParams, ParticleBatch, move_batch
+from .mover import (FieldMesh, Grid, MomentMesh, MoverParams, ParticleBatch, deposit_moments,
+                    move_batch)
 
 __all__ = ["AllocError", "CflViolation", "ConfigError", "DomainError", "EngineFault",
-           "MetricError", "MinipicError", "NumericalFault", "FieldMesh", "Grid", "MoverParams",
-           "ParticleBatch", "move_batch"]
+           "MetricError", "MinipicError", "NumericalFault", "FieldMesh", "Grid", "MomentMesh",
+           "MoverParams", "ParticleBatch", "deposit_moments", "move_batch"]

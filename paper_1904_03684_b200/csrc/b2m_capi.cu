@@ -155,6 +155,10 @@ struct b2m_ctx {
   // host pipeline (b2m_run_mover_host)
   cudaStream_t up = nullptr, down = nullptr;
   std::vector<cudaEvent_t> pipe_ev;
+  // moment mesh (b2m_moments_zero): 4 or 10 arrays of nx*ny*nz
+  double* mom[10] = {};
+  int mom_arrays = 0;
+  bool mom_pressure = false;
   // slab partition
   bool slab_on = false;
   SlabLaunch sl{};
@@ -776,6 +780,16 @@ b2m_status b2m_sync(b2m_ctx* ctx, int* bad_species, int64_t* first_bad) {
     ctx->poison_msg = "mover produced non-finite state at particle index " + std::to_string(i);
     return fail(B2M_NUMERICAL_FAULT, ctx->poison_msg);
   }
+  if (f.domain != ~0ull) {
+    const int s = static_cast<int>(f.domain >> 48);
+    const int64_t i = static_cast<int64_t>(f.domain & ((1ull << 48) - 1));
+    if (bad_species) *bad_species = s;
+    if (first_bad) *first_bad = i;
+    ctx->poisoned = true;
+    // grid.hpp:67 message text
+    ctx->poison_msg = "grid_cell_of: position outside domain (wrap first)";
+    return fail(B2M_DOMAIN_ERROR, ctx->poison_msg);
+  }
   if (f.cfl != ~0ull) {
     const int s = static_cast<int>(f.cfl >> 48);
     const int64_t i = static_cast<int64_t>(f.cfl & ((1ull << 48) - 1));
@@ -849,6 +863,88 @@ b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp, co
       else g_last_error = msg;
       if (first_bad) *first_bad = bad;
     }
+  }
+  const std::string msg = g_last_error;
+  b2m_ctx_destroy(ctx);
+  g_last_error = msg;
+  return st;
+}
+
+// ---- moments ------------------------------------------------------------------
+
+b2m_status b2m_moments_zero(b2m_ctx* ctx, int with_pressure) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  const int na = with_pressure ? 10 : 4;
+  const uint64_t nodes = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
+  if (ctx->mom_arrays < na) {
+    double* blk = nullptr;
+    if ((st = dalloc(ctx, &blk, na * nodes, "moment mesh")) != B2M_OK) return st;
+    for (int a = 0; a < 10; ++a) ctx->mom[a] = a < na ? blk + a * nodes : nullptr;
+    ctx->mom_arrays = na;
+  }
+  for (int a = 0; a < na; ++a)
+    B2M_CUDA(ctx, cudaMemsetAsync(ctx->mom[a], 0, nodes * sizeof(double), ctx->stream));
+  ctx->mom_pressure = with_pressure != 0;
+  return B2M_OK;
+}
+
+b2m_status b2m_deposit(b2m_ctx* ctx, int s, double q_per_particle) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if ((st = check_species(ctx, s)) != B2M_OK) return st;
+  if (!ctx->mom[0]) return fail(B2M_CONFIG_ERROR, "deposit: call b2m_moments_zero first");
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  SpeciesLaunch L{};
+  L.x = S.a[0]; L.y = S.a[1]; L.z = S.a[2];
+  L.u = S.a[3]; L.v = S.a[4]; L.w = S.a[5];
+  L.n = S.count;
+  L.species = s;
+  // kernels.cpp:148,162: qv = q_per_particle * (1 / cell_volume)
+  const double qv = q_per_particle * (1.0 / ((ctx->grid.dx * ctx->grid.dy) * ctx->grid.dz));
+  launch_deposit(to_dev(ctx->grid), L, qv, ctx->mom, ctx->mom_pressure, ctx->fault, ctx->stream);
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_moments_download(b2m_ctx* ctx, double* const* out, int n_arrays) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!out || n_arrays < 1 || n_arrays > (ctx->mom_pressure ? 10 : 4) || !ctx->mom[0])
+    return fail(B2M_INVALID_ARGUMENT, "moments_download: bad array count or no mesh");
+  const uint64_t nodes = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
+  for (int a = 0; a < n_arrays; ++a)
+    B2M_CUDA(ctx, cudaMemcpyAsync(out[a], ctx->mom[a], nodes * sizeof(double),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  return b2m_sync(ctx, nullptr, nullptr);
+}
+
+b2m_status b2m_deposit_moments_host(const b2m_grid* g, const double* x, const double* y,
+                                    const double* z, const double* u, const double* v,
+                                    const double* w, uint64_t n, double q_per_particle,
+                                    int with_pressure, double* const* out) {
+  if (!g || !out) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  if (n == 0) return B2M_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  b2m_ctx* ctx = nullptr;
+  const uint64_t cap = n;
+  b2m_status st = b2m_ctx_create(dev, g, 1, &cap, B2M_MODE_STRICT, &ctx);
+  if (st != B2M_OK) return st;
+  const double* src[6] = {x, y, z, u, v, w};
+  const int na = with_pressure ? 10 : 4;
+  const uint64_t nodes = static_cast<uint64_t>(g->nx) * g->ny * g->nz;
+  std::vector<double> host(static_cast<size_t>(na) * nodes);
+  std::vector<double*> dst(static_cast<size_t>(na));
+  for (int a = 0; a < na; ++a) dst[static_cast<size_t>(a)] = host.data() + a * nodes;
+  if ((st = b2m_species_upload(ctx, 0, src, n)) == B2M_OK &&
+      (st = b2m_moments_zero(ctx, with_pressure)) == B2M_OK &&
+      (st = b2m_deposit(ctx, 0, q_per_particle)) == B2M_OK &&
+      (st = b2m_moments_download(ctx, dst.data(), na)) == B2M_OK) {
+    // MomentMesh& out accumulates (kernels.cpp:169-180)
+    for (int a = 0; a < na; ++a)
+      for (uint64_t i = 0; i < nodes; ++i) out[a][i] += dst[static_cast<size_t>(a)][i];
   }
   const std::string msg = g_last_error;
   b2m_ctx_destroy(ctx);

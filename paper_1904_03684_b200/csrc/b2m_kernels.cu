@@ -234,6 +234,7 @@ __global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __re
 __global__ void fault_reset_kernel(FaultWord* f) {
   f->numerical = ~0ull;
   f->cfl = ~0ull;
+  f->domain = ~0ull;
 }
 
 __global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const double* __restrict__ x,

@@ -111,6 +111,18 @@ class DeviceStore:
             raise NumericalFault(_capi.last_error(), index=bi.value, species=bs.value)
         _capi.check(st)
 
+    # -- moments (deposit_moments, kernels.cpp:147-183) -----------------------
+    def moments_zero(self, with_pressure: bool = False):
+        _capi.check(_capi.lib().b2m_moments_zero(self.h, int(with_pressure)))
+
+    def deposit(self, s: int, q_per_particle: float):
+        _capi.check(_capi.lib().b2m_deposit(self.h, s, float(q_per_particle)))
+
+    def moments_download(self, mesh) -> None:
+        """Copy the device moment mesh into ``mesh`` (a MomentMesh) and sync."""
+        ptrs = (_capi._dp * len(mesh.arrays))(*[_capi.dptr(a) for a in mesh.arrays])
+        _capi.check(_capi.lib().b2m_moments_download(self.h, ptrs, len(mesh.arrays)))
+
     def record(self, slot: int):
         _capi.check(_capi.lib().b2m_event_record(self.h, slot))
 

@@ -234,3 +234,56 @@ def move_batch(p, field, grid: Grid, mp: MoverParams, mode="fast") -> None:
     if st == 4:
         raise NumericalFault(_capi.last_error(), index=bad.value)
     _capi.check(st)
+
+
+class MomentMesh:
+    """Charge, current and (optionally) pressure on the nx*ny*nz periodic
+    nodes (MomentMesh, kernels.hpp:54-69; index i + nx*(j + ny*k))."""
+
+    NAMES = ("rho", "jx", "jy", "jz", "pxx", "pxy", "pxz", "pyy", "pyz", "pzz")
+
+    def __init__(self, nx: int, ny: int, nz: int, with_pressure: bool = False):
+        self.nx, self.ny, self.nz = nx, ny, nz
+        self.with_pressure = bool(with_pressure)
+        n = nx * ny * nz
+        self.arrays = [np.zeros(n) for _ in range(10 if with_pressure else 4)]
+        for name, a in zip(self.NAMES, self.arrays):
+            setattr(self, name, a)
+
+    @staticmethod
+    def make(grid: Grid, with_pressure: bool = False) -> "MomentMesh":
+        return MomentMesh(grid.nx, grid.ny, grid.nz, with_pressure)
+
+    def index(self, i: int, j: int, k: int) -> int:
+        return i + self.nx * (j + self.ny * k)
+
+    def zero(self) -> None:
+        for a in self.arrays:
+            a[:] = 0.0
+
+    def add(self, other: "MomentMesh") -> None:
+        n = 10 if (self.with_pressure and other.with_pressure) else 4
+        for a, b in zip(self.arrays[:n], other.arrays[:n]):
+            a += b
+
+    def total_charge(self, grid: Grid) -> float:
+        # MomentMesh::total_charge (kernels.cpp:141-145): sequential sum * volume
+        return float(np.cumsum(self.rho)[-1]) * grid.cell_volume() if self.rho.size else 0.0
+
+
+def deposit_moments(b, grid: Grid, out: MomentMesh, q_per_particle: float | None = None) -> None:
+    """Scatter the particles' charge, current (and pressure) onto ``out`` on the
+    GPU (deposit_moments, kernels.cpp:147-183); ``out`` accumulates.  ``b`` is
+    a ParticleBatch (its q_per_particle) or six float64 arrays with
+    ``q_per_particle`` given.  Raises DomainError for a particle outside the
+    domain, like the reference's grid_cell_of."""
+    span = _as_span(b)
+    qp = b.q_per_particle if isinstance(b, ParticleBatch) else q_per_particle
+    if qp is None:
+        raise TypeError("q_per_particle required for raw arrays")
+    span = [np.ascontiguousarray(a, dtype=np.float64) for a in span]
+    g = grid.to_c()
+    ptrs = (_capi._dp * len(out.arrays))(*[_capi.dptr(a) for a in out.arrays])
+    _capi.check(_capi.lib().b2m_deposit_moments_host(C.byref(g), *[_capi.dptr(a) for a in span],
+                                                     len(span[0]), float(qp),
+                                                     int(out.with_pressure), ptrs))

@@ -71,6 +71,15 @@ def main():
     g["c1_move_gemfield_pc5"] = mover_case("c1b", c1, parts, E0, B0, 0.1, qoms, 5)
     g["c1_move_pc1"] = mover_case("c1c", c1, parts, E, B, 0.05, qoms, 1)
 
+    # deposit_moments (kernels.cpp:147-183) of the C1 GEM state, per species,
+    # with the pressure tensor: digests of the 10 moment arrays
+    _, qpp, _ = oracle.ref_gem_species(c1, 8)
+    g["c1_moments"] = {"qpp": hexs(qpp), "species": []}
+    for s, p in enumerate(parts):
+        m = oracle.ref_deposit_moments(p, c1, float(qpp[s]), True)
+        g["c1_moments"]["species"].append({"sha": [digest([a]) for a in m],
+                                           "rho_prefix": hexs(m[0][:8])})
+
     # desk preset (sim_config.hpp desk_benchmark_config): 32x32x16 at 64 ppc
     desk = (32, 32, 16, 25.6, 12.8, 6.4)
     parts, E0, B0 = oracle.ref_init_gem(desk, 64)

@@ -1,0 +1,141 @@
+"""GPU parity of moment deposition (deposit_moments, kernels.cpp:147-183)
+against the pinned C oracle.
+
+Per-particle terms are computed exactly as the reference (same divisions,
+same products), so single-particle meshes are bit-identical; sums over many
+particles are added in another order (per-lane cell runs + FP64 atomics), so
+they agree to rounding: |gpu - ref| <= 1e-12 * max|ref| per array (the
+reference's own tests use 1e-12 relative on totals, test_kernels.cpp:274).
+Mirrors test_kernels.cpp:232-295 and test_init.cpp:131-143.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1904_03684_b200 import DomainError, Grid, MomentMesh, ParticleBatch, deposit_moments
+from paper_1904_03684_b200 import gem
+from paper_1904_03684_b200.engine import DeviceStore
+from paper_1904_03684_b200.mover import MoverParams
+from tests._util import random_particles
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def assert_moments_close(got, want, tol=TOL, what=""):
+    assert len(got) == len(want)
+    for name, g, w in zip(MomentMesh.NAMES, got, want):
+        scale = float(np.max(np.abs(w))) if w.size else 0.0
+        err = float(np.max(np.abs(g - w))) if w.size else 0.0
+        if scale == 0.0:
+            assert err == 0.0, f"{what} {name}: expected zeros, max |got| {err}"
+        else:
+            assert err <= tol * scale, f"{what} {name}: max err {err:.3e} vs scale {scale:.3e}"
+
+
+def gpu_deposit(p6, grid, qp, pressure=False):
+    g = Grid.make(*grid)
+    m = MomentMesh.make(g, pressure)
+    deposit_moments([np.ascontiguousarray(a) for a in p6], g, m, q_per_particle=qp)
+    return m
+
+
+def test_single_particle_corners_and_seam_bitwise(gpu):
+    """test_kernels.cpp:232-256: one term per node -> bit-identical."""
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    for x, u in ((0.5, 2.0), (3.5, 0.0)):
+        p = [np.array([x]), np.array([x]), np.array([x]), np.array([u]), np.zeros(1),
+             np.zeros(1)]
+        m = gpu_deposit(p, grid, 0.75, pressure=True)
+        want = oracle.port_deposit_moments(p, grid, 0.75, True)
+        for a, b in zip(m.arrays, want):
+            np.testing.assert_array_equal(a, b)
+        assert m.total_charge(Grid.make(*grid)) == pytest.approx(0.75, rel=1e-15)
+
+
+def test_random_batch_conserves_charge_and_current(gpu):
+    """test_kernels.cpp:258-280: 5000 particles; total charge and current."""
+    grid = (6, 5, 7, 3.0, 2.5, 3.5)
+    p = random_particles(grid, 5000, 31, vscale=1.0)
+    q = -0.0125
+    m = gpu_deposit(p, grid, q, pressure=True)
+    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, q, True), what="random")
+    g = Grid.make(*grid)
+    assert abs(m.total_charge(g) - q * 5000) <= 1e-12 * abs(q * 5000)
+    assert float(np.sum(m.jx)) * g.cell_volume() == pytest.approx(q * float(np.sum(p[3])),
+                                                                    rel=1e-11)
+
+
+def test_gem_c1_all_species_with_pressure(gpu, golden):
+    """The reference C1 GEM state (oracle-pinned, golden.json c1_moments):
+    every species' moments incl. the pressure tensor."""
+    gd = golden["c1_init"]
+    grid = tuple(gd["grid"])
+    parts = oracle.port_gem_species(grid, gd["ppc"], gd["seed"])
+    qpp = [float.fromhex(h) for h in golden["c1_moments"]["qpp"]]
+    for s, p in enumerate(parts):
+        m = gpu_deposit(p, grid, qpp[s], pressure=True)
+        assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, qpp[s], True),
+                             what=f"species {s}")
+
+
+def test_quasi_neutral_gem_total_charge(gpu):
+    """test_init.cpp:131-143: the GEM state is neutral to 1e-12 of |q|."""
+    g = Grid.make(16, 16, 8, 12.8, 6.4, 3.2)
+    batches = gem.init_gem_species(g, 8)
+    m = MomentMesh.make(g)
+    abs_q = 0.0
+    for b in batches:
+        deposit_moments(b, g, m)
+        abs_q += abs(b.q_per_particle) * b.count()
+    assert abs(m.total_charge(g)) <= 1e-12 * abs_q
+
+
+def test_domain_error_names_reference_message(gpu):
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    p = [np.array([1.0, 4.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]), np.zeros(2),
+         np.zeros(2), np.zeros(2)]
+    with pytest.raises(DomainError, match="outside domain"):
+        gpu_deposit(p, grid, 1.0)
+
+
+def test_device_store_deposit_after_move_and_sort(gpu):
+    """Engine-level: resident particles are moved, cell-sorted, then
+    deposited on the device; equals the oracle deposit of the same particles
+    (cell order does not change the moments beyond rounding)."""
+    g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 8)
+    field = gem.gem_like_field(g)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    st = DeviceStore(g, [b.count() for b in batches], "fast")
+    st.upload_field(field)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    st.move_all(mps)
+    for s in range(len(batches)):
+        st.sort(s)
+    st.moments_zero(with_pressure=True)
+    for s, b in enumerate(batches):
+        st.deposit(s, b.q_per_particle)
+    mine = MomentMesh.make(g, True)
+    st.moments_download(mine)
+    want = [np.zeros(g.cells()) for _ in range(10)]
+    for s, b in enumerate(batches):
+        p = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, p)
+        st.sync()
+        for a, w in zip(oracle.port_deposit_moments(p, grid, b.q_per_particle, True), want):
+            w += a
+    assert_moments_close(mine.arrays, want, what="device store")
+
+
+def test_unsorted_large_batch(gpu):
+    """Random order (every particle its own cell run): the flush-per-particle
+    path, 200k particles."""
+    grid = (32, 16, 16, 12.8, 6.4, 6.4)
+    p = random_particles(grid, 200_000, 7)
+    m = gpu_deposit(p, grid, 0.01, pressure=False)
+    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.01, False),
+                         what="unsorted")

@@ -193,3 +193,58 @@ def test_port_vs_reference_grid_cell_of_known_answers(golden):
         ijk, f = oracle.ref_grid_cell_of(list(from_hex(c["pos"])), grid)
         assert list(ijk) == c["ijk"]
         np.testing.assert_array_equal(f, from_hex(c["f"]))
+
+
+# ---- deposit_moments (kernels.cpp:147-183) --------------------------------------
+
+def test_port_deposit_matches_reference_golden(golden):
+    """The C restatement of deposit_moments reproduces the reference's C1 GEM
+    moment meshes (rho, j, pressure) bit for bit."""
+    gd = golden["c1_moments"]
+    grid, parts = _port_gem(golden["c1_init"])
+    qpp = from_hex(gd["qpp"])
+    for s, sp in enumerate(gd["species"]):
+        m = oracle.port_deposit_moments(parts[s], grid, float(qpp[s]), True)
+        assert [digest([a]) for a in m] == sp["sha"], f"species {s}"
+        np.testing.assert_array_equal(m[0][:8], from_hex(sp["rho_prefix"]))
+
+
+def test_port_deposit_single_particle_and_seam():
+    """test_kernels.cpp:232-256: q/V/8 on each corner of cell (0,0,0); a
+    particle in the last cell folds its upper corners onto node 0."""
+    g = (4, 4, 4, 4.0, 4.0, 4.0)
+    q = 0.75
+    one = lambda x, u: [np.array([x]), np.array([x]), np.array([x]), np.array([u]),
+                        np.zeros(1), np.zeros(1)]
+    m = oracle.port_deposit_moments(one(0.5, 2.0), g, q)
+    expect = q / 1.0 / 8.0
+    for c in range(8):
+        idx = (c & 1) + 4 * (((c >> 1) & 1) + 4 * ((c >> 2) & 1))
+        assert m[0][idx] == expect and m[1][idx] == 2.0 * expect and m[2][idx] == 0.0
+    m2 = oracle.port_deposit_moments(one(3.5, 0.0), g, q)
+    for (i, j, k) in [(0, 0, 0), (3, 3, 3), (0, 3, 3)]:
+        assert m2[0][i + 4 * (j + 4 * k)] == expect
+    assert abs(np.cumsum(m2[0])[-1] - q) < 1e-15
+
+
+@needs_ref
+def test_port_deposit_bitwise_vs_reference_random():
+    """test_kernels.cpp:258-280 shape: 5000 particles, pressure on."""
+    g = (6, 5, 7, 3.0, 2.5, 3.5)
+    p = random_particles(g, 5000, 31, vscale=1.0)
+    a = oracle.port_deposit_moments(p, g, -0.0125, True)
+    b = oracle.ref_deposit_moments(p, g, -0.0125, True)
+    for x, y in zip(a, b):
+        assert_bitwise(x, y, "moments")
+
+
+@needs_ref
+def test_reference_deposit_domain_error():
+    g = (4, 4, 4, 4.0, 4.0, 4.0)
+    p = [np.array([1.0, 4.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]), np.zeros(2),
+         np.zeros(2), np.zeros(2)]
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.ref_deposit_moments(p, g, 1.0)
+    assert e.value.status == 2 and "outside domain" in e.value.msg
+    with pytest.raises(oracle.OracleError):
+        oracle.port_deposit_moments(p, g, 1.0)
