@@ -10,6 +10,8 @@
 //   cell_keys / gather6   the optional cell-sort pass (+ CUB radix sort)
 //   count_flags / scatter_out / fill_*   outbox compaction and hole filling
 //                         (merge_incoming, runtime.cpp:64-76)
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 #include <cudaTypedefs.h>
 
@@ -457,6 +459,11 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT>,
                                                   kWarpThreads, smem);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    // diagnostics: B2M_BLOCKS_PER_SM=k runs the persistent grid with k blocks per SM
+    if (const char* e = std::getenv("B2M_BLOCKS_PER_SM")) {
+      const int k = std::atoi(e);
+      if (k > 0 && k < per_sm) grid_cap = sms * k;
+    }
   }
   for (int base = 0; base < n_spans; base += kMaxTileSpans) {
     TensorSpans S{};
