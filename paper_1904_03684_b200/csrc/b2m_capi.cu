@@ -613,7 +613,7 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   ensure_tables(ctx, &s, mp, 1);
   const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
   if (ctx->mode == B2M_MODE_STRICT) {
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream)) {
@@ -646,7 +646,7 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
   for (int s = 0; s < ns; ++s)
     L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
   if (ctx->mode == B2M_MODE_STRICT) {
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault,
@@ -703,7 +703,7 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev[2 * c], 0));
       const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
       if (ctx->mode == B2M_MODE_STRICT) {
-        if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+        if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
                                       ctx->stream))
           return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream))
@@ -1029,7 +1029,7 @@ b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
   const int nb = flag_blocks(S.count);
   if (ctx->mode == B2M_MODE_STRICT) {
     uint8_t* fl[1] = {S.flags};
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
                                   ctx->stream, &ctx->sl, fl))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
     launch_count_flags(S.flags, S.count, S.blk, ctx->stream);

@@ -34,9 +34,9 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st,
                       const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
-bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B,
-                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                              cudaStream_t st, const SlabLaunch* sl = nullptr,
+bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
+                              const double* B, const SpeciesLaunch* sp, int n_spans,
+                              FaultWord* fault, cudaStream_t st, const SlabLaunch* sl = nullptr,
                               uint8_t* const* flags = nullptr);
 // Node AoS E/B -> per-cell polynomial coefficients of (scale[m]*E,
 // scale[m]*B) into tables[m] (48 doubles per cell), one field read per

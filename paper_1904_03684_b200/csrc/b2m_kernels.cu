@@ -114,7 +114,7 @@ __global__ void B2M_WARP_BOUNDS
 #pragma unroll 1
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        const unsigned bad = strict_tile_thread_p1<WT>(F.dg, F.E, F.B, sp, buf[st], p, cnt, cc);
+        const unsigned bad = strict_tile_thread_p1<WT>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           int flag = 0;
@@ -497,11 +497,13 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, F
   return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags);
 }
 
-bool launch_move_strict_tiles(const DevGrid& g, const double* E, const double* B,
-                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                              cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
+bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
+                              const double* B, const SpeciesLaunch* sp, int n_spans,
+                              FaultWord* fault, cudaStream_t st, const SlabLaunch* sl,
+                              uint8_t* const* flags) {
   TileField F{};
   F.dg = g;
+  F.fg = fg;  // wrap thresholds (WrapAxis)
   F.E = E;
   F.B = B;
   return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags);

@@ -470,17 +470,23 @@ __device__ __forceinline__ void strict_round(PState& P, const CellCache& cc, con
                              __dmul_rn(vdot, oz)), denom);
 }
 
-__device__ __forceinline__ void strict_predict(PState& P, const DevGrid& g, double dto2) {
-  P.tx = wrap_len_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dto2)), g.lx);
-  P.ty = wrap_len_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dto2)), g.ly);
-  P.tz = wrap_len_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dto2)), g.lz);
+// wrap_len (grid.hpp:45-50) bit for bit: the quotient's floor read off the
+// WrapAxis thresholds instead of an IEEE division (same result, see WrapAxis)
+__device__ __forceinline__ double wrap_strict(double v, const WrapAxis& a) {
+  return wrap_exact_bits(v, a, dbits(a.hi0), dbits(a.hi1), dbits(a.lom1) & kAbs);
 }
 
-__device__ __forceinline__ bool strict_finish(PState& P, const DevGrid& g, double dt, double* out) {
+__device__ __forceinline__ void strict_predict(PState& P, const FastGrid& w, double dto2) {
+  P.tx = wrap_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dto2)), w.ax);
+  P.ty = wrap_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dto2)), w.ay);
+  P.tz = wrap_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dto2)), w.az);
+}
+
+__device__ __forceinline__ bool strict_finish(PState& P, const FastGrid& w, double dt, double* out) {
   if (!P.ok) return false;
-  const double x1 = wrap_len_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dt)), g.lx);
-  const double y1 = wrap_len_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dt)), g.ly);
-  const double z1 = wrap_len_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dt)), g.lz);
+  const double x1 = wrap_strict(__dadd_rn(P.x0, __dmul_rn(P.bx, dt)), w.ax);
+  const double y1 = wrap_strict(__dadd_rn(P.y0, __dmul_rn(P.by, dt)), w.ay);
+  const double z1 = wrap_strict(__dadd_rn(P.z0, __dmul_rn(P.bz, dt)), w.az);
   const double u1 = __dsub_rn(__dmul_rn(2.0, P.bx), P.u0);
   const double v1 = __dsub_rn(__dmul_rn(2.0, P.by), P.v0);
   const double w1 = __dsub_rn(__dmul_rn(2.0, P.bz), P.w0);
@@ -503,7 +509,7 @@ __device__ __forceinline__ bool strict_finish(PState& P, const DevGrid& g, doubl
 // remain in the same cell: a bitwise-identical reuse of values the reference
 // would re-read.
 template <int TILE>
-__device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g,
+__device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, const FastGrid& wg,
                                                           const double* __restrict__ E,
                                                           const double* __restrict__ B,
                                                           const SpeciesLaunch& sp,
@@ -519,10 +525,10 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g,
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
     if (cell != cc.cell) cache_load_strict(cc, g, E, B, cell);
     strict_round(P, cc, wt, sp.beta);
-    if (r + 1 < sp.rounds) strict_predict(P, g, sp.dto2);
+    if (r + 1 < sp.rounds) strict_predict(P, wg, sp.dto2);
   }
   double out[6];
-  if (!strict_finish(P, g, sp.dt, out)) return 1u;
+  if (!strict_finish(P, wg, sp.dt, out)) return 1u;
 #pragma unroll
   for (int a = 0; a < 6; ++a) buf[a][p] = out[a];
   return 0u;
