@@ -145,12 +145,6 @@ class SlabWorld:
         self.total = int(t.item())
         return self.total
 
-    def _exchange(self, send_prev, send_next):
-        if self.stage_host:
-            a, b = self._exchange_on(send_prev.cpu(), send_next.cpu(), "cpu")
-            return a.to(self.device), b.to(self.device)
-        return self._exchange_on(send_prev, send_next, self.device)
-
     def _all_reduce(self, t, op=None):
         if self.stage_host:
             h = t.cpu()
@@ -159,60 +153,85 @@ class SlabWorld:
         else:
             self.dist.all_reduce(t) if op is None else self.dist.all_reduce(t, op=op)
 
-    def _exchange_on(self, send_prev, send_next, dev):
-        """Send (n,6) float64 tensors to prev/next, return what arrives from
-        prev and from next.  Counts first, then payloads, both as batched P2P
-        (grouped ncclSend/ncclRecv on NCCL).  With two ranks prev == next and
-        both directions travel in one message each way."""
+    def _exchange(self, outs):
+        """Migration of all species in one round trip: ``outs[s] = (to_prev,
+        to_next)`` (n, 6) float64 tensors; returns, per species, the (m, 6)
+        records that arrive from prev then next."""
+        if self.stage_host:
+            ins = self._exchange_on([(a.cpu(), b.cpu()) for a, b in outs], "cpu")
+            return [t.to(self.device) for t in ins]
+        return self._exchange_on(outs, self.device)
+
+    def _exchange_on(self, outs, dev):
+        """Counts first (one int64 row per direction and species), then one
+        payload per neighbour with every species concatenated: two grouped
+        ncclSend/ncclRecv rounds per cycle however many species.  With two
+        ranks prev == next and both directions travel in one message."""
         import torch
         dist = self.dist
+        ns = len(outs)
+        empty = torch.empty((0, 6), dtype=torch.float64, device=dev)
         if self.world == 1:
-            return send_next, send_prev   # periodic self-neighbour (never used: no leavers)
-        if self.world == 2:
-            other = self.prev
-            out = torch.cat([send_prev, send_next], dim=0) if send_next.shape[0] else send_prev
-            cnt_out = torch.tensor([out.shape[0]], dtype=torch.int64, device=dev)
-            cnt_in = torch.zeros(1, dtype=torch.int64, device=dev)
-            ops = [dist.P2POp(dist.isend, cnt_out, other), dist.P2POp(dist.irecv, cnt_in, other)]
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-            n_in = int(cnt_in.item())
-            buf = torch.empty((n_in, 6), dtype=torch.float64, device=dev)
-            ops = []
-            if out.shape[0]:
-                ops.append(dist.P2POp(dist.isend, out.contiguous(), other))
-            if n_in:
-                ops.append(dist.P2POp(dist.irecv, buf, other))
+            return [empty for _ in range(ns)]  # periodic self-neighbour: no leavers
+        cnt_out = torch.tensor([[int(a.shape[0]) for a, _ in outs],
+                                [int(b.shape[0]) for _, b in outs]], dtype=torch.int64, device=dev)
+        pay_prev = [a for a, _ in outs if a.shape[0]]
+        pay_next = [b for _, b in outs if b.shape[0]]
+        pay_prev = torch.cat(pay_prev, dim=0) if pay_prev else empty
+        pay_next = torch.cat(pay_next, dim=0) if pay_next else empty
+
+        def wait_all(ops):
             if ops:
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
-            return buf, torch.empty((0, 6), dtype=torch.float64, device=dev)
-        cnt_out = torch.tensor([send_prev.shape[0], send_next.shape[0]], dtype=torch.int64,
-                               device=dev)
-        c_from_prev = torch.zeros(1, dtype=torch.int64, device=dev)
-        c_from_next = torch.zeros(1, dtype=torch.int64, device=dev)
-        ops = [dist.P2POp(dist.isend, cnt_out[0:1].clone(), self.prev),
-               dist.P2POp(dist.isend, cnt_out[1:2].clone(), self.next),
-               dist.P2POp(dist.irecv, c_from_prev, self.prev),
-               dist.P2POp(dist.irecv, c_from_next, self.next)]
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-        n_prev, n_next = int(c_from_prev.item()), int(c_from_next.item())
-        from_prev = torch.empty((n_prev, 6), dtype=torch.float64, device=dev)
-        from_next = torch.empty((n_next, 6), dtype=torch.float64, device=dev)
+
+        def split(buf, counts):
+            parts, o = [], 0
+            for c in counts:
+                parts.append(buf[o:o + c])
+                o += c
+            return parts
+
+        if self.world == 2:
+            other = self.prev
+            cnt_in = torch.zeros((2, ns), dtype=torch.int64, device=dev)
+            wait_all([dist.P2POp(dist.isend, cnt_out, other),
+                      dist.P2POp(dist.irecv, cnt_in, other)])
+            c_in = cnt_in.cpu().tolist()       # [the other's to-prev, to-next] = both to me
+            out = torch.cat([pay_prev, pay_next], dim=0).contiguous()
+            n_in = sum(c_in[0]) + sum(c_in[1])
+            buf = torch.empty((n_in, 6), dtype=torch.float64, device=dev)
+            ops = []
+            if out.shape[0]:
+                ops.append(dist.P2POp(dist.isend, out, other))
+            if n_in:
+                ops.append(dist.P2POp(dist.irecv, buf, other))
+            wait_all(ops)
+            a = split(buf[:sum(c_in[0])], c_in[0])
+            b = split(buf[sum(c_in[0]):], c_in[1])
+            return [torch.cat([x, y], dim=0) if y.shape[0] else x for x, y in zip(a, b)]
+
+        c_from_prev = torch.zeros(ns, dtype=torch.int64, device=dev)
+        c_from_next = torch.zeros(ns, dtype=torch.int64, device=dev)
+        wait_all([dist.P2POp(dist.isend, cnt_out[0].clone(), self.prev),
+                  dist.P2POp(dist.isend, cnt_out[1].clone(), self.next),
+                  dist.P2POp(dist.irecv, c_from_prev, self.prev),
+                  dist.P2POp(dist.irecv, c_from_next, self.next)])
+        cp, cn = c_from_prev.cpu().tolist(), c_from_next.cpu().tolist()
+        from_prev = torch.empty((sum(cp), 6), dtype=torch.float64, device=dev)
+        from_next = torch.empty((sum(cn), 6), dtype=torch.float64, device=dev)
         ops = []
-        if send_prev.shape[0]:
-            ops.append(dist.P2POp(dist.isend, send_prev.contiguous(), self.prev))
-        if send_next.shape[0]:
-            ops.append(dist.P2POp(dist.isend, send_next.contiguous(), self.next))
-        if n_prev:
+        if pay_prev.shape[0]:
+            ops.append(dist.P2POp(dist.isend, pay_prev.contiguous(), self.prev))
+        if pay_next.shape[0]:
+            ops.append(dist.P2POp(dist.isend, pay_next.contiguous(), self.next))
+        if from_prev.shape[0]:
             ops.append(dist.P2POp(dist.irecv, from_prev, self.prev))
-        if n_next:
+        if from_next.shape[0]:
             ops.append(dist.P2POp(dist.irecv, from_next, self.next))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-        return from_prev, from_next
+        wait_all(ops)
+        a, b = split(from_prev, cp), split(from_next, cn)
+        return [torch.cat([x, y], dim=0) if y.shape[0] else x for x, y in zip(a, b)]
 
     def step(self, mps, check_counts: bool = True):
         """One mover cycle over all species with migration
@@ -234,23 +253,26 @@ class SlabWorld:
         except Exception as e:  # noqa: BLE001 - re-raised after the collective below
             err = e
         empty = torch.empty((0, 6), dtype=torch.float64, device=self.device)
-        moved = 0
+        outs = []
         for s in range(self.ns):
             if err is None:
                 try:
-                    send_prev, send_next = st.outbox(s, 0), st.outbox(s, 1)
-                except Exception as e:  # noqa: BLE001
-                    err, send_prev, send_next = e, empty, empty
-            else:
-                send_prev, send_next = empty, empty
-            from_prev, from_next = self._exchange(send_prev, send_next)
-            inbox = torch.cat([from_prev, from_next], dim=0) if from_next.shape[0] else from_prev
-            if err is None:
-                try:
-                    st.inbox_append(s, inbox.contiguous())
+                    outs.append((st.outbox(s, 0), st.outbox(s, 1)))
+                    continue
                 except Exception as e:  # noqa: BLE001
                     err = e
-            moved += int(send_prev.shape[0] + send_next.shape[0])
+            outs.append((empty, empty))
+        if err is not None:   # a faulted rank still takes part, with empty outboxes
+            outs = [(empty, empty)] * self.ns
+        ins = self._exchange(outs)
+        moved = sum(int(a.shape[0] + b.shape[0]) for a, b in outs)
+        if err is None:
+            for s in range(self.ns):
+                try:
+                    st.inbox_append(s, ins[s].contiguous())
+                except Exception as e:  # noqa: BLE001
+                    err = e
+                    break
         self.last_exchange = {"sent": moved}
         t = torch.tensor([self._count_all() if err is None else 0, 1 if err is not None else 0],
                          dtype=torch.int64, device=self.device)
