@@ -902,7 +902,8 @@ b2m_status b2m_deposit(b2m_ctx* ctx, int s, double q_per_particle) {
   L.species = s;
   // kernels.cpp:148,162: qv = q_per_particle * (1 / cell_volume)
   const double qv = q_per_particle * (1.0 / ((ctx->grid.dx * ctx->grid.dy) * ctx->grid.dz));
-  launch_deposit(to_dev(ctx->grid), L, qv, ctx->mom, ctx->mom_pressure, ctx->fault, ctx->stream);
+  launch_deposit(to_dev(ctx->grid), L, qv, ctx->mom, ctx->mom_pressure,
+                 ctx->mode == B2M_MODE_STRICT, ctx->fault, ctx->stream);
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }

@@ -48,8 +48,9 @@ void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double
 // Moment deposition (b2m_moments.cu, deposit_moments kernels.cpp:147-183) of
 // one species span, qv = q_per_particle / cell volume, accumulated into
 // mesh[0..3] = rho, jx, jy, jz (+ mesh[4..9] = pxx..pzz with pressure).
+// exact: bit-identical per-particle terms (STRICT); else FAST arithmetic.
 void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double* const* mesh,
-                    bool pressure, FaultWord* fault, cudaStream_t st);
+                    bool pressure, bool exact, FaultWord* fault, cudaStream_t st);
 // Reset the fault words to "clean".
 void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 

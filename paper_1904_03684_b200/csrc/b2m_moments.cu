@@ -42,12 +42,19 @@ __device__ __forceinline__ void load4(const double* p, double (&v)[4]) {
 }
 
 // SET 0: rho, jx, jy, jz.  SET 1: the six pressure components.
-template <int SET>
+// EXACT (STRICT contexts): the cell and weights with the reference's IEEE
+// divisions, every per-particle term bit-identical.  Otherwise (FAST) the
+// position is scaled by 1/d and the products may contract into FMAs: the
+// terms change by an ulp and a particle exactly on a cell face may pick the
+// neighbouring cell -- the deposit is continuous across faces, so the mesh
+// still agrees to rounding.
+template <int SET, bool EXACT>
 __global__ void __launch_bounds__(kDepositThreads, 2)
     deposit_kernel(const __grid_constant__ DevGrid g, const __grid_constant__ SpeciesLaunch sp,
                    double qv, const __grid_constant__ MomentPtrs M, unsigned long long span,
                    FaultWord* fault) {
   constexpr int NM = SET == 0 ? 4 : 6;
+  const double rdx = 1.0 / g.dx, rdy = 1.0 / g.dy, rdz = 1.0 / g.dz;
   const unsigned long long t =
       static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const unsigned long long lb = t * span;  // this lane's range [lb, le)
@@ -70,6 +77,10 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
     }
   };
 
+  // EXACT: every product/sum rounded on its own, as the reference (no FMA)
+  auto mul_ = [](double a, double b) { return EXACT ? __dmul_rn(a, b) : a * b; };
+  auto add_ = [](double a, double b) { return EXACT ? __dadd_rn(a, b) : a + b; };
+  auto sub_ = [](double a, double b) { return EXACT ? __dsub_rn(a, b) : a - b; };
   auto particle = [&](double px, double py, double pz, double ux, double uy, double uz,
                       unsigned long long p) {
     // grid.hpp:65-67: the reference throws DomainError
@@ -78,14 +89,16 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
       return;
     }
     // grid.hpp:69-80, bit for bit
-    const double sx = __ddiv_rn(px, g.dx), sy = __ddiv_rn(py, g.dy), sz = __ddiv_rn(pz, g.dz);
+    const double sx = EXACT ? __ddiv_rn(px, g.dx) : px * rdx;
+    const double sy = EXACT ? __ddiv_rn(py, g.dy) : py * rdy;
+    const double sz = EXACT ? __ddiv_rn(pz, g.dz) : pz * rdz;
     int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
     if (i >= g.nx) i = g.nx - 1;
     if (j >= g.ny) j = g.ny - 1;
     if (k >= g.nz) k = g.nz - 1;
-    const double fx = fmin(__dsub_rn(sx, static_cast<double>(i)), 1.0);
-    const double fy = fmin(__dsub_rn(sy, static_cast<double>(j)), 1.0);
-    const double fz = fmin(__dsub_rn(sz, static_cast<double>(k)), 1.0);
+    const double fx = fmin(sub_(sx, static_cast<double>(i)), 1.0);
+    const double fy = fmin(sub_(sy, static_cast<double>(j)), 1.0);
+    const double fz = fmin(sub_(sz, static_cast<double>(k)), 1.0);
     if (i != ai || j != aj || k != ak) {
       if (ai >= 0) flush();
       ai = i; aj = j; ak = k;
@@ -94,27 +107,27 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[m][c] = 0.0;
     }
-    const double wx[2] = {__dsub_rn(1.0, fx), fx};
-    const double wy[2] = {__dsub_rn(1.0, fy), fy};
-    const double wz[2] = {__dsub_rn(1.0, fz), fz};
+    const double wx[2] = {sub_(1.0, fx), fx};
+    const double wy[2] = {sub_(1.0, fy), fy};
+    const double wz[2] = {sub_(1.0, fz), fz};
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       // kernels.cpp:168: qv * wx * wy * wz, left to right
-      const double wq = __dmul_rn(__dmul_rn(__dmul_rn(qv, wx[c & 1]), wy[(c >> 1) & 1]),
+      const double wq = mul_(mul_(mul_(qv, wx[c & 1]), wy[(c >> 1) & 1]),
                                   wz[(c >> 2) & 1]);
       if (SET == 0) {
-        acc[0][c] = __dadd_rn(acc[0][c], wq);
-        acc[1][c] = __dadd_rn(acc[1][c], __dmul_rn(wq, ux));
-        acc[2][c] = __dadd_rn(acc[2][c], __dmul_rn(wq, uy));
-        acc[3][c] = __dadd_rn(acc[3][c], __dmul_rn(wq, uz));
+        acc[0][c] = add_(acc[0][c], wq);
+        acc[1][c] = add_(acc[1][c], mul_(wq, ux));
+        acc[2][c] = add_(acc[2][c], mul_(wq, uy));
+        acc[3][c] = add_(acc[3][c], mul_(wq, uz));
       } else {
-        const double wu = __dmul_rn(wq, ux), wv = __dmul_rn(wq, uy), ww = __dmul_rn(wq, uz);
-        acc[0][c] = __dadd_rn(acc[0][c], __dmul_rn(wu, ux));
-        acc[1][c] = __dadd_rn(acc[1][c], __dmul_rn(wu, uy));
-        acc[2][c] = __dadd_rn(acc[2][c], __dmul_rn(wu, uz));
-        acc[3][c] = __dadd_rn(acc[3][c], __dmul_rn(wv, uy));
-        acc[4][c] = __dadd_rn(acc[4][c], __dmul_rn(wv, uz));
-        acc[5][c] = __dadd_rn(acc[5][c], __dmul_rn(ww, uz));
+        const double wu = mul_(wq, ux), wv = mul_(wq, uy), ww = mul_(wq, uz);
+        acc[0][c] = add_(acc[0][c], mul_(wu, ux));
+        acc[1][c] = add_(acc[1][c], mul_(wu, uy));
+        acc[2][c] = add_(acc[2][c], mul_(wu, uz));
+        acc[3][c] = add_(acc[3][c], mul_(wv, uy));
+        acc[4][c] = add_(acc[4][c], mul_(wv, uz));
+        acc[5][c] = add_(acc[5][c], mul_(ww, uz));
       }
     }
   };
@@ -136,7 +149,7 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
 }  // namespace
 
 void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double* const* mesh,
-                    bool pressure, FaultWord* fault, cudaStream_t st) {
+                    bool pressure, bool exact, FaultWord* fault, cudaStream_t st) {
   if (sp.n == 0) return;
   static int sms = 0;
   if (sms == 0) {
@@ -153,10 +166,16 @@ void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double
   const int blocks = static_cast<int>((used + kDepositThreads - 1) / kDepositThreads);
   MomentPtrs M{};
   for (int m = 0; m < (pressure ? 10 : 4); ++m) M.m[m] = mesh[m];
-  deposit_kernel<0><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
+  if (exact)
+    deposit_kernel<0, true><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
+  else
+    deposit_kernel<0, false><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
   note_launch();
   if (pressure) {
-    deposit_kernel<1><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
+    if (exact)
+      deposit_kernel<1, true><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
+    else
+      deposit_kernel<1, false><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
     note_launch();
   }
 }
