@@ -184,6 +184,17 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
  * runtime.cpp:64-76). */
 b2m_status b2m_sort_species(b2m_ctx* ctx, int s);
 
+/* ---- field phase stand-in (field_phase_stub, kernels.cpp:185-215) ---------
+ * `passes` rounds of 7-point averaging of E on the context's device field
+ * (B untouched), then the seam mirror of E and B -- bit-identical to the
+ * reference.  The result becomes the context's field (the FAST tables are
+ * rebuilt on the next move), like Simulation's f_next (runtime.cpp:222).
+ * b2m_field_download copies the device field to host (FieldView layout).
+ * The _host form runs in place on host arrays (one-shot). */
+b2m_status b2m_field_phase_stub(b2m_ctx* ctx, int passes);
+b2m_status b2m_field_download(b2m_ctx* ctx, double* E, double* B);
+b2m_status b2m_field_phase_stub_host(const b2m_grid* g, double* E, double* B, int passes);
+
 /* ---- moments (deposit_moments, kernels.cpp:147-183; MomentMesh
  * kernels.hpp:54-69) -------------------------------------------------------
  * The context owns one device moment mesh of nx*ny*nz periodic nodes (index

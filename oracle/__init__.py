@@ -87,6 +87,8 @@ def port() -> C.CDLL:
         lib.or_fill_species_g.restype = None
         lib.or_fill_species_g.argtypes = [C.c_int] * 3 + [C.c_double] * 3 + \
             [C.c_int, C.c_int, _u64, C.c_double, _dp, _dp, _u64, _u64] + [_dp] * 6
+        lib.or_field_phase_stub_g.restype = None
+        lib.or_field_phase_stub_g.argtypes = [C.c_int] * 3 + [_dp, _dp, C.c_int, _dp]
         lib.or_deposit_moments_g.restype = C.c_int64
         lib.or_deposit_moments_g.argtypes = [_dp] * 6 + [_u64] + [C.c_int] * 3 + \
             [C.c_double] * 3 + [C.c_double, C.c_int, C.POINTER(_dp)]
@@ -115,6 +117,15 @@ def port_deposit_moments(p6, grid, qp: float, with_pressure: bool = False):
     if bad >= 0:
         raise OracleError(2, f"particle {bad} outside the domain")
     return out
+
+
+def port_field_phase_stub(E, B, grid, passes: int):
+    """The C restatement of field_phase_stub; returns new (E, B)."""
+    E, B = np.array(E, dtype=np.float64), np.array(B, dtype=np.float64)
+    scratch = np.empty_like(E)
+    port().or_field_phase_stub_g(grid[0], grid[1], grid[2], _ptr(E), _ptr(B), passes,
+                                 _ptr(scratch))
+    return E, B
 
 
 def port_wrap_len(v: float, l: float) -> float:
@@ -230,6 +241,7 @@ def _bind_ref(lib: C.CDLL) -> C.CDLL:
     lib.ref_aggregate_runs.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp] + eb
     lib.ref_decompose.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] + eb
     lib.ref_owner_of.argtypes = [C.c_double] + g6 + [C.c_int]
+    lib.ref_field_phase_stub.argtypes = g6 + [_dp, _dp, C.c_int] + eb
     lib.ref_deposit_moments.argtypes = [_dp] * 6 + [_u64] + g6 + [C.c_double, C.c_int,
                                                                    C.POINTER(_dp)] + eb
     return lib
@@ -276,6 +288,14 @@ def ref_deposit_moments(p6, grid, qp: float, with_pressure: bool = False):
                                    *grid, qp, int(with_pressure), ptrs, buf, 512)
     _check(st, buf)
     return out
+
+
+def ref_field_phase_stub(E, B, grid, passes: int):
+    """pic::field_phase_stub; returns new (E, B) node AoS arrays."""
+    E, B = np.array(E, dtype=np.float64), np.array(B, dtype=np.float64)
+    buf = _errbuf()
+    _check(ref().ref_field_phase_stub(*grid, _ptr(E), _ptr(B), passes, buf, 512), buf)
+    return E, B
 
 
 def ref_wrap_len(v: float, l: float) -> float:

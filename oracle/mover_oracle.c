@@ -162,6 +162,60 @@ int64_t or_move_batch_g(double* x, double* y, double* z, double* u, double* v, d
 
 /* ---- GEM input generation (init.cpp, rng.hpp) ---------------------------- */
 
+/* kernels.cpp:185-215 field_phase_stub: `passes` rounds of
+ * e + (1/12) * sum_nb (E_nb - e) over the 6 periodic face neighbours of
+ * every unique node (the six differences added left to right), ping-ponging
+ * between two meshes; then mirror_seams (field_mesh.hpp:46-59) copies the
+ * 0-planes of E and B onto the n-planes.  passes <= 0 returns the input
+ * unchanged (no mirroring).  E, B: node AoS with seams, updated in place. */
+void or_field_phase_stub_g(int nx, int ny, int nz, double* E, double* B, int passes,
+                           double* scratch) {
+  if (passes <= 0) return;
+  const int64_t sx = nx + 1, sy = ny + 1;
+  const int64_t nodes = sx * sy * (int64_t)(nz + 1);
+  double* cur = E;
+  double* nxt = scratch;
+  for (int64_t q = 0; q < 3 * nodes; ++q) nxt[q] = E[q];
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int k = 0; k < nz; ++k) {
+      const int km = (k + nz - 1) % nz, kp = (k + 1) % nz;
+      for (int j = 0; j < ny; ++j) {
+        const int jm = (j + ny - 1) % ny, jp = (j + 1) % ny;
+        for (int i = 0; i < nx; ++i) {
+          const int im = (i + nx - 1) % nx, ip = (i + 1) % nx;
+          const int64_t c = i + sx * (j + sy * k);
+          const int64_t nb[6] = {im + sx * (j + sy * k), ip + sx * (j + sy * k),
+                                 i + sx * (jm + sy * k), i + sx * (jp + sy * k),
+                                 i + sx * (j + sy * km), i + sx * (j + sy * kp)};
+          for (int a = 0; a < 3; ++a) {
+            const double e = cur[3 * c + a];
+            double sum = cur[3 * nb[0] + a] - e;
+            for (int m = 1; m < 6; ++m) sum = sum + (cur[3 * nb[m] + a] - e);
+            nxt[3 * c + a] = e + (1.0 / 12.0) * sum;
+          }
+        }
+      }
+    }
+    double* t = cur; cur = nxt; nxt = t;
+  }
+  if (cur != E)
+    for (int64_t q = 0; q < 3 * nodes; ++q) E[q] = cur[q];
+  /* mirror_seams */
+  for (int k = 0; k <= nz; ++k)
+    for (int j = 0; j <= ny; ++j) {
+      const int ks = k == nz ? 0 : k, js = j == ny ? 0 : j;
+      for (int i = 0; i <= nx; ++i) {
+        const int is = i == nx ? 0 : i;
+        if (is == i && js == j && ks == k) continue;
+        const int64_t d = i + sx * (j + sy * k), src = is + sx * (js + sy * ks);
+        for (int a = 0; a < 3; ++a) {
+          E[3 * d + a] = E[3 * src + a];
+          B[3 * d + a] = B[3 * src + a];
+        }
+      }
+    }
+}
+
 /* kernels.cpp:147-183 deposit_moments: every particle scatters
  * wq = ((q/V * wx) * wy) * wz onto the 8 corners of its cell, corner order
  * c = di + 2dj + 4dk, the upper corners wrapping onto node 0 (periodic, nodes

@@ -166,6 +166,22 @@ int ref_deposit_moments(const double* x, const double* y, const double* z, const
   SHIM_CATCH
 }
 
+// pic::field_phase_stub (kernels.cpp:185-215) on a FieldMesh built from node
+// AoS E/B (in place).
+int ref_field_phase_stub(int nx, int ny, int nz, double lx, double ly, double lz, double* E,
+                         double* B, int passes, char* err, int errlen) {
+  SHIM_TRY
+  const Grid g = Grid::make(nx, ny, nz, lx, ly, lz);
+  FieldMesh m = FieldMesh::make(g);
+  const std::size_t nodes = m.E.size();
+  std::memcpy(m.E.data(), E, nodes * sizeof(Vec3));
+  std::memcpy(m.B.data(), B, nodes * sizeof(Vec3));
+  const FieldMesh out = field_phase_stub(m, g, passes);
+  std::memcpy(E, out.E.data(), nodes * sizeof(Vec3));
+  std::memcpy(B, out.B.data(), nodes * sizeof(Vec3));
+  SHIM_CATCH
+}
+
 int ref_wrap_len(double v, double l, double* out) {
   *out = wrap_len(v, l);
   return kOk;

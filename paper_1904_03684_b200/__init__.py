@@ -8,8 +8,8 @@ include/b2m.h).
 from .errors import (AllocError, CflViolation, ConfigError, DomainError, EngineFault,
                      MetricError, MinipicError, NumericalFault)
 from .mover import (FieldMesh, Grid, MomentMesh, MoverParams, ParticleBatch, deposit_moments,
-                    move_batch)
+                    field_phase_stub, move_batch)
 
 __all__ = ["AllocError", "CflViolation", "ConfigError", "DomainError", "EngineFault",
            "MetricError", "MinipicError", "NumericalFault", "FieldMesh", "Grid", "MomentMesh",
-           "MoverParams", "ParticleBatch", "deposit_moments", "move_batch"]
+           "MoverParams", "ParticleBatch", "deposit_moments", "field_phase_stub", "move_batch"]

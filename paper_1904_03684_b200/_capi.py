@@ -81,6 +81,9 @@ SIGNATURES = {
                                  C.POINTER(b2m_mover_params), _u64]),
     "b2m_sort_species": (_st, [C.c_void_p, C.c_int]),
     "b2m_sync": (_st, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(_i64)]),
+    "b2m_field_phase_stub": (_st, [C.c_void_p, C.c_int]),
+    "b2m_field_download": (_st, [C.c_void_p, _dp, _dp]),
+    "b2m_field_phase_stub_host": (_st, [C.POINTER(b2m_grid), _dp, _dp, C.c_int]),
     "b2m_moments_zero": (_st, [C.c_void_p, C.c_int]),
     "b2m_deposit": (_st, [C.c_void_p, C.c_int, C.c_double]),
     "b2m_moments_download": (_st, [C.c_void_p, C.POINTER(_dp), C.c_int]),

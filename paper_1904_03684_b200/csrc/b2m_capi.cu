@@ -133,6 +133,7 @@ struct b2m_ctx {
   std::vector<Species> sp;
   uint64_t n_nodes = 0;
   double* dE = nullptr;
+  double* dE_alt = nullptr;  // field-stub ping-pong (allocated on first use)
   double* dB = nullptr;
   bool field_ready = false;
   uint64_t field_gen = 0;  // bumped by every field upload
@@ -513,6 +514,49 @@ b2m_status b2m_field_upload_device(b2m_ctx* ctx, const double* dE, const double*
   if (dB != ctx->dB)
     B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dB, dB, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   return relayout(ctx);
+}
+
+b2m_status b2m_field_download(b2m_ctx* ctx, double* E, double* B) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!E || !B) return fail(B2M_INVALID_ARGUMENT, "null field pointer");
+  const size_t bytes = 3 * ctx->n_nodes * sizeof(double);
+  B2M_CUDA(ctx, cudaMemcpyAsync(E, ctx->dE, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  B2M_CUDA(ctx, cudaMemcpyAsync(B, ctx->dB, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return b2m_sync(ctx, nullptr, nullptr);
+}
+
+b2m_status b2m_field_phase_stub(b2m_ctx* ctx, int passes) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "field stub: no field uploaded");
+  if (passes <= 0) return B2M_OK;
+  if (!ctx->dE_alt && (st = dalloc(ctx, &ctx->dE_alt, 3 * ctx->n_nodes, "field stub")) != B2M_OK)
+    return st;
+  double* out = launch_field_stub(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
+                                  ctx->dE_alt, passes, ctx->stream);
+  if (out != ctx->dE) std::swap(ctx->dE, ctx->dE_alt);
+  B2M_CUDA(ctx, cudaGetLastError());
+  return relayout(ctx);  // a new field: FAST tables rebuild on the next move
+}
+
+b2m_status b2m_field_phase_stub_host(const b2m_grid* g, double* E, double* B, int passes) {
+  if (!g || !E || !B) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  if (passes <= 0) return B2M_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  b2m_ctx* ctx = nullptr;
+  b2m_status st = b2m_ctx_create(dev, g, 0, nullptr, B2M_MODE_STRICT, &ctx);
+  if (st != B2M_OK) return st;
+  const uint64_t nodes = static_cast<uint64_t>(g->nx + 1) * (g->ny + 1) * (g->nz + 1);
+  if ((st = b2m_field_upload(ctx, E, B, nodes)) == B2M_OK &&
+      (st = b2m_field_phase_stub(ctx, passes)) == B2M_OK)
+    st = b2m_field_download(ctx, E, B);
+  const std::string msg = g_last_error;
+  b2m_ctx_destroy(ctx);
+  g_last_error = msg;
+  return st;
 }
 
 b2m_status b2m_species_upload_range(b2m_ctx* ctx, int s, const double* const* host6,

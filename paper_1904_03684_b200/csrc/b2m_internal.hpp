@@ -51,6 +51,11 @@ void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double
 // exact: bit-identical per-particle terms (STRICT); else FAST arithmetic.
 void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double* const* mesh,
                     bool pressure, bool exact, FaultWord* fault, cudaStream_t st);
+// field_phase_stub (b2m_field.cu, kernels.cpp:185-215) on the node AoS E/B:
+// `passes` stencil rounds ping-ponging between E and scratch, then the seam
+// mirror of E and B.  Returns the buffer that holds the result (E or scratch).
+double* launch_field_stub(int nx, int ny, int nz, double* E, double* B, double* scratch,
+                          int passes, cudaStream_t st);
 // Reset the fault words to "clean".
 void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 

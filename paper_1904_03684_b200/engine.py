@@ -56,6 +56,14 @@ class DeviceStore:
         _capi.check(_capi.lib().b2m_field_upload(self.h, _capi.dptr(field.E), _capi.dptr(field.B),
                                                  field.node_count()))
 
+    def field_stub(self, passes: int):
+        """field_phase_stub on the device field (kernels.cpp:185-215)."""
+        _capi.check(_capi.lib().b2m_field_phase_stub(self.h, int(passes)))
+
+    def download_field(self, field: FieldMesh):
+        _capi.check(_capi.lib().b2m_field_download(self.h, _capi.dptr(field.E),
+                                                   _capi.dptr(field.B)))
+
     def upload_field_device(self, dE: int, dB: int):
         _capi.check(_capi.lib().b2m_field_upload_device(self.h, C.c_void_p(dE), C.c_void_p(dB),
                                                         self.grid.nodes()))

@@ -120,6 +120,18 @@ class FieldMesh:
             G[nz, :, :] = G[0, :, :]
 
 
+def field_phase_stub(mesh: FieldMesh, grid: Grid, passes: int) -> FieldMesh:
+    """The field-phase stand-in on the GPU (kernels.cpp:185-215): a new mesh
+    with ``passes`` rounds of 7-point averaging of E (B unchanged, seams
+    mirrored), bit-identical to the reference."""
+    out = FieldMesh(grid, mesh.E.copy(), mesh.B.copy())
+    if passes > 0:
+        g = grid.to_c()
+        _capi.check(_capi.lib().b2m_field_phase_stub_host(C.byref(g), _capi.dptr(out.E),
+                                                          _capi.dptr(out.B), int(passes)))
+    return out
+
+
 class ParticleBatch:
     """SoA store of one species with fixed capacity (particle_batch.hpp:29-85).
 

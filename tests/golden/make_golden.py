@@ -80,6 +80,10 @@ def main():
         g["c1_moments"]["species"].append({"sha": [digest([a]) for a in m],
                                            "rho_prefix": hexs(m[0][:8])})
 
+    # field_phase_stub (kernels.cpp:185-215) of the C1 gem_like field, 3 passes
+    Es, Bs = oracle.ref_field_phase_stub(E, B, c1, 3)
+    g["c1_field_stub3"] = {"sha": digest([Es, Bs]), "E_prefix": hexs(Es[:12])}
+
     # desk preset (sim_config.hpp desk_benchmark_config): 32x32x16 at 64 ppc
     desk = (32, 32, 16, 25.6, 12.8, 6.4)
     parts, E0, B0 = oracle.ref_init_gem(desk, 64)

@@ -248,3 +248,24 @@ def test_reference_deposit_domain_error():
     assert e.value.status == 2 and "outside domain" in e.value.msg
     with pytest.raises(oracle.OracleError):
         oracle.port_deposit_moments(p, g, 1.0)
+
+
+# ---- field_phase_stub (kernels.cpp:185-215) ---------------------------------------
+
+def test_port_field_stub_matches_reference_golden(golden):
+    grid = tuple(golden["c1_init"]["grid"])
+    E, B = oracle.port_gem_like_field(grid)
+    Es, Bs = oracle.port_field_phase_stub(E, B, grid, 3)
+    assert digest([Es, Bs]) == golden["c1_field_stub3"]["sha"]
+    np.testing.assert_array_equal(Es[:12], from_hex(golden["c1_field_stub3"]["E_prefix"]))
+
+
+@needs_ref
+@pytest.mark.parametrize("passes", [0, 1, 4])
+def test_port_field_stub_bitwise_vs_reference(passes):
+    g = (7, 5, 6, 1.0, 2.0, 3.0)
+    E, B = random_field(g, 9)
+    a = oracle.port_field_phase_stub(E, B, g, passes)
+    b = oracle.ref_field_phase_stub(E, B, g, passes)
+    assert_bitwise(a[0], b[0], "E")
+    assert_bitwise(a[1], b[1], "B")
