@@ -175,11 +175,16 @@ __global__ void B2M_WARP_BOUNDS
     if (lane == 0) {
       tma_store_2d(&S.tmap[s], static_cast<int>(sp.col0 + off), 0, buf[st], stream_pol);
       tma_commit();
-      // refill the stage of tile k-1, whose store was issued a whole tile ago
-      // (its shared-memory read is long done): no wait on the store just issued
-      if (k > 0) {
-        tma_wait_read<1>();
-        issue();  // tile k-1+stages into the stage of tile k-1
+      if (kWarpStages >= 3) {
+        // refill the stage of tile k-1, whose store was issued a whole tile
+        // ago (its shared-memory read is long done): no wait on this store
+        if (k > 0) {
+          tma_wait_read<1>();
+          issue();  // tile k-1+stages into the stage of tile k-1
+        }
+      } else {
+        tma_wait_read<0>();  // two stages: this tile's stage is the next refill
+        issue();             // tile k+2 into it
       }
     }
     __syncwarp();
