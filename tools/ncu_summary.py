@@ -42,7 +42,8 @@ def main():
     iN, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     tot = collections.defaultdict(float)
     cnt = collections.Counter()
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "second": 1e6, "s": 1e6}
     for r in rows[1:]:
         name = r[iN].split("(")[0].replace("void ", "")[:80]
         tot[name] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)

@@ -8,7 +8,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 grid = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
 batches = gem.init_gem_species(grid, 216, pinned=True)
 mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
-st = DeviceStore(grid, [b.count() for b in batches], "fast")
+st = DeviceStore(grid, [b.count() for b in batches], os.environ.get("B2M_MODE", "fast"))
 st.upload_field(gem.gem_field(grid))
 for s, b in enumerate(batches): st.upload(s, b.span())
 for s in range(4): st.sort(s)
