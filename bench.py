@@ -317,22 +317,28 @@ def run_ours(args):
     # of the resident state after the timed steps, rho + J for all species
     moments = None
     if args.moments:
-        store.moments_zero(False)
-        for s, b in enumerate(batches):
-            store.deposit(s, b.q_per_particle)  # warm-up
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        store.moments_zero(False)
-        a.record()
-        for s, b in enumerate(batches):
-            store.deposit(s, b.q_per_particle)
-        b_.record()
-        torch.cuda.synchronize()
-        store.sync()
-        dep_ms = a.elapsed_time(b_)
-        moments = {"value": n_total / (dep_ms * 1e-3) / 1e6, "unit": "MPA/s", "ms": dep_ms,
-                   "what": "deposit_moments rho+J, all species, device-resident state after "
-                           "the timed steps (cell-sorted every --resort steps)",
-                   "hbm_frac": 48 * n_total / (dep_ms * 1e-3) / 1e9 / load_peaks()[0]}
+        def deposit_ms():
+            store.moments_zero(False)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for s, b in enumerate(batches):
+                store.deposit(s, b.q_per_particle)
+            b_.record()
+            torch.cuda.synchronize()
+            store.sync()
+            return a.elapsed_time(b_)
+        deposit_ms()  # warm-up
+        drifted = deposit_ms()   # the state the timed steps left (drifted since the last sort)
+        for s in range(len(batches)):
+            store.sort(s)
+        fresh = deposit_ms()     # right after a cell sort
+        moments = {"value": n_total / (fresh * 1e-3) / 1e6, "unit": "MPA/s", "ms": fresh,
+                   "what": "deposit_moments rho+J, all species, device-resident C2 state right "
+                           "after a cell sort",
+                   "ms_drifted": drifted,
+                   "drifted_what": "the same on the state left by the timed steps (particles "
+                                   "drifted out of cell order: more per-run mesh updates)",
+                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / load_peaks()[0]}
     store.close()
 
     peak, peak_src = load_peaks()
