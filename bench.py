@@ -227,7 +227,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # B2M_SLAB_PATH=1 runs the partition-layer step (mover fused with the
+    # owner scan + compaction + exchange + count all-reduce) even at N = 1, to
+    # measure what the multi-GPU step adds over the plain mover
+    if world > 1 or os.environ.get("B2M_SLAB_PATH") == "1":
         from paper_1904_03684_b200 import partition
         return partition.bench_world(args)
 

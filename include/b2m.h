@@ -241,6 +241,9 @@ int b2m_owner_of(const b2m_grid* g, int world, double y);
  * place preserving scan order.  A particle landing in a non-neighbour slab
  * records a CflViolation.  Asynchronous. */
 b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp);
+/* All species (mp[n_species]) in one mover launch, then each species'
+ * compaction -- the per-cycle form of the above. */
+b2m_status b2m_move_migrate_all(b2m_ctx* ctx, const b2m_mover_params* mp);
 /* After b2m_sync: outbox of species s towards dir (0 = prev, 1 = next);
  * device pointer to count records. */
 b2m_status b2m_outbox(b2m_ctx* ctx, int s, int dir, double** d_recs, uint64_t* count);

@@ -94,6 +94,7 @@ SIGNATURES = {
     "b2m_slab_config": (_st, [C.c_void_p, C.c_int, C.c_int]),
     "b2m_owner_of": (C.c_int, [C.POINTER(b2m_grid), C.c_int, C.c_double]),
     "b2m_move_migrate": (_st, [C.c_void_p, C.c_int, C.POINTER(b2m_mover_params)]),
+    "b2m_move_migrate_all": (_st, [C.c_void_p, C.POINTER(b2m_mover_params)]),
     "b2m_outbox": (_st, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_u64)]),
     "b2m_inbox_append": (_st, [C.c_void_p, C.c_int, C.c_void_p, _u64]),
     "b2m_gem_counts": (_st, [C.POINTER(b2m_grid), C.c_int, C.POINTER(_u64)]),

@@ -107,7 +107,8 @@ struct Species {
   uint64_t count = 0;
   // migration scratch
   uint8_t* flags = nullptr;
-  uint32_t* blk = nullptr;  // [3][nb] counts + [3][nb] offsets
+  unsigned long long* tcnt = nullptr;  // per-tile packed leaver counts (next << 32 | prev)
+  unsigned long long* toff = nullptr;  // their exclusive scan
   double* out[2] = {};
   uint64_t cap_out = 0;
   unsigned long long* holes = nullptr;
@@ -1027,15 +1028,44 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
   ctx->sl.slab = slab;
   ctx->sl.dy = ctx->grid.dy;
   ctx->sl.ny = ctx->grid.ny;
+  // y-range of slab r under owner_of (runtime.cpp:39-44): trunc(RN(y/dy))
+  // reaches m exactly from the smallest y with RN(y/dy) >= m on (RN(y/dy) is
+  // monotone in y); the last slab also takes the clamped j >= ny
+  auto first_y = [&](int m) {
+    if (m <= 0) return 0.0;
+    uint64_t lo = 0, hi = 0;
+    const double top = 2.0 * ctx->grid.ly;
+    std::memcpy(&hi, &top, sizeof(double));
+    while (lo < hi) {  // smallest bit pattern with (y / dy) >= m
+      const uint64_t mid = lo + (hi - lo) / 2;
+      double y;
+      std::memcpy(&y, &mid, sizeof(double));
+      if (y / ctx->grid.dy >= static_cast<double>(m))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    double y;
+    std::memcpy(&y, &lo, sizeof(double));
+    return y;
+  };
+  auto range = [&](int r, double& a, double& b) {
+    a = first_y(r * slab);
+    b = r == world - 1 ? std::numeric_limits<double>::infinity() : first_y((r + 1) * slab);
+  };
+  range(rank, ctx->sl.own_lo, ctx->sl.own_hi);
+  range(ctx->sl.prev, ctx->sl.prev_lo, ctx->sl.prev_hi);
+  range(ctx->sl.next, ctx->sl.next_lo, ctx->sl.next_hi);
   ctx->slab_on = true;
   // migration scratch per species
   for (Species& S : ctx->sp) {
     if (S.flags) continue;
     const uint64_t cap = S.capacity;
-    const int nb = std::max(1, flag_blocks(cap));
+    const uint64_t nt = std::max<uint64_t>(1, migrate_tiles(cap));
     S.cap_out = std::max<uint64_t>(std::min<uint64_t>(cap, 1u << 16), cap / 8);
     if ((st = dalloc(ctx, &S.flags, cap, "migration flags")) != B2M_OK) return st;
-    if ((st = dalloc(ctx, &S.blk, 6 * static_cast<size_t>(nb), "block counts")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.tcnt, nt, "tile counts")) != B2M_OK) return st;
+    if ((st = dalloc(ctx, &S.toff, nt, "tile offsets")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[0], 6 * S.cap_out, "outbox prev")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[1], 6 * S.cap_out, "outbox next")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.holes, cap, "hole list")) != B2M_OK) return st;
@@ -1044,7 +1074,7 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
       cudaGetLastError();
       return fail(B2M_ALLOC_ERROR, "pinned migration totals");
     }
-    const size_t need = scan_temp_bytes(nb);
+    const size_t need = scan_temp_bytes(nt);
     if (need > ctx->scan_temp_bytes) {
       char* tmp = nullptr;
       if ((st = dalloc(ctx, &tmp, need, "scan temp")) != B2M_OK) return st;
@@ -1055,43 +1085,82 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
   return B2M_OK;
 }
 
+// Migration bookkeeping after the mover wrote species s's flags: per-block
+// counts, scan, outbox scatter, totals to the host.
+static b2m_status migrate_compact(b2m_ctx* ctx, int s, const SpeciesLaunch& L) {
+  Species& S = ctx->sp[static_cast<size_t>(s)];
+  launch_scan_tiles(ctx->scan_temp, ctx->scan_temp_bytes, S.tcnt, S.toff,
+                    migrate_tiles(S.count), S.totals, ctx->stream);
+  launch_scatter_tiles(L, S.flags, S.tcnt, S.toff, S.out[0], S.out[1], S.cap_out, S.holes,
+                       ctx->stream);
+  B2M_CUDA(ctx, cudaMemcpyAsync(S.totals_h, S.totals, 3 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  return B2M_OK;
+}
+
+// The mover over `n` species in ONE launch, fused with the owner scan (each
+// particle gets its destination flag), then each species' compaction.
+static b2m_status move_migrate_species(b2m_ctx* ctx, const int* species,
+                                       const b2m_mover_params* mp, int n) {
+  b2m_status st;
+  if (!ctx->slab_on) return fail(B2M_CONFIG_ERROR, "move_migrate: call b2m_slab_config first");
+  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
+  ensure_tables(ctx, species, mp, n);
+  std::vector<SpeciesLaunch> L;
+  std::vector<uint8_t*> fl;
+  std::vector<unsigned long long*> tc;
+  std::vector<int> live;
+  for (int m = 0; m < n; ++m) {
+    const int s = species[m];
+    Species& S = ctx->sp[static_cast<size_t>(s)];
+    S.pre_count = S.count;
+    S.migrate_pending = true;
+    if (S.count == 0) {
+      std::memset(S.totals_h, 0, 3 * sizeof(unsigned long long));
+      continue;
+    }
+    L.push_back(make_launch(ctx, s, mp[m], 0, S.count));
+    fl.push_back(S.flags);
+    tc.push_back(S.tcnt);
+    live.push_back(s);
+  }
+  if (L.empty()) return B2M_OK;
+  const int nl = static_cast<int>(L.size());
+  const bool ok =
+      ctx->mode == B2M_MODE_STRICT
+          ? launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB,
+                                     L.data(), nl, ctx->fault, ctx->stream, &ctx->sl, fl.data(),
+                                     tc.data())
+          : launch_move_fast(to_fast(ctx->grid), L.data(), nl, ctx->fault, ctx->stream, &ctx->sl,
+                             fl.data(), tc.data());
+  if (!ok) return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
+  for (int m = 0; m < nl; ++m)
+    if ((st = migrate_compact(ctx, live[static_cast<size_t>(m)], L[static_cast<size_t>(m)])) !=
+        B2M_OK)
+      return st;
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
 b2m_status b2m_move_migrate(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
   b2m_status st = check_ctx(ctx);
   if (st != B2M_OK) return st;
   if ((st = check_species(ctx, s)) != B2M_OK) return st;
   if ((st = check_params(mp)) != B2M_OK) return st;
-  if (!ctx->slab_on) return fail(B2M_CONFIG_ERROR, "move_migrate: call b2m_slab_config first");
-  if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
-  Species& S = ctx->sp[static_cast<size_t>(s)];
-  ensure_tables(ctx, &s, mp, 1);
-  const SpeciesLaunch L = make_launch(ctx, s, *mp, 0, S.count);
-  S.pre_count = S.count;
-  S.migrate_pending = true;
-  if (S.count == 0) {
-    std::memset(S.totals_h, 0, 3 * sizeof(unsigned long long));
-    return B2M_OK;
+  return move_migrate_species(ctx, &s, mp, 1);
+}
+
+b2m_status b2m_move_migrate_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
+  const int ns = static_cast<int>(ctx->sp.size());
+  std::vector<int> all(static_cast<size_t>(ns));
+  for (int s = 0; s < ns; ++s) {
+    if ((st = check_params(&mp[s])) != B2M_OK) return st;
+    all[static_cast<size_t>(s)] = s;
   }
-  const int nb = flag_blocks(S.count);
-  if (ctx->mode == B2M_MODE_STRICT) {
-    uint8_t* fl[1] = {S.flags};
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
-                                  ctx->stream, &ctx->sl, fl))
-      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-    launch_count_flags(S.flags, S.count, S.blk, ctx->stream);
-  } else {
-    // the production mover writes the flags itself; a light kernel counts them
-    uint8_t* fl[1] = {S.flags};
-    if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, &ctx->sl,
-                          fl))
-      return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-    launch_count_flags(S.flags, S.count, S.blk, ctx->stream);
-  }
-  launch_scan_blocks(ctx->scan_temp, ctx->scan_temp_bytes, S.blk, nb, S.totals, ctx->stream);
-  launch_scatter_out(L, S.flags, S.blk, S.out[0], S.out[1], S.cap_out, S.holes, ctx->stream);
-  B2M_CUDA(ctx, cudaMemcpyAsync(S.totals_h, S.totals, 3 * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, ctx->stream));
-  B2M_CUDA(ctx, cudaGetLastError());
-  return B2M_OK;
+  return move_migrate_species(ctx, all.data(), mp, ns);
 }
 
 b2m_status b2m_outbox(b2m_ctx* ctx, int s, int dir, double** d_recs, uint64_t* count) {

@@ -32,12 +32,14 @@ FastGrid to_fast(const b2m_grid& g);
 struct SlabLaunch;
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st,
-                      const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr);
+                      const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr,
+                      unsigned long long* const* tcnt = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
                               const double* B, const SpeciesLaunch* sp, int n_spans,
                               FaultWord* fault, cudaStream_t st, const SlabLaunch* sl = nullptr,
-                              uint8_t* const* flags = nullptr);
+                              uint8_t* const* flags = nullptr,
+                              unsigned long long* const* tcnt = nullptr);
 // Node AoS E/B -> per-cell polynomial coefficients of (scale[m]*E,
 // scale[m]*B) into tables[m] (48 doubles per cell), one field read per
 // kMaxTables tables.
@@ -80,21 +82,26 @@ struct SlabLaunch {
   int slab;        // ny / world
   double dy;       // owner_of divisor (grid.hpp Grid::dy)
   int ny;
+  // owner_of(y) == r  <=>  y in [lo_r, hi_r): exact thresholds of the
+  // reference's trunc(y / dy) (b2m_slab_config), for this rank, prev, next
+  double own_lo, own_hi, prev_lo, prev_hi, next_lo, next_hi;
 };
 
-// The movers above, given `sl` and `flags`, also run the owner_of scan and
-// write flags[i] (0 stay, 1 prev, 2 next).
-int flag_blocks(uint64_t n);
-// per-block (prev, next, any) counts of an existing flag array
-void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStream_t st);
-// In-place exclusive scan of the 3-wide per-block counts; totals[3] written.
-size_t scan_temp_bytes(int n_blocks);
-void launch_scan_blocks(void* temp, size_t temp_bytes, uint32_t* blk, int n_blocks,
-                        unsigned long long* totals, cudaStream_t st);
+// The movers above, given `sl`, `flags` and `tcnt`, also run the owner_of
+// scan: flags[i] (0 stay, 1 prev, 2 next) and, per 128-particle tile t,
+// tcnt[t] = next << 32 | prev.
+uint64_t migrate_tiles(uint64_t n);
+// Exclusive scan of the packed tile counts -> per-tile offsets; totals[3] =
+// prev, next, all leavers.
+size_t scan_temp_bytes(uint64_t n_tiles);
+void launch_scan_tiles(void* temp, size_t temp_bytes, const unsigned long long* cnt,
+                       unsigned long long* off, uint64_t n_tiles, unsigned long long* totals,
+                       cudaStream_t st);
 // Leavers -> outboxes (AoS PartRec, scan order); hole list (ascending).
-void launch_scatter_out(const SpeciesLaunch& sp, const uint8_t* flags, const uint32_t* blk,
-                        double* out_prev, double* out_next, uint64_t cap_out,
-                        unsigned long long* holes, cudaStream_t st);
+void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
+                          const unsigned long long* cnt, const unsigned long long* off,
+                          double* out_prev, double* out_next, uint64_t cap_out,
+                          unsigned long long* holes, cudaStream_t st);
 // Fill holes with incoming records, then append / compact the tail.
 void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
                  const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st);

@@ -33,12 +33,14 @@ __device__ __forceinline__ void store6(const SpeciesLaunch& sp, unsigned long lo
   sp.u[i] = p[3]; sp.v[i] = p[4]; sp.w[i] = p[5];
 }
 
-// owner_of (runtime.cpp:39-44) with the reference's IEEE division.
-__device__ __forceinline__ int owner_of_slab(double y, const SlabLaunch& sl) {
-  int j = __double2int_rz(__ddiv_rn(y, sl.dy));
-  if (j >= sl.ny) j = sl.ny - 1;
-  if (j < 0) j = 0;
-  return j / sl.slab;
+// Migration flag of a (wrapped, finite) new y: 0 stays, 1 prev, 2 next,
+// 3 another slab (CflViolation).  owner_of (runtime.cpp:39-44) evaluated
+// through the exact thresholds of trunc(RN(y/dy)) -- no division.
+__device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
+  if (y >= sl.own_lo && y < sl.own_hi) return 0;
+  if (y >= sl.prev_lo && y < sl.prev_hi) return 1;
+  if (y >= sl.next_lo && y < sl.next_hi) return 2;
+  return 3;
 }
 
 // FAST mover with warp-private TMA pipelines: every warp streams its own
@@ -107,6 +109,7 @@ __global__ void B2M_WARP_BOUNDS
     const unsigned long long left = sp.n - off;
     const int cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
     mbar_wait(&bar[st], phase);
+    unsigned n_prev = 0, n_next = 0;  // this lane's leavers in the tile
     if (STRICT) {
       CellCache cc;
       cc.cell = -1;
@@ -119,17 +122,15 @@ __global__ void B2M_WARP_BOUNDS
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
-            const int dest = owner_of_slab(buf[st][1][p], sl);
-            if (dest != sl.rank) {
-              if (dest == sl.prev)
-                flag = 1;
-              else if (dest == sl.next)
-                flag = 2;
-              else
-                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+            flag = slab_flag(buf[st][1][p], sl);
+            if (flag == 3) {
+              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+              flag = 0;
             }
           }
           flags[off + p] = static_cast<uint8_t>(flag);
+          n_prev += flag == 1;
+          n_next += flag == 2;
         }
       }
     } else {
@@ -156,19 +157,23 @@ __global__ void B2M_WARP_BOUNDS
           // destination records a CflViolation
           int flag = 0;
           if (!bad) {
-            const int dest = owner_of_slab(buf[st][1][p], sl);
-            if (dest != sl.rank) {
-              if (dest == sl.prev)
-                flag = 1;
-              else if (dest == sl.next)
-                flag = 2;
-              else
-                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+            flag = slab_flag(buf[st][1][p], sl);
+            if (flag == 3) {
+              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+              flag = 0;
             }
           }
           flags[off + p] = static_cast<uint8_t>(flag);
+          n_prev += flag == 1;
+          n_next += flag == 2;
         }
       }
+    }
+    if (S.tcnt[s]) {  // per-tile leaver counts: the scan input of the compaction
+      const unsigned cp = __reduce_add_sync(0xffffffffu, n_prev);
+      const unsigned cn = __reduce_add_sync(0xffffffffu, n_next);
+      if (lane == 0)
+        S.tcnt[s][tile - S.tile_start[s]] = (static_cast<unsigned long long>(cn) << 32) | cp;
     }
     fence_proxy_async();
     __syncwarp();
@@ -283,84 +288,65 @@ __global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __r
 
 // ---- migration ------------------------------------------------------------
 
-constexpr int kFlagThreads = 256;
+// ---- migration compaction (partition_outgoing, runtime.cpp:46-62) ---------
+// The mover wrote a flag per particle (0 stay, 1 prev, 2 next) and, per
+// 128-particle tile, the packed counts (next << 32 | prev).  An exclusive scan
+// of the packed counts gives every tile its outbox offsets (prev, next) and
+// hole offset (prev + next); one block per tile then writes its leavers in
+// scan order.  Tiles without leavers (most of them) return after one load.
+constexpr int kTileParticles = 32 * B2M_FAST_PPT;
 
-// Per-block counts (prev, next, any) of the flags the mover wrote, for the
-// scan that orders the outboxes.
-__global__ void __launch_bounds__(kFlagThreads)
-    count_flags_kernel(const uint8_t* __restrict__ flags, unsigned long long n,
-                       uint32_t* __restrict__ blk, unsigned n_blocks) {
-  const unsigned long long i =
-      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
-  const int flag = i < n ? flags[i] : 0;
-  const int c_prev = __syncthreads_count(flag == 1);
-  const int c_next = __syncthreads_count(flag == 2);
-  const int c_any = __syncthreads_count(flag != 0);
+__global__ void tile_totals_kernel(const unsigned long long* cnt, const unsigned long long* off,
+                                   unsigned long long n_tiles, unsigned long long* totals) {
   if (threadIdx.x == 0) {
-    blk[blockIdx.x] = static_cast<uint32_t>(c_prev);
-    blk[n_blocks + blockIdx.x] = static_cast<uint32_t>(c_next);
-    blk[2 * n_blocks + blockIdx.x] = static_cast<uint32_t>(c_any);
+    const unsigned long long t = off[n_tiles - 1] + cnt[n_tiles - 1];
+    totals[0] = t & 0xffffffffull;  // prev
+    totals[1] = t >> 32;            // next
+    totals[2] = totals[0] + totals[1];
   }
 }
 
-__global__ void totals_kernel(const uint32_t* counts, const uint32_t* offsets, unsigned n_blocks,
-                              unsigned long long* totals) {
-  const int t = threadIdx.x;
-  if (t < 3) {
-    const unsigned last = n_blocks - 1;
-    totals[t] = static_cast<unsigned long long>(offsets[t * n_blocks + last]) +
-                counts[t * n_blocks + last];
-  }
-}
-
-// Block-wide exclusive ranks of three predicates via warp ballots.
-__device__ __forceinline__ void block_ranks(int flag, int* r_prev, int* r_next, int* r_any) {
-  __shared__ int warp_tot[3][kFlagThreads / 32];
+__global__ void __launch_bounds__(kTileParticles)
+    scatter_tiles_kernel(const __grid_constant__ SpeciesLaunch sp, const uint8_t* __restrict__ flags,
+                         const unsigned long long* __restrict__ cnt,
+                         const unsigned long long* __restrict__ off, unsigned long long n_tiles,
+                         double* __restrict__ out_prev, double* __restrict__ out_next,
+                         unsigned long long cap_out, unsigned long long* __restrict__ holes) {
+  __shared__ int warp_tot[2][kTileParticles / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const unsigned bp = __ballot_sync(~0u, flag == 1);
-  const unsigned bn = __ballot_sync(~0u, flag == 2);
-  const unsigned ba = __ballot_sync(~0u, flag != 0);
-  if (lane == 0) {
-    warp_tot[0][wid] = __popc(bp);
-    warp_tot[1][wid] = __popc(bn);
-    warp_tot[2][wid] = __popc(ba);
-  }
-  __syncthreads();
-  int op = 0, on = 0, oa = 0;
-  for (int w = 0; w < wid; ++w) {
-    op += warp_tot[0][w];
-    on += warp_tot[1][w];
-    oa += warp_tot[2][w];
-  }
-  *r_prev = op + __popc(bp & lt);
-  *r_next = on + __popc(bn & lt);
-  *r_any = oa + __popc(ba & lt);
-}
-
-__global__ void __launch_bounds__(kFlagThreads)
-    scatter_out_kernel(const __grid_constant__ SpeciesLaunch sp, const uint8_t* __restrict__ flags,
-                       const uint32_t* __restrict__ offs, unsigned n_blocks,
-                       double* __restrict__ out_prev, double* __restrict__ out_next,
-                       unsigned long long cap_out, unsigned long long* __restrict__ holes) {
-  const unsigned long long i =
-      static_cast<unsigned long long>(blockIdx.x) * kFlagThreads + threadIdx.x;
-  const int flag = i < sp.n ? flags[i] : 0;
-  int rp, rn, ra;
-  block_ranks(flag, &rp, &rn, &ra);
-  if (flag == 0) return;
-  const unsigned long long hp = offs[blockIdx.x] + static_cast<unsigned long long>(rp);
-  const unsigned long long hn = offs[n_blocks + blockIdx.x] + static_cast<unsigned long long>(rn);
-  const unsigned long long ha = offs[2 * n_blocks + blockIdx.x] + static_cast<unsigned long long>(ra);
-  holes[ha] = i;
-  double* dst = nullptr;
-  if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
-  if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
-  if (dst) {
-    double p[6];
-    load6(sp, i, p);
+  // grid-stride over tiles: a tile without leavers costs one load
+  for (unsigned long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    if (cnt[t] == 0) continue;  // uniform across the block
+    const unsigned long long i = t * kTileParticles + threadIdx.x;
+    const int flag = i < sp.n ? flags[i] : 0;
+    const unsigned bp = __ballot_sync(~0u, flag == 1);
+    const unsigned bn = __ballot_sync(~0u, flag == 2);
+    __syncthreads();  // warp_tot of the previous tile has been read
+    if (lane == 0) {
+      warp_tot[0][wid] = __popc(bp);
+      warp_tot[1][wid] = __popc(bn);
+    }
+    __syncthreads();
+    if (flag == 0) continue;
+    int rp = __popc(bp & lt), rn = __popc(bn & lt);
+    for (int w = 0; w < wid; ++w) {
+      rp += warp_tot[0][w];
+      rn += warp_tot[1][w];
+    }
+    const unsigned long long o = off[t];
+    const unsigned long long op = o & 0xffffffffull, on = o >> 32;
+    const unsigned long long hp = op + rp, hn = on + rn;
+    holes[op + on + rp + rn] = i;  // all leavers in index order
+    double* dst = nullptr;
+    if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
+    if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
+    if (dst) {
+      double p[6];
+      load6(sp, i, p);
 #pragma unroll
-    for (int a = 0; a < 6; ++a) dst[a] = p[a];
+      for (int a = 0; a < 6; ++a) dst[a] = p[a];
+    }
   }
 }
 
@@ -449,7 +435,8 @@ bool encode_species_map(CUtensorMap* map, const SpeciesLaunch& sp, int box_cols)
 
 template <bool STRICT>
 bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                       cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
+                       cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
+                       unsigned long long* const* tcnt) {
   constexpr int P = B2M_FAST_PPT;
   constexpr int WT = 32 * P;
   constexpr int smem = (kWarpThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
@@ -478,6 +465,7 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
       if (sp[s].col0 + sp[s].n > 0x7fffffffull) return false;  // 32-bit TMA coordinates
       S.sp[S.n] = sp[s];
       S.flags[S.n] = flags ? flags[s] : nullptr;
+      S.tcnt[S.n] = flags && tcnt ? tcnt[s] : nullptr;
       if (!encode_species_map(&S.tmap[S.n], sp[s], WT)) return false;
       S.tile_start[S.n] = tiles;
       tiles += (sp[s].n + WT - 1) / WT;
@@ -496,22 +484,23 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
 }
 
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
-                      cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags) {
+                      cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
+                      unsigned long long* const* tcnt) {
   TileField F{};
   F.fg = g;
-  return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags);
+  return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags, tcnt);
 }
 
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
                               const double* B, const SpeciesLaunch* sp, int n_spans,
                               FaultWord* fault, cudaStream_t st, const SlabLaunch* sl,
-                              uint8_t* const* flags) {
+                              uint8_t* const* flags, unsigned long long* const* tcnt) {
   TileField F{};
   F.dg = g;
   F.fg = fg;  // wrap thresholds (WrapAxis)
   F.E = E;
   F.B = B;
-  return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags);
+  return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags, tcnt);
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
@@ -579,45 +568,40 @@ void launch_sort_pairs(void* temp, size_t temp_bytes, const uint32_t* kin, uint3
   note_launch((key_bits + 7) / 8 + 1);
 }
 
-int flag_blocks(uint64_t n) { return static_cast<int>(grid_for(n, kFlagThreads)); }
+uint64_t migrate_tiles(uint64_t n) { return (n + kTileParticles - 1) / kTileParticles; }
 
-void launch_count_flags(const uint8_t* flags, uint64_t n, uint32_t* blk, cudaStream_t st) {
-  const unsigned nb = static_cast<unsigned>(flag_blocks(n));
-  if (nb == 0) return;
-  count_flags_kernel<<<nb, kFlagThreads, 0, st>>>(flags, n, blk, nb);
-  note_launch();
-}
-
-size_t scan_temp_bytes(int n_blocks) {
+size_t scan_temp_bytes(uint64_t n_tiles) {
   size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
-                                static_cast<uint32_t*>(nullptr), n_blocks);
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), n_tiles);
   return bytes;
 }
 
-void launch_scan_blocks(void* temp, size_t temp_bytes, uint32_t* blk, int n_blocks,
-                        unsigned long long* totals, cudaStream_t st) {
-  // blk holds [3][n_blocks] counts followed by [3][n_blocks] offsets
-  uint32_t* counts = blk;
-  uint32_t* offs = blk + 3 * static_cast<size_t>(n_blocks);
-  for (int t = 0; t < 3; ++t) {
-    size_t b = temp_bytes;
-    cub::DeviceScan::ExclusiveSum(temp, b, counts + static_cast<size_t>(t) * n_blocks,
-                                  offs + static_cast<size_t>(t) * n_blocks, n_blocks, st);
-    note_launch();
-  }
-  totals_kernel<<<1, 32, 0, st>>>(counts, offs, static_cast<unsigned>(n_blocks), totals);
+void launch_scan_tiles(void* temp, size_t temp_bytes, const unsigned long long* cnt,
+                       unsigned long long* off, uint64_t n_tiles, unsigned long long* totals,
+                       cudaStream_t st) {
+  size_t b = temp_bytes;
+  cub::DeviceScan::ExclusiveSum(temp, b, cnt, off, n_tiles, st);
+  note_launch();
+  tile_totals_kernel<<<1, 32, 0, st>>>(cnt, off, n_tiles, totals);
   note_launch();
 }
 
-void launch_scatter_out(const SpeciesLaunch& sp, const uint8_t* flags, const uint32_t* blk,
-                        double* out_prev, double* out_next, uint64_t cap_out,
-                        unsigned long long* holes, cudaStream_t st) {
-  const unsigned nb = static_cast<unsigned>(flag_blocks(sp.n));
-  if (nb == 0) return;
-  const uint32_t* offs = blk + 3 * static_cast<size_t>(nb);
-  scatter_out_kernel<<<nb, kFlagThreads, 0, st>>>(sp, flags, offs, nb, out_prev, out_next,
-                                                   cap_out, holes);
+void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
+                          const unsigned long long* cnt, const unsigned long long* off,
+                          double* out_prev, double* out_next, uint64_t cap_out,
+                          unsigned long long* holes, cudaStream_t st) {
+  const uint64_t nt = migrate_tiles(sp.n);
+  if (nt == 0) return;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  scatter_tiles_kernel<<<static_cast<unsigned>(nt < cap ? nt : cap), kTileParticles, 0, st>>>(
+      sp, flags, cnt, off, nt, out_prev, out_next, cap_out, holes);
   note_launch();
 }
 

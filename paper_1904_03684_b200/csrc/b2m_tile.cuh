@@ -138,6 +138,7 @@ struct alignas(64) TensorSpans {
   SpeciesLaunch sp[kMaxTileSpans];
   unsigned long long tile_start[kMaxTileSpans + 1];
   uint8_t* flags[kMaxTileSpans];  // migration: per-particle destination flag (or null)
+  unsigned long long* tcnt[kMaxTileSpans];  // migration: per-tile (next << 32 | prev) counts
   int n;
 };
 // ---------------------------------------------------------------------------

@@ -42,7 +42,10 @@ class DeviceStore:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library may be gone already
+            pass
 
     # -- plumbing -----------------------------------------------------------
     def set_stream(self, stream_handle: int | None):

@@ -88,6 +88,10 @@ class DeviceMigration:
     def move_migrate(self, s: int, mp):
         self._capi.check(self._capi.lib().b2m_move_migrate(self.store.h, s, C.byref(mp.to_c())))
 
+    def move_migrate_all(self, mps):
+        arr = (self._capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+        self._capi.check(self._capi.lib().b2m_move_migrate_all(self.store.h, arr))
+
     def outbox(self, s: int, direction: int):
         import torch
         p = C.c_void_p()
@@ -247,8 +251,11 @@ class SlabWorld:
         st = self.store
         err = None
         try:
-            for s in range(self.ns):
-                st.move_migrate(s, mps[s])
+            if hasattr(st, "move_migrate_all"):
+                st.move_migrate_all(mps)   # one mover launch for every species
+            else:
+                for s in range(self.ns):
+                    st.move_migrate(s, mps[s])
             st.sync()   # NumericalFault / CflViolation, as the reference raises them
         except Exception as e:  # noqa: BLE001 - re-raised after the collective below
             err = e
