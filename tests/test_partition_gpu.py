@@ -89,3 +89,48 @@ def test_gpu_slab_world_nan_fault(gpu):
     res, errs = run_ranks(_rank_fn("strict", 1, inject=(0, 3, float("nan"))), 2)
     assert isinstance(errs[0], NumericalFault) and "particle index 0" in str(errs[0]), errs
     assert isinstance(errs[1], EngineFault), errs
+
+
+@pytest.mark.parametrize("mode", ["fast", "strict"])
+def test_owner_thresholds_at_slab_boundaries(gpu, mode):
+    """The mover's migration scan classifies y through exact thresholds of
+    trunc(y / dy) (b2m_slab_config) instead of dividing: particles at rest
+    placed on every slab boundary and one ulp either side must land in the
+    outbox of exactly the rank owner_of (runtime.cpp:39-44) names."""
+    g = Grid.make(8, 16, 4, 6.4, 3.3, 1.2)   # dy = 0.20625: not a power of two
+    world, rank = 4, 1
+    ys = []
+    for j in range(0, g.ny + 1):
+        b = j * g.dy
+        ys += [np.nextafter(b, -1.0), b, np.nextafter(b, 10.0)]
+    ys = np.array([y for y in ys if 0.0 <= y < g.ly] + [np.nextafter(g.ly, 0.0)])
+    n = len(ys)
+    p6 = [np.full(n, 1.0), ys.copy(), np.full(n, 0.3), np.zeros(n), np.zeros(n), np.zeros(n)]
+    E = np.zeros(3 * g.nodes())
+    B = np.zeros(3 * g.nodes())
+    from paper_1904_03684_b200.mover import FieldMesh
+    store = DeviceStore(g, [n + 64], mode)
+    store.upload_field(FieldMesh(g, E, B))
+    store.upload(0, p6)
+    mig = DeviceMigration(store, rank, world)
+    owners = owner_of(ys, g, world)
+    cfl = np.any((owners != rank) & (owners != (rank + 1) % world) & (owners != (rank - 1) % world))
+    assert cfl  # rank 3 particles must raise: test the neighbour ones separately
+    keep = (owners == rank) | (owners == 0) | (owners == 2)
+    p6 = [a[keep] for a in p6]
+    store.upload(0, p6)
+    mig.move_migrate(0, MoverParams.make(0.1, 1.0, 3))
+    mig.sync()
+    to_prev = mig.outbox(0, 0).cpu().numpy()
+    to_next = mig.outbox(0, 1).cpu().numpy()
+    want = owner_of(p6[1], g, world)
+    np.testing.assert_array_equal(np.sort(to_prev[:, 1]), np.sort(p6[1][want == 0]))
+    np.testing.assert_array_equal(np.sort(to_next[:, 1]), np.sort(p6[1][want == 2]))
+    mig.inbox_append(0, torch.empty((0, 6), dtype=torch.float64, device="cuda"))
+    mig.sync()
+    assert store.count(0) + len(to_prev) + len(to_next) == len(p6[0])
+    stay = [np.empty(store.count(0)) for _ in range(6)]
+    store.download(0, stay)
+    store.sync()
+    np.testing.assert_array_equal(np.sort(stay[1]), np.sort(p6[1][want == rank]))
+    store.close()
