@@ -16,6 +16,8 @@ namespace b2m {
 void set_error(const std::string& msg);
 b2m_status fail(b2m_status s, const std::string& msg);
 
+// SM count of the device (queried once; every GPU of the process is a B200).
+int device_sms();
 // Count of kernel launches issued by this process (b2m_launch_count).
 void note_launch(int n = 1);
 

@@ -392,6 +392,20 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+}  // namespace
+
+int device_sms() {
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 1;
+  }();
+  return sms;
+}
+
+namespace {
+
 unsigned grid_for(uint64_t n, int threads) {
   return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -441,8 +455,9 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
   constexpr int WT = 32 * P;
   constexpr int smem = (kWarpThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
   static_assert(smem <= 227 * 1024, "warp tiles exceed shared memory");
-  static int grid_cap = -1;
-  if (grid_cap < 0) {
+  // resident grid, computed once (thread-safe static initialisation: engines
+  // on several host threads may launch concurrently)
+  static const int grid_cap = [] {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -450,13 +465,14 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
                          smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT>,
                                                   kWarpThreads, smem);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    int cap = sms * (per_sm > 0 ? per_sm : 1);
     // diagnostics: B2M_BLOCKS_PER_SM=k runs the persistent grid with k blocks per SM
     if (const char* e = std::getenv("B2M_BLOCKS_PER_SM")) {
       const int k = std::atoi(e);
-      if (k > 0 && k < per_sm) grid_cap = sms * k;
+      if (k > 0 && k < per_sm) cap = sms * k;
     }
-  }
+    return cap;
+  }();
   for (int base = 0; base < n_spans; base += kMaxTileSpans) {
     TensorSpans S{};
     unsigned long long tiles = 0;
@@ -593,13 +609,7 @@ void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
                           unsigned long long* holes, cudaStream_t st) {
   const uint64_t nt = migrate_tiles(sp.n);
   if (nt == 0) return;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  const uint64_t cap = static_cast<uint64_t>(device_sms()) * 16;
   scatter_tiles_kernel<<<static_cast<unsigned>(nt < cap ? nt : cap), kTileParticles, 0, st>>>(
       sp, flags, cnt, off, nt, out_prev, out_next, cap_out, holes);
   note_launch();

@@ -151,12 +151,7 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
 void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double* const* mesh,
                     bool pressure, bool exact, FaultWord* fault, cudaStream_t st) {
   if (sp.n == 0) return;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   // enough lanes to fill the GPU, each a contiguous range of whole groups
   const unsigned long long lanes = static_cast<unsigned long long>(sms) * 12 * 32;
   unsigned long long span = (sp.n + lanes - 1) / lanes;
