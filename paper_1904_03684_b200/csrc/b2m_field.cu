@@ -21,20 +21,18 @@ unsigned grid_for(long long n, int threads) {
   return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
+// grid (ceil(3*nx / threads), ny, nz): a thread per (i, component) of one
+// (j, k) row -- no 64-bit index divisions
 __global__ void __launch_bounds__(kStubThreads)
     field_stub_kernel(int nx, int ny, int nz, const double* __restrict__ cur,
                       double* __restrict__ nxt) {
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long unique = static_cast<long long>(nx) * ny * nz;
-  if (t >= 3 * unique) return;
-  const int a = static_cast<int>(t % 3);
-  const long long u = t / 3;
-  const int i = static_cast<int>(u % nx);
-  const int j = static_cast<int>((u / nx) % ny);
-  const int k = static_cast<int>(u / (static_cast<long long>(nx) * ny));
-  const int im = (i + nx - 1) % nx, ip = (i + 1) % nx;
-  const int jm = (j + ny - 1) % ny, jp = (j + 1) % ny;
-  const int km = (k + nz - 1) % nz, kp = (k + 1) % nz;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * nx) return;
+  const int a = t % 3, i = t / 3;
+  const int j = blockIdx.y, k = blockIdx.z;
+  const int im = i == 0 ? nx - 1 : i - 1, ip = i + 1 == nx ? 0 : i + 1;
+  const int jm = j == 0 ? ny - 1 : j - 1, jp = j + 1 == ny ? 0 : j + 1;
+  const int km = k == 0 ? nz - 1 : k - 1, kp = k + 1 == nz ? 0 : k + 1;
   const long long sx = nx + 1, sy = ny + 1;
   auto at = [&](int ii, int jj, int kk) { return __ldg(cur + 3 * (ii + sx * (jj + sy * kk)) + a); };
   const double e = at(i, j, k);
@@ -73,13 +71,12 @@ __global__ void __launch_bounds__(kStubThreads)
 double* launch_field_stub(int nx, int ny, int nz, double* E, double* B, double* scratch,
                           int passes, cudaStream_t st) {
   if (passes <= 0) return E;  // the reference returns the input unchanged
-  const long long unique = static_cast<long long>(nx) * ny * nz;
   const long long nodes = static_cast<long long>(nx + 1) * (ny + 1) * (nz + 1);
   double* cur = E;
   double* nxt = scratch;
   for (int p = 0; p < passes; ++p) {
-    field_stub_kernel<<<grid_for(3 * unique, kStubThreads), kStubThreads, 0, st>>>(nx, ny, nz,
-                                                                                   cur, nxt);
+    const dim3 grid(grid_for(3 * nx, kStubThreads), ny, nz);
+    field_stub_kernel<<<grid, kStubThreads, 0, st>>>(nx, ny, nz, cur, nxt);
     note_launch();
     double* t = cur;
     cur = nxt;
