@@ -209,6 +209,11 @@ b2m_status b2m_field_phase_stub_host(const b2m_grid* g, double* E, double* B, in
 b2m_status b2m_moments_zero(b2m_ctx* ctx, int with_pressure);
 b2m_status b2m_deposit(b2m_ctx* ctx, int s, double q_per_particle);
 b2m_status b2m_moments_download(b2m_ctx* ctx, double* const* out, int n_arrays);
+/* Device view of the moment mesh: one contiguous block of n_doubles =
+ * (4 or 10) * nx*ny*nz, arrays in the order above -- for reducing the
+ * per-rank meshes across GPUs (the reference sums per-worker meshes,
+ * runtime.cpp:256-262). */
+b2m_status b2m_moments_device_ptr(b2m_ctx* ctx, double** d_mesh, uint64_t* n_doubles);
 /* One-shot pic::deposit_moments for host arrays: ADDS the n particles'
  * moments into out[0..3] (+ out[4..9] with pressure), nx*ny*nz each.
  * B2M_DOMAIN_ERROR (nothing added) if a particle lies outside the domain. */

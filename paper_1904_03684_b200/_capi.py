@@ -87,6 +87,7 @@ SIGNATURES = {
     "b2m_moments_zero": (_st, [C.c_void_p, C.c_int]),
     "b2m_deposit": (_st, [C.c_void_p, C.c_int, C.c_double]),
     "b2m_moments_download": (_st, [C.c_void_p, C.POINTER(_dp), C.c_int]),
+    "b2m_moments_device_ptr": (_st, [C.c_void_p, C.POINTER(_dp), C.POINTER(_u64)]),
     "b2m_deposit_moments_host": (_st, [C.POINTER(b2m_grid)] + [_dp] * 6 +
                                  [_u64, C.c_double, C.c_int, C.POINTER(_dp)]),
     "b2m_event_record": (_st, [C.c_void_p, C.c_int]),

@@ -965,6 +965,17 @@ b2m_status b2m_moments_download(b2m_ctx* ctx, double* const* out, int n_arrays) 
   return b2m_sync(ctx, nullptr, nullptr);
 }
 
+b2m_status b2m_moments_device_ptr(b2m_ctx* ctx, double** d_mesh, uint64_t* n_doubles) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!d_mesh || !n_doubles) return fail(B2M_INVALID_ARGUMENT, "null argument");
+  if (!ctx->mom[0]) return fail(B2M_CONFIG_ERROR, "moments: call b2m_moments_zero first");
+  const uint64_t nodes = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
+  *d_mesh = ctx->mom[0];
+  *n_doubles = static_cast<uint64_t>(ctx->mom_pressure ? 10 : 4) * nodes;
+  return B2M_OK;
+}
+
 b2m_status b2m_deposit_moments_host(const b2m_grid* g, const double* x, const double* y,
                                     const double* z, const double* u, const double* v,
                                     const double* w, uint64_t n, double q_per_particle,

@@ -129,6 +129,13 @@ class DeviceStore:
     def deposit(self, s: int, q_per_particle: float):
         _capi.check(_capi.lib().b2m_deposit(self.h, s, float(q_per_particle)))
 
+    def moments_device(self):
+        """(device pointer, n_doubles) of the contiguous device moment mesh."""
+        p = _capi._dp()
+        n = C.c_uint64()
+        _capi.check(_capi.lib().b2m_moments_device_ptr(self.h, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value, n.value
+
     def moments_download(self, mesh) -> None:
         """Copy the device moment mesh into ``mesh`` (a MomentMesh) and sync."""
         ptrs = (_capi._dp * len(mesh.arrays))(*[_capi.dptr(a) for a in mesh.arrays])

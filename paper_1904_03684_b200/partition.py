@@ -113,6 +113,18 @@ class DeviceMigration:
     def count(self, s: int) -> int:
         return self.store.count(s)
 
+    # moments of this rank's particles (b2m_deposit), as a device tensor
+    def moments_zero(self, with_pressure: bool = False):
+        self.store.moments_zero(with_pressure)
+
+    def deposit(self, s: int, q_per_particle: float):
+        self.store.deposit(s, q_per_particle)
+
+    def moments_tensor(self):
+        import torch
+        ptr, n = self.store.moments_device()
+        return torch.as_tensor(_CudaArray(ptr, (n,)), device="cuda")
+
 
 class SlabWorld:
     """One rank of the slab-partitioned mover.
@@ -236,6 +248,19 @@ class SlabWorld:
         wait_all(ops)
         a, b = split(from_prev, cp), split(from_next, cn)
         return [torch.cat([x, y], dim=0) if y.shape[0] else x for x, y in zip(a, b)]
+
+    def deposit_moments(self, q_per_particle, with_pressure: bool = False):
+        """Moments of every rank's particles summed over the ranks into every
+        rank's mesh: the reference's per-worker private meshes added up by
+        worker 0 (runtime.cpp:251-262), as one all-reduce of the device mesh."""
+        st = self.store
+        st.moments_zero(with_pressure)
+        for s in range(self.ns):
+            st.deposit(s, q_per_particle[s])
+        st.sync()   # DomainError, as the reference raises it
+        mesh = st.moments_tensor()
+        self._all_reduce(mesh)
+        return mesh
 
     def step(self, mps, check_counts: bool = True):
         """One mover cycle over all species with migration

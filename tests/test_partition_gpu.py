@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 GRID_T = (8, 8, 8, 6.4, 6.4, 6.4)
 
 
-def _rank_fn(mode, cycles, inject=None):
+def _rank_fn(mode, cycles, inject=None, moments=False):
     def fn(rank, dist):
         torch.cuda.set_device(0)
         g = Grid.make(*GRID_T)
@@ -42,6 +42,9 @@ def _rank_fn(mode, cycles, inject=None):
         mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
         for _ in range(cycles):
             sw.step(mps)
+        mesh = None
+        if moments:
+            mesh = sw.deposit_moments([b.q_per_particle for b in batches]).cpu().numpy().copy()
         out = []
         for s in range(4):
             n = store.count(s)
@@ -50,7 +53,7 @@ def _rank_fn(mode, cycles, inject=None):
             out.append(p6)
         store.sync()
         store.close()
-        return out
+        return (out, mesh) if moments else out
     return fn
 
 
@@ -134,3 +137,26 @@ def test_owner_thresholds_at_slab_boundaries(gpu, mode):
     store.sync()
     np.testing.assert_array_equal(np.sort(stay[1]), np.sort(p6[1][want == rank]))
     store.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gpu_slab_world_moments_all_reduce(gpu, world):
+    """Each rank deposits its own particles, one all-reduce sums the device
+    meshes (the reference's worker-0 sum of private meshes,
+    runtime.cpp:251-262): every rank ends with the moments of ALL particles,
+    equal to the oracle's deposit of the union to rounding of the sums."""
+    res, errs = run_ranks(_rank_fn("fast", 2, moments=True), world)
+    assert not any(errs), errs
+    g = Grid.make(*GRID_T)
+    _, qpp = gem.gem_species_params(g, 8)
+    want = np.zeros(4 * g.cells())
+    for s in range(4):
+        union = [np.concatenate([res[r][0][s][a] for r in range(world)]) for a in range(6)]
+        for m, arr in enumerate(oracle.port_deposit_moments(union, GRID_T, float(qpp[s]))):
+            want[m * g.cells():(m + 1) * g.cells()] += arr
+    nc = g.cells()
+    for r in range(world):
+        for m in range(4):   # rho, jx, jy, jz: each to 1e-12 of its own scale
+            w = want[m * nc:(m + 1) * nc]
+            assert np.max(np.abs(res[r][1][m * nc:(m + 1) * nc] - w)) <= 1e-12 * np.max(np.abs(w))
+        np.testing.assert_array_equal(res[r][1], res[0][1])
