@@ -8,8 +8,9 @@
 //   field_to_cells_kernel node-layout E/B (field_mesh.hpp:13-60) -> per-cell
 //                         trilinear polynomial for the FAST gather
 //   cell_keys / gather6   the optional cell-sort pass (+ CUB radix sort)
-//   count_flags / scatter_out / fill_*   outbox compaction and hole filling
-//                         (merge_incoming, runtime.cpp:64-76)
+//   scatter_tiles / fill_*   outbox compaction (scan of the mover's per-tile
+//                         counts) and hole filling (merge_incoming,
+//                         runtime.cpp:64-76)
 #include <cstdlib>
 
 #include <cub/cub.cuh>
@@ -43,7 +44,7 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
   return 3;
 }
 
-// FAST mover with warp-private TMA pipelines: every warp streams its own
+// The mover with warp-private TMA pipelines: every warp streams its own
 // tiles of 32*P particles (kWarpStages deep) through its slice of shared
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
 // tensor-map box per tile carries all six SoA arrays in (and one out); the
