@@ -62,6 +62,7 @@ class B200Engine final : public Engine {
   }
 
   ~B200Engine() override {
+    for (void* p : pinned_) b2m_host_unregister(p);
     if (ctx_) b2m_ctx_destroy(ctx_);
   }
 
@@ -76,6 +77,19 @@ class B200Engine final : public Engine {
     std::memcpy(&g, &grid_, sizeof(g));
     check(b2m_ctx_create(device_, &g, static_cast<int>(caps.size()), caps.data(), mode_, &ctx_),
           "prime");
+    // pinned / prefetch kinds: page-lock the batches' own arrays in place
+    // (their capacity is fixed at allocation, particle_batch.hpp:29-34), so
+    // the per-cycle copies run at full PCIe speed straight from / into them;
+    // the naive kind keeps pageable copies, as NaiveEngine does
+    if (kind_ != EngineKind::naive) {
+      for (ParticleBatch& b : batches) {
+        double* a[6] = {b.xs(), b.ys(), b.zs(), b.us(), b.vs(), b.ws()};
+        for (double* p : a)
+          if (p && b.capacity() &&
+              b2m_host_register(p, b.capacity() * sizeof(double)) == B2M_OK)
+            pinned_.push_back(p);  // best effort: pageable copies still work
+      }
+    }
     stage_next(field, batches);
   }
 
@@ -137,6 +151,7 @@ class B200Engine final : public Engine {
   int mode_ = B2M_MODE_STRICT;
   b2m_ctx* ctx_ = nullptr;
   bool staged_ = false;
+  std::vector<void*> pinned_;
 };
 
 }  // namespace
