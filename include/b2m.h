@@ -103,7 +103,10 @@ b2m_status b2m_mover_params_make(double dt, double qom, int pc_iterations,
  * returns B2M_NUMERICAL_FAULT with *first_bad = index of the first faulting
  * particle; particles [0, first_bad) are updated and [first_bad, n) left
  * untouched, exactly like the reference (kernels.cpp:98-99).
- * Runs on the current device (device 0 unless b2m_set_device was called). */
+ * Runs on the current device (device 0 unless b2m_set_device was called).
+ * Each host thread keeps one cached context (reused while grid, mode and
+ * device match and the capacity suffices), so repeated calls cost the copies
+ * and the kernel only. */
 b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp,
                                const double* E, const double* B, double* x, double* y,
                                double* z, double* u, double* v, double* w, uint64_t n,

@@ -885,9 +885,39 @@ b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp, co
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
-  b2m_ctx* ctx = nullptr;
-  const uint64_t cap = n;
-  if ((st = b2m_ctx_create(dev, g, 1, &cap, mode, &ctx)) != B2M_OK) return st;
+  // One cached context per host thread, reused while the grid, mode and
+  // device match and the capacity suffices: a kernel-level caller moves every
+  // species every cycle, and creating a context per call would dominate.
+  struct Cache {
+    b2m_ctx* ctx = nullptr;
+    b2m_grid grid{};
+    int mode = -1, dev = -1;
+    uint64_t cap = 0;
+    ~Cache() {
+      if (ctx) b2m_ctx_destroy(ctx);
+    }
+  };
+  thread_local Cache cache;
+  if (cache.ctx && (cache.dev != dev || cache.mode != mode || cache.cap < n ||
+                    std::memcmp(&cache.grid, g, sizeof(b2m_grid)) != 0)) {
+    b2m_ctx_destroy(cache.ctx);
+    cache.ctx = nullptr;
+  }
+  if (!cache.ctx) {
+    const uint64_t cap = n;
+    if ((st = b2m_ctx_create(dev, g, 1, &cap, mode, &cache.ctx)) != B2M_OK) {
+      cache.ctx = nullptr;
+      return st;
+    }
+    cache.grid = *g;
+    cache.mode = mode;
+    cache.dev = dev;
+    cache.cap = cap;
+  }
+  b2m_ctx* ctx = cache.ctx;
+  // a previous call's fault must not leak into this one
+  ctx->poisoned = false;
+  launch_fault_reset(ctx->fault, ctx->stream);
   const uint64_t nodes = static_cast<uint64_t>(g->nx + 1) * (g->ny + 1) * (g->nz + 1);
   const double* src[6] = {x, y, z, u, v, w};
   double* dst[6] = {x, y, z, u, v, w};
@@ -903,15 +933,20 @@ b2m_status b2m_move_batch_host(const b2m_grid* g, const b2m_mover_params* mp, co
       const uint64_t keep = st == B2M_OK ? n : static_cast<uint64_t>(bad);
       ctx->poisoned = false;
       b2m_status st2 = b2m_species_download_range(ctx, 0, dst, 0, keep);
-      if (st2 == B2M_OK) st2 = b2m_sync(ctx, nullptr, nullptr);
+      if (st2 == B2M_OK) {
+        B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      }
       if (st == B2M_OK) st = st2;
       else g_last_error = msg;
       if (first_bad) *first_bad = bad;
     }
   }
-  const std::string msg = g_last_error;
-  b2m_ctx_destroy(ctx);
-  g_last_error = msg;
+  if (st != B2M_OK && st != B2M_NUMERICAL_FAULT) {  // unknown state: start afresh next time
+    const std::string msg = g_last_error;
+    b2m_ctx_destroy(cache.ctx);
+    cache.ctx = nullptr;
+    g_last_error = msg;
+  }
   return st;
 }
 
