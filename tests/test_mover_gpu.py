@@ -313,3 +313,39 @@ def test_full_c2_sampled_parity(gpu):
         got = [a[idx] for a in out]
         assert_within_contract(got, want, grid, what=f"C2 species {s}")
         np.testing.assert_array_equal(cells_of(got, grid), cells_of(want, grid))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [1, 31, 127, 128, 129, 4097, 100003])
+def test_ragged_sizes(gpu, mode, n):
+    """Partial tiles (the TMA box clips the tail) and single particles."""
+    grid = (8, 8, 8, 6.4, 6.4, 6.4)
+    E, B = random_field(grid, 4, 0.3)
+    p0 = random_particles(grid, n, 100 + n)
+    check(gpu_move(p0, E, B, grid, 0.1, -25.0, 3, mode), port_move(p0, E, B, grid, 0.1, -25.0, 3),
+          grid, mode, f"n={n}")
+
+
+def test_full_c2_strict_sampled_bitwise(gpu):
+    """BASELINE config 2 at full size in STRICT mode: the whole GEM state
+    moved on the GPU, with the stock GEM field plus the gem_like E (nonzero
+    E); a 100k-particle sample per species is bit-identical to the
+    oracle."""
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    f = gem.gem_bench_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    st = DeviceStore(g, [b.count() for b in batches], "strict")
+    st.upload_field(f)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    st.move_all([MoverParams.make(0.1, b.qom, 3) for b in batches])
+    r = np.random.default_rng(1)
+    for s, b in enumerate(batches):
+        out = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, out)
+        st.sync()
+        idx = np.sort(r.choice(b.count(), size=min(100000, b.count()), replace=False))
+        want = port_move([a[idx].copy() for a in b.span()], E, B, grid, 0.1, b.qom, 3)
+        assert_bitwise([a[idx] for a in out], want, f"C2 strict species {s}")
