@@ -349,3 +349,29 @@ def test_full_c2_strict_sampled_bitwise(gpu):
         idx = np.sort(r.choice(b.count(), size=min(100000, b.count()), replace=False))
         want = port_move([a[idx].copy() for a in b.span()], E, B, grid, 0.1, b.qom, 3)
         assert_bitwise([a[idx] for a in out], want, f"C2 strict species {s}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_host_call_context_cache(gpu, mode):
+    """b2m_move_batch_host keeps one context per host thread: a fault in one
+    call must not leak into the next, and a different grid or a larger batch
+    gets a fresh context -- every call still equals the oracle."""
+    grid = (8, 8, 8, 6.4, 6.4, 6.4)
+    E, B = random_field(grid, 7, 0.3)
+    p = random_particles(grid, 1000, 70)
+    check(gpu_move(p, E, B, grid, 0.1, 1.0, 3, mode), port_move(p, E, B, grid, 0.1, 1.0, 3),
+          grid, mode, "first")
+    bad = [a.copy() for a in p]
+    bad[3][10] = np.nan
+    with pytest.raises(NumericalFault):
+        gpu_move(bad, E, B, grid, 0.1, 1.0, 3, mode)
+    check(gpu_move(p, E, B, grid, 0.1, 1.0, 3, mode), port_move(p, E, B, grid, 0.1, 1.0, 3),
+          grid, mode, "after a fault")
+    big = random_particles(grid, 5000, 71)
+    check(gpu_move(big, E, B, grid, 0.1, 1.0, 3, mode), port_move(big, E, B, grid, 0.1, 1.0, 3),
+          grid, mode, "larger batch")
+    g2 = (4, 6, 5, 2.0, 3.0, 2.5)
+    E2, B2 = random_field(g2, 8, 0.3)
+    p2 = random_particles(g2, 700, 72)
+    check(gpu_move(p2, E2, B2, g2, 0.1, 1.0, 3, mode), port_move(p2, E2, B2, g2, 0.1, 1.0, 3),
+          g2, mode, "other grid")
