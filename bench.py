@@ -403,11 +403,20 @@ def run_ours(args):
                      "traffic": args.traffic if args.traffic is not None
                                 else measured_traffic(args.mode),
                      "traffic_source": "ncu --set full, profiles/r01_c2_bench.json",
-                     "kernel": "warp_tile_kernel (FAST)" if args.mode == "fast"
-                               else "tile_kernel<STRICT>",
+                     "kernel": "warp_tile_kernel<4,0> (FAST)" if args.mode == "fast"
+                               else "warp_tile_kernel<4,1> (STRICT)",
                      "kernel_ms": kernel_ms, "bytes_per_launch": alg_bytes,
                      "sort_share_of_step": sort_share,
                      "peak_source": peak_src},
+        # the resource that actually binds this kernel: FP64 dependency
+        # latency at 12 warps/SM (profiles/README.md).  225 FP64 instructions
+        # per particle (ncu, FAST) against the FP64 FMA rate measured by
+        # tools/micro/dfma.cu (56 lane-ops/clk/SM x 148 SMs x 1.965 GHz)
+        "fp64_pipe": ({"ops_per_particle": 225, "achieved_tops": 225 * n_total / (kernel_ms * 1e-3)
+                       / 1e12, "peak_tops": 56 * 148 * 1.965e9 / 1e12,
+                       "frac": 225 * n_total / (kernel_ms * 1e-3) / (56 * 148 * 1.965e9),
+                       "peak_source": "tools/micro/dfma.cu on this B200 (FP64 FMA, ILP 8)"}
+                      if args.mode == "fast" else None),
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
