@@ -49,6 +49,9 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
 // tensor-map box per tile carries all six SoA arrays in (and one out); the
 // TMA unit zero-fills / clips partial tiles, so there is a single code path.
+#ifndef B2M_ABL_STREAM_ONLY
+#define B2M_ABL_STREAM_ONLY 0
+#endif
 #ifndef B2M_J_UNROLL
 #define B2M_J_UNROLL 1
 #endif
@@ -134,6 +137,9 @@ __global__ void B2M_WARP_BOUNDS
           n_next += flag == 2;
         }
       }
+    } else if (B2M_ABL_STREAM_ONLY) {
+      // ablation: the tile pipeline without the mover arithmetic
+      if (lane < cnt) buf[st][0][lane] += 0.0;
     } else {
       const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
