@@ -121,7 +121,11 @@ __global__ void B2M_WARP_BOUNDS
 #pragma unroll 1
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        const unsigned bad = strict_tile_thread_p1<WT>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc);
+        // pc_iterations = 3 (the reference default) gets a fully unrolled body
+        const unsigned bad =
+            sp.rounds == 3
+                ? strict_tile_thread_p1<WT, 3>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc)
+                : strict_tile_thread_p1<WT, 0>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           int flag = 0;

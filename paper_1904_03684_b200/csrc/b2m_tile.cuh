@@ -474,6 +474,8 @@ __device__ __forceinline__ void strict_round(PState& P, const CellCache& cc, con
 // wrap_len (grid.hpp:45-50) bit for bit: the quotient's floor read off the
 // WrapAxis thresholds instead of an IEEE division (same result, see WrapAxis)
 __device__ __forceinline__ double wrap_strict(double v, const WrapAxis& a) {
+  // common case v in [+0, hi0]: floor(RN(v/l)) = 0, w = v, no fix-up applies
+  if (dbits(v) <= dbits(a.hi0)) return v;
   return wrap_exact_bits(v, a, dbits(a.hi0), dbits(a.hi1), dbits(a.lom1) & kAbs);
 }
 
@@ -509,7 +511,7 @@ __device__ __forceinline__ bool strict_finish(PState& P, const FastGrid& w, doub
 // stay in registers while the particle -- and the lane's next particles --
 // remain in the same cell: a bitwise-identical reuse of values the reference
 // would re-read.
-template <int TILE>
+template <int TILE, int ROUNDS = 0>
 __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, const FastGrid& wg,
                                                           const double* __restrict__ E,
                                                           const double* __restrict__ B,
@@ -520,13 +522,15 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, cons
   PState P;
   const double in[6] = {buf[0][p], buf[1][p], buf[2][p], buf[3][p], buf[4][p], buf[5][p]};
   begin(P, in);
-  for (int r = 0; r < sp.rounds; ++r) {
+  const int rounds = ROUNDS > 0 ? ROUNDS : sp.rounds;
+#pragma unroll
+  for (int r = 0; r < rounds; ++r) {
     double wt[8];
     const int cell = strict_locate(P, g, wt);
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
     if (cell != cc.cell) cache_load_strict(cc, g, E, B, cell);
     strict_round(P, cc, wt, sp.beta);
-    if (r + 1 < sp.rounds) strict_predict(P, wg, sp.dto2);
+    if (r + 1 < rounds) strict_predict(P, wg, sp.dto2);
   }
   double out[6];
   if (!strict_finish(P, wg, sp.dt, out)) return 1u;
