@@ -152,6 +152,13 @@ struct b2m_ctx {
   uint32_t* vals[2] = {};
   double* scratch = nullptr;
   uint64_t sort_cap = 0;
+  // counting sort by cell: per-cell counts / offsets and the scan's temp
+  uint32_t* bin_keys = nullptr;
+  uint64_t bin_keys_cap = 0;
+  uint32_t* bin_count = nullptr;
+  uint32_t* bin_offs = nullptr;
+  void* bin_temp = nullptr;
+  size_t bin_temp_bytes = 0;
   void* scan_temp = nullptr;
   size_t scan_temp_bytes = 0;
   // host pipeline (b2m_run_mover_host)
@@ -773,17 +780,8 @@ b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
   const uint64_t n = S.count;
   if (n < 2) return B2M_OK;
   if (n > 0xffffffffull) return fail(B2M_CONFIG_ERROR, "sort: species larger than 2^32");
-  if ((st = ensure_sort_scratch(ctx, n)) != B2M_OK) return st;
   const uint64_t ncell = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
-  int bits = 1;
-  while ((1ull << bits) <= ncell) ++bits;
-  launch_cell_keys(to_fast(ctx->grid), S.a[0], S.a[1], S.a[2], n, ctx->keys[0], ctx->vals[0],
-                   ctx->stream);
-  launch_sort_pairs(ctx->sort_temp, ctx->sort_temp_bytes, ctx->keys[0], ctx->keys[1],
-                    ctx->vals[0], ctx->vals[1], n, bits, ctx->stream);
-  // permute into the ping-pong set and swap (no copy back); fall back to a
-  // scratch array + copy when the second set does not fit in device memory
-  if (!S.alt[0]) {
+  if (!S.alt[0]) {  // the ping-pong set, allocated on first sort
     double* blk = nullptr;
     if (cudaMalloc(reinterpret_cast<void**>(&blk), 6 * S.stride * sizeof(double)) != cudaSuccess) {
       cudaGetLastError();
@@ -793,14 +791,46 @@ b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
     }
   }
   if (S.alt[0]) {
-    launch_gather6(S.a, ctx->vals[1], n, S.alt, ctx->stream);
-    for (int a = 0; a < 6; ++a) std::swap(S.a[a], S.alt[a]);
-  } else {
-    for (int a = 0; a < 6; ++a) {
-      launch_gather(S.a[a], ctx->vals[1], n, ctx->scratch, ctx->stream);
-      B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a], ctx->scratch, n * sizeof(double),
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    // counting sort straight into the ping-pong set, then swap
+    if (n > ctx->bin_keys_cap) {
+      if (ctx->bin_keys) {
+        cudaFree(ctx->bin_keys);
+        ctx->allocations.erase(
+            std::remove(ctx->allocations.begin(), ctx->allocations.end(), ctx->bin_keys),
+            ctx->allocations.end());
+        ctx->bin_keys = nullptr;
+        ctx->bin_keys_cap = 0;
+      }
+      if ((st = dalloc(ctx, &ctx->bin_keys, n, "sort keys")) != B2M_OK) return st;
+      ctx->bin_keys_cap = n;
     }
+    if (!ctx->bin_count) {
+      if ((st = dalloc(ctx, &ctx->bin_count, ncell + 1, "sort bins")) != B2M_OK) return st;
+      if ((st = dalloc(ctx, &ctx->bin_offs, ncell + 1, "sort bins")) != B2M_OK) return st;
+      ctx->bin_temp_bytes = bin_scan_temp_bytes(ncell + 1);
+      char* tmp = nullptr;
+      if ((st = dalloc(ctx, &tmp, ctx->bin_temp_bytes, "sort scan temp")) != B2M_OK) return st;
+      ctx->bin_temp = tmp;
+    }
+    launch_bin_sort(to_fast(ctx->grid), S.a, S.alt, n, ctx->bin_keys, ctx->bin_count,
+                    ctx->bin_offs, ctx->bin_temp, ctx->bin_temp_bytes, ctx->stream);
+    for (int a = 0; a < 6; ++a) std::swap(S.a[a], S.alt[a]);
+    B2M_CUDA(ctx, cudaGetLastError());
+    return B2M_OK;
+  }
+  // no memory for a second set: radix-sort (key, index) and gather array by
+  // array through one scratch array
+  if ((st = ensure_sort_scratch(ctx, n)) != B2M_OK) return st;
+  int bits = 1;
+  while ((1ull << bits) <= ncell) ++bits;
+  launch_cell_keys(to_fast(ctx->grid), S.a[0], S.a[1], S.a[2], n, ctx->keys[0], ctx->vals[0],
+                   ctx->stream);
+  launch_sort_pairs(ctx->sort_temp, ctx->sort_temp_bytes, ctx->keys[0], ctx->keys[1],
+                    ctx->vals[0], ctx->vals[1], n, bits, ctx->stream);
+  for (int a = 0; a < 6; ++a) {
+    launch_gather(S.a[a], ctx->vals[1], n, ctx->scratch, ctx->stream);
+    B2M_CUDA(ctx, cudaMemcpyAsync(S.a[a], ctx->scratch, n * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
   }
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;

@@ -66,9 +66,12 @@ void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 // Cell keys of the current positions (cell-unit locate), for sorting.
 void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,
                       uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st);
-// out[a][i] = in[a][perm[i]] for the six SoA arrays
-void launch_gather6(double* const* in, const uint32_t* perm, uint64_t n, double* const* out,
-                    cudaStream_t st);
+// Counting sort of the six SoA arrays by cell (unstable within a cell) from
+// `in` into `out`; keys: n scratch, count / offs: nx*ny*nz + 1 scratch each.
+size_t bin_scan_temp_bytes(uint64_t n_bins);
+void launch_bin_sort(const FastGrid& g, double* const* in, double* const* out, uint64_t n,
+                     uint32_t* keys, uint32_t* count, uint32_t* offs, void* temp,
+                     size_t temp_bytes, cudaStream_t st);
 // out[i] = in[perm[i]]
 void launch_gather(const double* in, const uint32_t* perm, uint64_t n, double* out,
                    cudaStream_t st);

@@ -7,7 +7,8 @@
 //                         runtime.cpp:46-62) writing migration flags
 //   field_to_cells_kernel node-layout E/B (field_mesh.hpp:13-60) -> per-cell
 //                         trilinear polynomial for the FAST gather
-//   cell_keys / gather6   the optional cell-sort pass (+ CUB radix sort)
+//   bin_count / bin_scatter   the cell sort (a counting sort by cell; the CUB
+//                         radix sort + gather is the low-memory fallback)
 //   scatter_tiles / fill_*   outbox compaction (scan of the mover's per-tile
 //                         counts) and hole filling (merge_incoming,
 //                         runtime.cpp:64-76)
@@ -277,18 +278,60 @@ __global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const doubl
   vals[i] = static_cast<uint32_t>(i);
 }
 
+// ---- counting sort by cell (b2m_sort_species) -----------------------------
+// Cell order is all the mover needs, not a stable order, so the sort is a
+// counting sort: (1) the cell key of every particle and per-cell counts,
+// (2) an exclusive scan of the counts, (3) every particle written straight to
+// its cell's segment of the ping-pong arrays.  Both atomic passes aggregate
+// over the lanes of a warp that share a cell (__match_any_sync), so a
+// cell-ordered species costs a few atomics per warp.  One read of the
+// positions, one read and one write of the six arrays: HBM-bound.
+__device__ __forceinline__ uint32_t cell_key(const FastGrid& g, double x, double y, double z) {
+  const double cx = x * g.rdx, cy = y * g.rdy, cz = z * g.rdz;
+  uint32_t key = static_cast<uint32_t>(static_cast<long long>(g.nx) * g.ny * g.nz);
+  if (cx >= 0.0 && cx <= g.nxd && cy >= 0.0 && cy <= g.nyd && cz >= 0.0 && cz <= g.nzd) {
+    const int ci = min(__double2int_rz(cx), g.nx - 1);
+    const int cj = min(__double2int_rz(cy), g.ny - 1);
+    const int ck = min(__double2int_rz(cz), g.nz - 1);
+    key = static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
+  }
+  return key;
+}
+
+__global__ void bin_count_kernel(const __grid_constant__ FastGrid g, const double* __restrict__ x,
+                                 const double* __restrict__ y, const double* __restrict__ z,
+                                 unsigned long long n, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ count) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned active = __ballot_sync(0xffffffffu, i < n);
+  if (i >= n) return;
+  const uint32_t key = cell_key(g, x[i], y[i], z[i]);
+  keys[i] = key;
+  const unsigned peers = __match_any_sync(active, key);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[key], __popc(peers));
+}
+
 struct Ptr6 {
   const double* in[6];
   double* out[6];
 };
 
-__global__ void gather6_kernel(const __grid_constant__ Ptr6 P, const uint32_t* __restrict__ perm,
-                               unsigned long long n) {
+__global__ void bin_scatter_kernel(const __grid_constant__ Ptr6 P, const uint32_t* __restrict__ keys,
+                                   unsigned long long n, const uint32_t* __restrict__ offs,
+                                   uint32_t* __restrict__ cursor) {
   const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned active = __ballot_sync(0xffffffffu, i < n);
   if (i >= n) return;
-  const uint32_t j = perm[i];
+  const int lane = threadIdx.x & 31;
+  const uint32_t key = keys[i];
+  const unsigned peers = __match_any_sync(active, key);
+  const int leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  const uint32_t slot = offs[key] + base + __popc(peers & ((1u << lane) - 1u));
 #pragma unroll
-  for (int a = 0; a < 6; ++a) P.out[a][i] = __ldg(P.in[a] + j);
+  for (int a = 0; a < 6; ++a) P.out[a][slot] = __ldcs(P.in[a] + i);
 }
 
 __global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __restrict__ perm,
@@ -550,17 +593,34 @@ void launch_fault_reset(FaultWord* fault, cudaStream_t st) {
   note_launch();
 }
 
-void launch_gather6(double* const* in, const uint32_t* perm, uint64_t n, double* const* out,
-                    cudaStream_t st) {
+size_t bin_scan_temp_bytes(uint64_t n_bins) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), n_bins);
+  return bytes;
+}
+
+void launch_bin_sort(const FastGrid& g, double* const* in, double* const* out, uint64_t n,
+                     uint32_t* keys, uint32_t* count, uint32_t* offs, void* temp,
+                     size_t temp_bytes, cudaStream_t st) {
   if (n == 0) return;
+  const uint64_t n_bins = static_cast<uint64_t>(g.nx) * g.ny * g.nz + 1;  // + out-of-domain bin
+  cudaMemsetAsync(count, 0, n_bins * sizeof(uint32_t), st);
+  bin_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, in[0], in[1], in[2], n, keys, count);
+  note_launch();
+  size_t b = temp_bytes;
+  cub::DeviceScan::ExclusiveSum(temp, b, count, offs, n_bins, st);
+  note_launch();
+  cudaMemsetAsync(count, 0, n_bins * sizeof(uint32_t), st);  // reused as the cursors
   Ptr6 P;
   for (int a = 0; a < 6; ++a) {
     P.in[a] = in[a];
     P.out[a] = out[a];
   }
-  gather6_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, perm, n);
+  bin_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, keys, n, offs, count);
   note_launch();
 }
+
 
 void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,
                       uint64_t n, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
