@@ -375,3 +375,19 @@ def test_host_call_context_cache(gpu, mode):
     p2 = random_particles(g2, 700, 72)
     check(gpu_move(p2, E2, B2, g2, 0.1, 1.0, 3, mode), port_move(p2, E2, B2, g2, 0.1, 1.0, 3),
           g2, mode, "other grid")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+@pytest.mark.parametrize("mode", MODES)
+def test_against_the_reference_library_itself(gpu, mode):
+    """Not only the C restatement: the UNMODIFIED reference pic::move_batch
+    (oracle/_ref/libminipic_ref.so, built from the reference sources) on the
+    same inputs -- STRICT bit-identical, FAST within the contract."""
+    grid = (12, 10, 8, 4.8, 3.0, 2.4)
+    E, B = random_field(grid, 12, 0.4)
+    for qom, pc in ((-25.0, 3), (1.0, 5)):
+        p0 = random_particles(grid, 30000, 1200 + pc)
+        want = [a.copy() for a in p0]
+        oracle.ref_move_batch(want, E, B, grid, 0.1, qom, pc)
+        check(gpu_move(p0, E, B, grid, 0.1, qom, pc, mode), want, grid, mode,
+              f"vs reference qom={qom} pc={pc}")
