@@ -80,3 +80,13 @@ def test_device_field_stub_then_move(gpu):
             for a, w in zip(out, want):
                 np.testing.assert_allclose(a, w, rtol=1e-12, atol=1e-12)
         st.close()
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_stub_against_the_reference_library_itself(gpu):
+    g = Grid.make(10, 7, 6, 1.0, 2.0, 3.0)
+    E, B = random_field(g.as_tuple(), 13)
+    out = field_phase_stub(FieldMesh(g, E, B), g, 4)
+    Ew, Bw = oracle.ref_field_phase_stub(E, B, g.as_tuple(), 4)
+    assert_bitwise(out.E.ravel(), Ew, "E")
+    assert_bitwise(out.B.ravel(), Bw, "B")

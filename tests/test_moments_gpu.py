@@ -139,3 +139,13 @@ def test_unsorted_large_batch(gpu):
     m = gpu_deposit(p, grid, 0.01, pressure=False)
     assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.01, False),
                          what="unsorted")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_against_the_reference_library_itself(gpu):
+    """The UNMODIFIED reference deposit_moments on the same particles."""
+    grid = (6, 5, 7, 3.0, 2.5, 3.5)
+    p = random_particles(grid, 20000, 33, vscale=1.0)
+    m = gpu_deposit(p, grid, -0.0125, pressure=True)
+    assert_moments_close(m.arrays, oracle.ref_deposit_moments(p, grid, -0.0125, True),
+                         what="vs reference")
