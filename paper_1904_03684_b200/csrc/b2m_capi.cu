@@ -135,6 +135,8 @@ struct b2m_ctx {
   uint64_t n_nodes = 0;
   double* dE = nullptr;
   double* dE_alt = nullptr;  // field-stub ping-pong (allocated on first use)
+  double* strict_nodes = nullptr;  // STRICT per-cell corner node table
+  uint64_t strict_gen = 0;
   double* dB = nullptr;
   bool field_ready = false;
   uint64_t field_gen = 0;  // bumped by every field upload
@@ -241,6 +243,17 @@ SpeciesLaunch make_launch(b2m_ctx* ctx, int s, const b2m_mover_params& mp, uint6
   L.col0 = offset;
   L.stride = S.stride;
   return L;
+}
+
+// STRICT: the per-cell corner node table of the current field (built on first
+// use after every field change).
+double* strict_nodes(b2m_ctx* ctx) {
+  if (ctx->strict_gen != ctx->field_gen) {  // allocated at context creation
+    launch_strict_nodes(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
+                        ctx->strict_nodes, ctx->stream);
+    ctx->strict_gen = ctx->field_gen;
+  }
+  return ctx->strict_nodes;
 }
 
 // FAST: (re)build, in one launch, the beta-scaled cell tables of the given
@@ -401,6 +414,8 @@ b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const ui
   b2m_status st;
   if ((st = dalloc(ctx, &ctx->dE, 3 * nodes, "field E")) != B2M_OK) return bail(st);
   if ((st = dalloc(ctx, &ctx->dB, 3 * nodes, "field B")) != B2M_OK) return bail(st);
+  if ((st = dalloc(ctx, &ctx->strict_nodes, 48 * ncell, "strict node table")) != B2M_OK)
+    return bail(st);
   if ((st = dalloc(ctx, &ctx->fault, 1, "fault word")) != B2M_OK) return bail(st);
   if (cudaMallocHost(&ctx->fault_h, sizeof(FaultWord)) != cudaSuccess) {
     cudaGetLastError();
@@ -665,7 +680,7 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   ensure_tables(ctx, &s, mp, 1);
   const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
   if (ctx->mode == B2M_MODE_STRICT) {
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream)) {
@@ -698,7 +713,7 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
   for (int s = 0; s < ns; ++s)
     L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
   if (ctx->mode == B2M_MODE_STRICT) {
-    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, L.data(), ns, ctx->fault,
+    if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), L.data(), ns, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault,
@@ -755,7 +770,7 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev[2 * c], 0));
       const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
       if (ctx->mode == B2M_MODE_STRICT) {
-        if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB, &L, 1, ctx->fault,
+        if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
                                       ctx->stream))
           return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream))
@@ -1204,7 +1219,7 @@ static b2m_status move_migrate_species(b2m_ctx* ctx, const int* species,
   const int nl = static_cast<int>(L.size());
   const bool ok =
       ctx->mode == B2M_MODE_STRICT
-          ? launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), ctx->dE, ctx->dB,
+          ? launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx),
                                      L.data(), nl, ctx->fault, ctx->stream, &ctx->sl, fl.data(),
                                      tc.data())
           : launch_move_fast(to_fast(ctx->grid), L.data(), nl, ctx->fault, ctx->stream, &ctx->sl,

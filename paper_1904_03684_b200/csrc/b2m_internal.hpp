@@ -37,11 +37,14 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr,
                       unsigned long long* const* tcnt = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
-bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
-                              const double* B, const SpeciesLaunch* sp, int n_spans,
-                              FaultWord* fault, cudaStream_t st, const SlabLaunch* sl = nullptr,
+bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st, const SlabLaunch* sl = nullptr,
                               uint8_t* const* flags = nullptr,
                               unsigned long long* const* tcnt = nullptr);
+// STRICT cell table: per cell the 8 corner nodes' E, B (48 doubles).
+void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* B, double* out,
+                         cudaStream_t st);
 // Node AoS E/B -> per-cell polynomial coefficients of (scale[m]*E,
 // scale[m]*B) into tables[m] (48 doubles per cell), one field read per
 // kMaxTables tables.

@@ -125,8 +125,8 @@ __global__ void B2M_WARP_BOUNDS
         // pc_iterations = 3 (the reference default) gets a fully unrolled body
         const unsigned bad =
             sp.rounds == 3
-                ? strict_tile_thread_p1<WT, 3>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc)
-                : strict_tile_thread_p1<WT, 0>(F.dg, F.fg, F.E, F.B, sp, buf[st], p, cnt, cc);
+                ? strict_tile_thread_p1<WT, 3>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc)
+                : strict_tile_thread_p1<WT, 0>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           int flag = 0;
@@ -211,6 +211,27 @@ __global__ void B2M_WARP_BOUNDS
     }
   }
   if (lane == 0) tma_wait_all();
+}
+
+// STRICT: per cell, the 8 corner nodes' (Ex, Ey, Ez, Bx, By, Bz) in corner
+// order c = di + 2dj + 4dk (kernels.cpp:10-22) -- 48 doubles the mover's cell
+// cache loads with twelve 256-bit loads.  Thread = (cell, corner).
+__global__ void strict_nodes_kernel(int nx, int ny, int nz, const double* __restrict__ E,
+                                    const double* __restrict__ B, double* __restrict__ out) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long ncell = static_cast<long long>(nx) * ny * nz;
+  if (t >= 8 * ncell) return;
+  const long long cell = t / 8;
+  const int c = static_cast<int>(t % 8);
+  const int i = static_cast<int>(cell % nx);
+  const int j = static_cast<int>((cell / nx) % ny);
+  const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
+  const long long n = 3 * ((i + (c & 1)) + static_cast<long long>(nx + 1) *
+                                               ((j + ((c >> 1) & 1)) +
+                                                static_cast<long long>(ny + 1) * (k + (c >> 2))));
+  double* o = out + 6 * t;
+  o[0] = __ldg(E + n); o[1] = __ldg(E + n + 1); o[2] = __ldg(E + n + 2);
+  o[3] = __ldg(B + n); o[4] = __ldg(B + n + 1); o[5] = __ldg(B + n + 2);
 }
 
 // Per-cell trilinear polynomials of (beta*E, beta*B) for up to kMaxTables
@@ -561,16 +582,22 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, F
   return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags, tcnt);
 }
 
-bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* E,
-                              const double* B, const SpeciesLaunch* sp, int n_spans,
-                              FaultWord* fault, cudaStream_t st, const SlabLaunch* sl,
-                              uint8_t* const* flags, unsigned long long* const* tcnt) {
+bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
+                              const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
+                              cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
+                              unsigned long long* const* tcnt) {
   TileField F{};
   F.dg = g;
   F.fg = fg;  // wrap thresholds (WrapAxis)
-  F.E = E;
-  F.B = B;
+  F.nodes = nodes;
   return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+}
+
+void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* B, double* out,
+                         cudaStream_t st) {
+  const long long ncell = static_cast<long long>(nx) * ny * nz;
+  strict_nodes_kernel<<<grid_for(8 * ncell, 256), 256, 0, st>>>(nx, ny, nz, E, B, out);
+  note_launch();
 }
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,

@@ -126,8 +126,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 struct TileField {
   FastGrid fg;
   DevGrid dg;
-  const double* E;       // STRICT
-  const double* B;
+  const double* nodes;   // STRICT: per-cell corner node values (strict_nodes_kernel)
 };
 
 // FAST launch: per span a 2-D tensor map over the species' [6][stride]
@@ -392,20 +391,21 @@ struct CellCache {
   int cell;
 };
 
-__device__ __forceinline__ void cache_load_strict(CellCache& cc, const DevGrid& g,
-                                                  const double* __restrict__ E,
-                                                  const double* __restrict__ B, int cell) {
-  const int i = cell % g.nx;
-  const int j = (cell / g.nx) % g.ny;
-  const int k = cell / (g.nx * g.ny);
-  const long long sx1 = g.nx + 1, sy1 = g.ny + 1;
+// The 8 corner nodes' E and B of a cell: 48 doubles laid out by
+// strict_nodes_kernel in exactly the cache's order (corner c: Ex Ey Ez Bx By
+// Bz), so the reload is twelve 256-bit loads -- the same values the
+// reference reads from the node mesh, bit for bit.
+__device__ __forceinline__ void cache_load_strict(CellCache& cc, const double* __restrict__ nodes,
+                                                  int cell) {
+  const double* c = nodes + static_cast<long long>(cell) * 48;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int di = c & 1, dj = (c >> 1) & 1, dk = (c >> 2) & 1;
-    const long long n = 3 * ((i + di) + sx1 * ((j + dj) + sy1 * (k + dk)));
-    cc.c[3 * c + 0] = make_double2(__ldg(E + n + 0), __ldg(E + n + 1));
-    cc.c[3 * c + 1] = make_double2(__ldg(E + n + 2), __ldg(B + n + 0));
-    cc.c[3 * c + 2] = make_double2(__ldg(B + n + 1), __ldg(B + n + 2));
+  for (int q = 0; q < 12; ++q) {
+    double a, b, d, e;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(a), "=d"(b), "=d"(d), "=d"(e)
+        : "l"(c + 4 * q));
+    cc.c[2 * q] = make_double2(a, b);
+    cc.c[2 * q + 1] = make_double2(d, e);
   }
   cc.cell = cell;
 }
@@ -513,8 +513,7 @@ __device__ __forceinline__ bool strict_finish(PState& P, const FastGrid& w, doub
 // would re-read.
 template <int TILE, int ROUNDS = 0>
 __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, const FastGrid& wg,
-                                                          const double* __restrict__ E,
-                                                          const double* __restrict__ B,
+                                                          const double* __restrict__ nodes,
                                                           const SpeciesLaunch& sp,
                                                           double (*buf)[TILE], int p, int cnt,
                                                           CellCache& cc) {
@@ -528,7 +527,7 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, cons
     double wt[8];
     const int cell = strict_locate(P, g, wt);
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
-    if (cell != cc.cell) cache_load_strict(cc, g, E, B, cell);
+    if (cell != cc.cell) cache_load_strict(cc, nodes, cell);
     strict_round(P, cc, wt, sp.beta);
     if (r + 1 < rounds) strict_predict(P, wg, sp.dto2);
   }
