@@ -22,6 +22,8 @@
 // stays in one cell for a whole run (~216 particles per species in GEM), so
 // it adds 8 corners x NM moments to the mesh once per run, and the 32 lanes
 // of a warp work in 32 different cells -- no colliding atomics.
+#include <cstdlib>
+
 #include "b2m_internal.hpp"
 
 namespace b2m {
@@ -146,11 +148,275 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
   if (ai >= 0) flush();
 }
 
+// Warp-group variant: a warp streams a contiguous chunk of the species 32
+// particles at a time (coalesced loads, one particle per lane, the next 32
+// prefetched into registers).
+//  * The warp carries one cell: each lane sums, in registers, the terms of
+//    its own particles in that cell.  Cell-sorted particles stay in one cell
+//    for ~216 particles per species, so the common iteration is FP64
+//    arithmetic only -- no shared memory, no atomics.
+//  * When the sorted order moves on (the last lanes form a new cell) the
+//    carry is reduced across the warp with a shuffle transpose (lane j ends
+//    with column j), added to the mesh with one atomic per lane, and the new
+//    cell becomes the carry.
+//  * Other particles (drifted out of the sorted order) are grouped by cell
+//    (__match_any_sync): one alone in its cell adds its terms to the mesh
+//    directly; a group writes its terms to shared-memory rows and lane j sums
+//    column j over them before one atomic per column.
+constexpr int kGroupThreads = 128;
+
+template <int SET>
+constexpr int group_row() { return (SET == 0 ? 32 : 48) + 1; }  // +1: conflict-free rows
+
+template <int SET>
+constexpr size_t group_smem() {
+  return sizeof(double) * (kGroupThreads / 32) * 32 * group_row<SET>();
+}
+
+// v[0..H2-1] over the 32 lanes -> lane j holds sum over lanes of v[j mod H2]
+// (H2 = 32: lane j gets column j; H2 = 16: lanes j and j+16 get column j%16)
+template <int H2, bool EXACT, int N>
+__device__ __forceinline__ double xreduce(double (&v)[N], int o, int lane) {
+#pragma unroll
+  for (int h = H2 / 2; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[o + i] : v[o + i + h];
+      const double keep = up ? v[o + i + h] : v[o + i];
+      const double r = __shfl_xor_sync(0xffffffffu, send, h);
+      v[o + i] = EXACT ? __dadd_rn(keep, r) : keep + r;
+    }
+  }
+  double x = v[o];
+  if (H2 == 16) {
+    const double r = __shfl_xor_sync(0xffffffffu, x, 16);
+    x = EXACT ? __dadd_rn(x, r) : x + r;
+  }
+  return x;
+}
+
+template <int SET, bool EXACT>
+__global__ void __launch_bounds__(kGroupThreads, 3)
+    deposit_group_kernel(const __grid_constant__ DevGrid g, const __grid_constant__ SpeciesLaunch sp,
+                         double qv, const __grid_constant__ MomentPtrs M, unsigned long long span,
+                         FaultWord* fault) {
+  constexpr int NM = SET == 0 ? 4 : 6;
+  constexpr int NV = NM * 8;
+  constexpr int CPL = (NV + 31) / 32;  // columns per lane in a reduction
+  constexpr int LD = group_row<SET>();
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(128) double sbuf[];
+  const int lane = threadIdx.x & 31;
+  double* const wbuf = sbuf + (threadIdx.x >> 5) * 32 * LD;
+  double* const row = wbuf + lane * LD;
+  const unsigned long long wid =
+      (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long lb = wid * span;
+  if (lb >= sp.n) return;
+  const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
+  const double rdx = 1.0 / g.dx, rdy = 1.0 / g.dy, rdz = 1.0 / g.dz;
+
+  auto mul_ = [](double a, double b) { return EXACT ? __dmul_rn(a, b) : a * b; };
+  auto add_ = [](double a, double b) { return EXACT ? __dadd_rn(a, b) : a + b; };
+  auto sub_ = [](double a, double b) { return EXACT ? __dsub_rn(a, b) : a - b; };
+
+  // add t to the mesh at column col (moment col/8, corner col%8) of cell (ci, cj, ck)
+  auto red = [&](int col, int ci, int cj, int ck, double t) {
+    const int mom = col >> 3, c = col & 7;
+    const int ii = (c & 1) ? (ci + 1 == g.nx ? 0 : ci + 1) : ci;
+    const int jj = (c & 2) ? (cj + 1 == g.ny ? 0 : cj + 1) : cj;
+    const int kk = (c & 4) ? (ck + 1 == g.nz ? 0 : ck + 1) : ck;
+    atomicAdd(M.m[SET * 4 + mom] + ii +
+                  static_cast<long long>(g.nx) * (jj + static_cast<long long>(g.ny) * kk),
+              t);
+  };
+
+  double acc[NV];  // this lane's sums for the carried cell
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  long long ckey = -1;  // carried cell (warp-uniform); -1: none
+  int cci = 0, ccj = 0, cck = 0;
+  // reduce the carry across the warp into the mesh and clear it
+  auto flush_carry = [&]() {
+    const double c0 = xreduce<32, EXACT>(acc, 0, lane);
+    red(lane, cci, ccj, cck, c0);
+    if (NV > 32) {
+      const double c1 = xreduce<16, EXACT>(acc, 32, lane);
+      if (lane < 16) red(32 + lane, cci, ccj, cck, c1);
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  };
+
+  auto load = [&](unsigned long long p, double (&q)[6]) {
+    if (p < le) {
+      q[0] = sp.x[p]; q[1] = sp.y[p]; q[2] = sp.z[p];
+      q[3] = sp.u[p]; q[4] = sp.v[p]; q[5] = sp.w[p];
+    }
+  };
+  double nxt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  load(lb + lane, nxt);
+
+  for (unsigned long long base = lb; base < le; base += 32) {
+    const unsigned long long p = base + lane;
+    bool ok = p < le;
+    const double px = nxt[0], py = nxt[1], pz = nxt[2], ux = nxt[3], uy = nxt[4], uz = nxt[5];
+    load(p + 32, nxt);
+    // grid.hpp:65-67: the reference throws DomainError
+    if (ok && !(px >= 0.0 && px < g.lx && py >= 0.0 && py < g.ly && pz >= 0.0 && pz < g.lz)) {
+      atomicMin(&fault->domain, fault_key(sp.species, sp.base + p));
+      ok = false;
+    }
+    // grid.hpp:69-80, bit for bit
+    const double sx = EXACT ? __ddiv_rn(px, g.dx) : px * rdx;
+    const double sy = EXACT ? __ddiv_rn(py, g.dy) : py * rdy;
+    const double sz = EXACT ? __ddiv_rn(pz, g.dz) : pz * rdz;
+    int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
+    if (i >= g.nx) i = g.nx - 1;
+    if (j >= g.ny) j = g.ny - 1;
+    if (k >= g.nz) k = g.nz - 1;
+    const double fx = fmin(sub_(sx, static_cast<double>(i)), 1.0);
+    const double fy = fmin(sub_(sy, static_cast<double>(j)), 1.0);
+    const double fz = fmin(sub_(sz, static_cast<double>(k)), 1.0);
+    const double wx[2] = {sub_(1.0, fx), fx};
+    const double wy[2] = {sub_(1.0, fy), fy};
+    const double wz[2] = {sub_(1.0, fz), fz};
+    // the NV terms of this particle, column by column (kernels.cpp:168-181)
+    auto terms = [&](auto&& f) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        // kernels.cpp:168: qv * wx * wy * wz, left to right
+        const double wq = mul_(mul_(mul_(qv, wx[c & 1]), wy[(c >> 1) & 1]), wz[(c >> 2) & 1]);
+        if (SET == 0) {
+          f(c, wq);
+          f(8 + c, mul_(wq, ux));
+          f(16 + c, mul_(wq, uy));
+          f(24 + c, mul_(wq, uz));
+        } else {
+          const double wu = mul_(wq, ux), wv = mul_(wq, uy), ww = mul_(wq, uz);
+          f(c, mul_(wu, ux));
+          f(8 + c, mul_(wu, uy));
+          f(16 + c, mul_(wu, uz));
+          f(24 + c, mul_(wv, uy));
+          f(32 + c, mul_(wv, uz));
+          f(40 + c, mul_(ww, uz));
+        }
+      }
+    };
+    const long long key =
+        ok ? i + static_cast<long long>(g.nx) * (j + static_cast<long long>(g.ny) * k) : -1;
+    const bool in_carry = ok && key == ckey;
+    if (in_carry) terms([&](int v, double t) { acc[v] = add_(acc[v], t); });
+    unsigned rest = __ballot_sync(FULL, ok && !in_carry);
+    if (rest == 0) continue;  // the common case after a sort
+
+    const unsigned grp = __match_any_sync(FULL, key);
+    // the sorted order moved on (or drift): the largest other group takes
+    // over the carry when it outnumbers the carried cell here; ties go to the
+    // group of the last lane (the sorted order continues there)
+    const unsigned score = (ok && !in_carry)
+                               ? (static_cast<unsigned>(__popc(grp)) << 6) |
+                                     (((grp >> 31) & 1u) << 5) | static_cast<unsigned>(lane)
+                               : 0u;
+    const unsigned best = __reduce_max_sync(FULL, score);
+    const int ncarried = __popc(__ballot_sync(FULL, in_carry));
+    if (static_cast<int>(best >> 6) >= (ncarried > 1 ? ncarried : 2) ||
+        (ncarried == 0 && (best >> 6) >= 1 && ckey < 0)) {
+      const int bl = best & 31;
+      if (ckey >= 0) flush_carry();
+      ckey = __shfl_sync(FULL, key, bl);
+      cci = __shfl_sync(FULL, i, bl);
+      ccj = __shfl_sync(FULL, j, bl);
+      cck = __shfl_sync(FULL, k, bl);
+      const unsigned took = __shfl_sync(FULL, grp, bl);
+      if ((took >> lane) & 1) terms([&](int v, double t) { acc[v] = t; });
+      rest &= ~took;
+      if (rest == 0) continue;
+    }
+    const bool mine = (rest >> lane) & 1;
+    // alone in its cell: straight to the mesh
+    const bool single = mine && __popc(grp) == 1;
+    if (single) terms([&](int v, double t) { red(v, i, j, k, t); });
+    unsigned multi = rest & ~__ballot_sync(FULL, single);
+    if (multi == 0) continue;
+    if ((multi >> lane) & 1) terms([&](int v, double t) { row[v] = t; });
+    __syncwarp();
+    while (multi) {
+      const int leader = __ffs(multi) - 1;
+      const unsigned mem = __shfl_sync(FULL, grp, leader);
+      multi &= ~mem;
+      const int gi = __shfl_sync(FULL, i, leader), gj = __shfl_sync(FULL, j, leader),
+                gk = __shfl_sync(FULL, k, leader);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int col = lane + 32 * q;
+        if (col < NV) {
+          double a0 = 0.0, a1 = 0.0;  // two chains over the member rows
+          unsigned b = mem;
+          while (b) {
+            a0 = add_(a0, wbuf[(__ffs(b) - 1) * LD + col]);
+            b &= b - 1;
+            if (b) {
+              a1 = add_(a1, wbuf[(__ffs(b) - 1) * LD + col]);
+              b &= b - 1;
+            }
+          }
+          red(col, gi, gj, gk, add_(a0, a1));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (ckey >= 0) flush_carry();
+}
+
+template <int SET, bool EXACT>
+void launch_group(const DevGrid& g, const SpeciesLaunch& sp, double qv, const MomentPtrs& M,
+                  FaultWord* fault, cudaStream_t st) {
+  constexpr size_t smem = group_smem<SET>();
+  static const int per_sm = [] {
+    cudaFuncSetAttribute(deposit_group_kernel<SET, EXACT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_group_kernel<SET, EXACT>,
+                                                  kGroupThreads, smem);
+    return b > 0 ? b : 1;
+  }();
+  const unsigned long long warps =
+      static_cast<unsigned long long>(device_sms()) * per_sm * (kGroupThreads / 32);
+  unsigned long long span = (sp.n + warps - 1) / warps;
+  span = (span + 31) / 32 * 32;
+  const unsigned long long used = (sp.n + span - 1) / span;
+  const int blocks = static_cast<int>((used + kGroupThreads / 32 - 1) / (kGroupThreads / 32));
+  deposit_group_kernel<SET, EXACT><<<blocks, kGroupThreads, smem, st>>>(g, sp, qv, M, span, fault);
+  note_launch();
+}
+
+bool use_group_deposit() {
+  static const bool v = [] {
+    const char* e = getenv("B2M_DEPOSIT");
+    return !(e && e[0] == 'l');  // B2M_DEPOSIT=lane: the per-lane-range kernel
+  }();
+  return v;
+}
+
 }  // namespace
 
 void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double* const* mesh,
                     bool pressure, bool exact, FaultWord* fault, cudaStream_t st) {
   if (sp.n == 0) return;
+  MomentPtrs M{};
+  for (int m = 0; m < (pressure ? 10 : 4); ++m) M.m[m] = mesh[m];
+  if (use_group_deposit()) {
+    if (exact) launch_group<0, true>(g, sp, qv, M, fault, st);
+    else launch_group<0, false>(g, sp, qv, M, fault, st);
+    if (pressure) {
+      if (exact) launch_group<1, true>(g, sp, qv, M, fault, st);
+      else launch_group<1, false>(g, sp, qv, M, fault, st);
+    }
+    return;
+  }
   const int sms = device_sms();
   // enough lanes to fill the GPU, each a contiguous range of whole groups
   const unsigned long long lanes = static_cast<unsigned long long>(sms) * 12 * 32;
@@ -159,8 +425,6 @@ void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double
   if (span < 64) span = 64;
   const unsigned long long used = (sp.n + span - 1) / span;
   const int blocks = static_cast<int>((used + kDepositThreads - 1) / kDepositThreads);
-  MomentPtrs M{};
-  for (int m = 0; m < (pressure ? 10 : 4); ++m) M.m[m] = mesh[m];
   if (exact)
     deposit_kernel<0, true><<<blocks, kDepositThreads, 0, st>>>(g, sp, qv, M, span, fault);
   else

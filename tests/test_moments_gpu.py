@@ -149,3 +149,26 @@ def test_against_the_reference_library_itself(gpu):
     m = gpu_deposit(p, grid, -0.0125, pressure=True)
     assert_moments_close(m.arrays, oracle.ref_deposit_moments(p, grid, -0.0125, True),
                          what="vs reference")
+
+
+@pytest.mark.parametrize("order", ["random", "sorted", "sorted_jittered"])
+def test_cell_groups_runs_and_strays(gpu, order):
+    """The warp-group deposit's paths: many particles per cell within 32
+    (shared-memory group sums), runs of one cell across groups (the carried
+    cell), strays alone in their cell (direct atomics), a ragged tail."""
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    n = 100_003
+    p = random_particles(grid, n, 41, vscale=1.0)
+    cell = (np.floor(p[0]).astype(np.int64) + 4 * (np.floor(p[1]).astype(np.int64)
+            + 4 * np.floor(p[2]).astype(np.int64)))
+    if order != "random":
+        perm = np.argsort(cell, kind="stable")
+        if order == "sorted_jittered":
+            rng = np.random.default_rng(5)
+            sw = rng.integers(0, n, size=(n // 10, 2))
+            for a, b in sw:
+                perm[a], perm[b] = perm[b], perm[a]
+        p = [np.ascontiguousarray(a[perm]) for a in p]
+    m = gpu_deposit(p, grid, 0.003, pressure=True)
+    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.003, True),
+                         what=order)
