@@ -14,7 +14,8 @@ ncu --set full --import-source on --clock-control none -k regex:warp_tile_kernel
 B2M_MODE=strict ncu --set full --import-source on --clock-control none -k regex:warp_tile_kernel \
     --launch-skip 2 --launch-count 1 -f -o gpurun_out/prof_strict python tools/one_launch.py 3 \
     > gpurun_out/ncu_strict.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:deposit_kernel \
-    --launch-skip 4 --launch-count 1 -f -o gpurun_out/prof_deposit python tools/deposit_time.py \
+# species 0 right after a cell sort (FAST context)
+ncu --set full --import-source on --clock-control none -k regex:deposit_ \
+    --launch-skip 0 --launch-count 1 -f -o gpurun_out/prof_deposit python tools/deposit_drift.py \
     > gpurun_out/ncu_deposit.log 2>&1
 echo profiles captured
