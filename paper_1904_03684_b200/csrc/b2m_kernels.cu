@@ -388,39 +388,52 @@ __global__ void __launch_bounds__(kTileParticles)
                          double* __restrict__ out_prev, double* __restrict__ out_next,
                          unsigned long long cap_out, unsigned long long* __restrict__ holes) {
   __shared__ int warp_tot[2][kTileParticles / 32];
+  __shared__ unsigned active[kTileParticles];  // tiles of this group with leavers
+  __shared__ int n_active;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  // grid-stride over tiles: a tile without leavers costs one load
-  for (unsigned long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    if (cnt[t] == 0) continue;  // uniform across the block
-    const unsigned long long i = t * kTileParticles + threadIdx.x;
-    const int flag = i < sp.n ? flags[i] : 0;
-    const unsigned bp = __ballot_sync(~0u, flag == 1);
-    const unsigned bn = __ballot_sync(~0u, flag == 2);
-    __syncthreads();  // warp_tot of the previous tile has been read
-    if (lane == 0) {
-      warp_tot[0][wid] = __popc(bp);
-      warp_tot[1][wid] = __popc(bn);
-    }
+  // grid-stride over groups of kTileParticles tiles: one coalesced load of
+  // the group's counts, then only the tiles with leavers
+  for (unsigned long long g0 = static_cast<unsigned long long>(blockIdx.x) * kTileParticles;
+       g0 < n_tiles; g0 += static_cast<unsigned long long>(gridDim.x) * kTileParticles) {
+    __syncthreads();  // the previous group's list has been consumed
+    if (threadIdx.x == 0) n_active = 0;
     __syncthreads();
-    if (flag == 0) continue;
-    int rp = __popc(bp & lt), rn = __popc(bn & lt);
-    for (int w = 0; w < wid; ++w) {
-      rp += warp_tot[0][w];
-      rn += warp_tot[1][w];
-    }
-    const unsigned long long o = off[t];
-    const unsigned long long op = o & 0xffffffffull, on = o >> 32;
-    const unsigned long long hp = op + rp, hn = on + rn;
-    holes[op + on + rp + rn] = i;  // all leavers in index order
-    double* dst = nullptr;
-    if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
-    if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
-    if (dst) {
-      double p[6];
-      load6(sp, i, p);
+    const unsigned long long tt = g0 + threadIdx.x;
+    if (tt < n_tiles && cnt[tt] != 0) active[atomicAdd(&n_active, 1)] = threadIdx.x;
+    __syncthreads();
+    const int na = n_active;
+    for (int a = 0; a < na; ++a) {
+      const unsigned long long t = g0 + active[a];
+      const unsigned long long i = t * kTileParticles + threadIdx.x;
+      const int flag = i < sp.n ? flags[i] : 0;
+      const unsigned bp = __ballot_sync(~0u, flag == 1);
+      const unsigned bn = __ballot_sync(~0u, flag == 2);
+      __syncthreads();  // warp_tot of the previous tile has been read
+      if (lane == 0) {
+        warp_tot[0][wid] = __popc(bp);
+        warp_tot[1][wid] = __popc(bn);
+      }
+      __syncthreads();
+      if (flag == 0) continue;
+      int rp = __popc(bp & lt), rn = __popc(bn & lt);
+      for (int w = 0; w < wid; ++w) {
+        rp += warp_tot[0][w];
+        rn += warp_tot[1][w];
+      }
+      const unsigned long long o = off[t];
+      const unsigned long long op = o & 0xffffffffull, on = o >> 32;
+      const unsigned long long hp = op + rp, hn = on + rn;
+      holes[op + on + rp + rn] = i;  // all leavers in index order
+      double* dst = nullptr;
+      if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
+      if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
+      if (dst) {
+        double p[6];
+        load6(sp, i, p);
 #pragma unroll
-      for (int a = 0; a < 6; ++a) dst[a] = p[a];
+        for (int a6 = 0; a6 < 6; ++a6) dst[a6] = p[a6];
+      }
     }
   }
 }
@@ -707,8 +720,10 @@ void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
                           unsigned long long* holes, cudaStream_t st) {
   const uint64_t nt = migrate_tiles(sp.n);
   if (nt == 0) return;
+  const uint64_t groups = (nt + kTileParticles - 1) / kTileParticles;
   const uint64_t cap = static_cast<uint64_t>(device_sms()) * 16;
-  scatter_tiles_kernel<<<static_cast<unsigned>(nt < cap ? nt : cap), kTileParticles, 0, st>>>(
+  scatter_tiles_kernel<<<static_cast<unsigned>(groups < cap ? groups : cap), kTileParticles, 0,
+                         st>>>(
       sp, flags, cnt, off, nt, out_prev, out_next, cap_out, holes);
   note_launch();
 }
