@@ -73,6 +73,7 @@ DevGrid to_dev(const b2m_grid& g) {
   d.nx = g.nx; d.ny = g.ny; d.nz = g.nz;
   d.lx = g.lx; d.ly = g.ly; d.lz = g.lz;
   d.dx = g.dx; d.dy = g.dy; d.dz = g.dz;
+  d.rdx = 1.0 / g.dx; d.rdy = 1.0 / g.dy; d.rdz = 1.0 / g.dz;
   return d;
 }
 

@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
                    double qv, const __grid_constant__ MomentPtrs M, unsigned long long span,
                    FaultWord* fault) {
   constexpr int NM = SET == 0 ? 4 : 6;
-  const double rdx = 1.0 / g.dx, rdy = 1.0 / g.dy, rdz = 1.0 / g.dz;
   const unsigned long long t =
       static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const unsigned long long lb = t * span;  // this lane's range [lb, le)
@@ -91,9 +90,9 @@ __global__ void __launch_bounds__(kDepositThreads, 2)
       return;
     }
     // grid.hpp:69-80, bit for bit
-    const double sx = EXACT ? __ddiv_rn(px, g.dx) : px * rdx;
-    const double sy = EXACT ? __ddiv_rn(py, g.dy) : py * rdy;
-    const double sz = EXACT ? __ddiv_rn(pz, g.dz) : pz * rdz;
+    const double sx = EXACT ? div_axis(px, g.dx, g.rdx) : px * g.rdx;
+    const double sy = EXACT ? div_axis(py, g.dy, g.rdy) : py * g.rdy;
+    const double sz = EXACT ? div_axis(pz, g.dz, g.rdz) : pz * g.rdz;
     int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
     if (i >= g.nx) i = g.nx - 1;
     if (j >= g.ny) j = g.ny - 1;
@@ -215,7 +214,6 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
   const unsigned long long lb = wid * span;
   if (lb >= sp.n) return;
   const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
-  const double rdx = 1.0 / g.dx, rdy = 1.0 / g.dy, rdz = 1.0 / g.dz;
 
   auto mul_ = [](double a, double b) { return EXACT ? __dmul_rn(a, b) : a * b; };
   auto add_ = [](double a, double b) { return EXACT ? __dadd_rn(a, b) : a + b; };
@@ -269,9 +267,9 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
       ok = false;
     }
     // grid.hpp:69-80, bit for bit
-    const double sx = EXACT ? __ddiv_rn(px, g.dx) : px * rdx;
-    const double sy = EXACT ? __ddiv_rn(py, g.dy) : py * rdy;
-    const double sz = EXACT ? __ddiv_rn(pz, g.dz) : pz * rdz;
+    const double sx = EXACT ? div_axis(px, g.dx, g.rdx) : px * g.rdx;
+    const double sy = EXACT ? div_axis(py, g.dy, g.rdy) : py * g.rdy;
+    const double sz = EXACT ? div_axis(pz, g.dz, g.rdz) : pz * g.rdz;
     int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
     if (i >= g.nx) i = g.nx - 1;
     if (j >= g.ny) j = g.ny - 1;

@@ -418,33 +418,13 @@ __device__ __forceinline__ void begin(PState& P, const double* p) {
   P.ok = true;
 }
 
-#ifndef B2M_STRICT_DIV
-#define B2M_STRICT_DIV 1
-#endif
-// RN(x / d) for a position x in [0, l) (grid_cell_of, grid.hpp:69-71).  These
-// are the last three steps of CUDA's own correctly rounded division
-// (__ddiv_rn's fast path: q = x*y, r = x - q*d exact by FMA, q + r*y), with
-// y = RN(1/d) computed once on the host instead of refined per call by
-// Newton steps from MUFU.RCP64H; subnormal x take the IEEE division.
-// tools/micro/div_check.cu compares it with __ddiv_rn: 0 differences over
-// 2.7e11 random x (4016 spacings) and every x within 32 ulps of a cell face
-// (tests/test_division_gpu.py runs it).  B2M_STRICT_DIV=0 builds the IEEE
-// division instead.
-__device__ __forceinline__ double div_axis(double x, double d, double rd) {
-  if (B2M_STRICT_DIV == 0 || (x != 0.0 && x < 0x1p-900)) return __ddiv_rn(x, d);
-  const double q = __dmul_rn(x, rd);
-  const double r = __fma_rn(-q, d, x);
-  return __fma_rn(r, rd, q);
-}
-
-__device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, const FastGrid& w,
-                                             double* wt) {
+__device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, double* wt) {
   if (!(P.tx >= 0.0 && P.tx < g.lx && P.ty >= 0.0 && P.ty < g.ly && P.tz >= 0.0 && P.tz < g.lz)) {
     P.ok = false;
     return -1;
   }
-  const double sx = div_axis(P.tx, g.dx, w.rdx), sy = div_axis(P.ty, g.dy, w.rdy),
-               sz = div_axis(P.tz, g.dz, w.rdz);
+  const double sx = div_axis(P.tx, g.dx, g.rdx), sy = div_axis(P.ty, g.dy, g.rdy),
+               sz = div_axis(P.tz, g.dz, g.rdz);
   int i = __double2int_rz(sx), j = __double2int_rz(sy), k = __double2int_rz(sz);
   if (i >= g.nx) i = g.nx - 1;
   if (j >= g.ny) j = g.ny - 1;
@@ -546,7 +526,7 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, cons
 #pragma unroll
   for (int r = 0; r < rounds; ++r) {
     double wt[8];
-    const int cell = strict_locate(P, g, wg, wt);
+    const int cell = strict_locate(P, g, wt);
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
     if (cell != cc.cell) cache_load_strict(cc, nodes, cell);
     strict_round(P, cc, wt, sp.beta);

@@ -1,4 +1,4 @@
-"""The STRICT locate's division (div_axis in csrc/b2m_tile.cuh: q = x*rd,
+"""The STRICT locate's division (div_axis in csrc/b2m_mover.cuh: q = x*rd,
 r = fma(-q, d, x), fma(r, rd, q) with rd = RN(1/d)) against the IEEE
 division __ddiv_rn on the GPU: random positions over 40 binades below l for
 the C1-C5 / test spacings and 4000 random spacings, and every position within

@@ -1,5 +1,5 @@
 // div_check.cu -- the STRICT locate's division RN(x/d) as q = x*rd,
-// r = fma(-q, d, x), fma(r, rd, q) with rd = RN(1/d) from the host (b2m::div_axis), against
+// r = fma(-q, d, x), fma(r, rd, q) with rd = RN(1/d) from the host (b2m::div_axis in b2m_mover.cuh), against
 // the IEEE division __ddiv_rn, for x in [0, l): random mantissas over the
 // top 40 binades below l, and every x within +-32 ulps of each cell face k*d
 // (the truncation boundary).  Divisors: the C1-C5 grid spacings, the test
@@ -22,7 +22,7 @@ __device__ __forceinline__ uint64_t mix(uint64_t z) {
 
 // the product's function itself (B2M_STRICT_DIV=1 path)
 #define B2M_STRICT_DIV 1
-#include "b2m_tile.cuh"
+#include "b2m_mover.cuh"
 
 __device__ __forceinline__ double fast_div(double x, double d, double rd) {
   return b2m::div_axis(x, d, rd);
