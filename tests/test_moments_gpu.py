@@ -172,3 +172,34 @@ def test_cell_groups_runs_and_strays(gpu, order):
     m = gpu_deposit(p, grid, 0.003, pressure=True)
     assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.003, True),
                          what=order)
+
+
+@pytest.mark.parametrize("mode", ["fast", "strict"])
+def test_deposit_on_drifted_state(gpu, mode):
+    """The realistic cycle state: cell-sorted, then several mover steps of
+    drift (runs broken, strays in neighbouring cells) before the deposit."""
+    g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 16)
+    field = gem.gem_like_field(g)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    st = DeviceStore(g, [b.count() for b in batches], mode)
+    st.upload_field(field)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+        st.sort(s)
+    for _ in range(6):
+        st.move_all(mps)
+    st.moments_zero(with_pressure=True)
+    for s, b in enumerate(batches):
+        st.deposit(s, b.q_per_particle)
+    mine = MomentMesh.make(g, True)
+    st.moments_download(mine)
+    want = [np.zeros(g.cells()) for _ in range(10)]
+    for s, b in enumerate(batches):
+        p = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, p)
+        st.sync()
+        for a, w in zip(oracle.port_deposit_moments(p, grid, b.q_per_particle, True), want):
+            w += a
+    assert_moments_close(mine.arrays, want, what=f"drifted {mode}")
