@@ -99,7 +99,9 @@ class DeviceMigration:
         self._capi.check(self._capi.lib().b2m_outbox(self.store.h, s, direction, C.byref(p),
                                                      C.byref(n)))
         if n.value == 0:
-            return torch.empty((0, 6), dtype=torch.float64, device="cuda")
+            if getattr(self, "_empty", None) is None:
+                self._empty = torch.empty((0, 6), dtype=torch.float64, device="cuda")
+            return self._empty
         return torch.as_tensor(_CudaArray(p.value, (n.value, 6)), device="cuda")
 
     def inbox_append(self, s: int, recs):
@@ -149,6 +151,21 @@ class SlabWorld:
         # gloo has no CUDA point-to-point: stage device tensors through host
         backend = getattr(dist, "get_backend", lambda: "")()
         self.stage_host = (str(backend) == "gloo" and getattr(device, "type", "") == "cuda")
+
+    def _reduce_count(self, count: int, faulted: int):
+        """Global (count, faulted ranks): one all-reduce of two int64 through
+        reused pinned-host / device buffers (no pageable copy per cycle)."""
+        import torch
+        if getattr(self, "_cnt_dev", None) is None:
+            pin = getattr(self.device, "type", "") == "cuda"
+            self._cnt_host = torch.empty(2, dtype=torch.int64, pin_memory=pin)
+            self._cnt_dev = torch.empty(2, dtype=torch.int64, device=self.device)
+        self._cnt_host[0] = count
+        self._cnt_host[1] = faulted
+        self._cnt_dev.copy_(self._cnt_host, non_blocking=True)
+        self._all_reduce(self._cnt_dev)
+        self._cnt_host.copy_(self._cnt_dev)  # synchronises
+        return int(self._cnt_host[0]), int(self._cnt_host[1])
 
     def _count_all(self) -> int:
         return sum(self.store.count(s) for s in range(self.ns))
@@ -306,10 +323,8 @@ class SlabWorld:
                     err = e
                     break
         self.last_exchange = {"sent": moved}
-        t = torch.tensor([self._count_all() if err is None else 0, 1 if err is not None else 0],
-                         dtype=torch.int64, device=self.device)
-        self._all_reduce(t)
-        n, n_faulted = int(t[0].item()), int(t[1].item())
+        n, n_faulted = self._reduce_count(self._count_all() if err is None else 0,
+                                          1 if err is not None else 0)
         if err is not None:
             raise err
         if n_faulted:

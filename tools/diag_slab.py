@@ -40,7 +40,7 @@ for _ in range(K):
     ins = sw._exchange(outs); t = tick("exchange", t)
     for s in range(4): mig.inbox_append(s, ins[s].contiguous())
     t = tick("inbox_append", t)
-    c = torch.tensor([sw._count_all(), 0], dtype=torch.int64, device="cuda"); sw._all_reduce(c); int(c[0].item())
+    sw._reduce_count(sw._count_all(), 0)
     t = tick("count all-reduce", t)
 e1.record(); torch.cuda.synchronize()
 wall = (time.perf_counter() - t_all) / K * 1e3
