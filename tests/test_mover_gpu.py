@@ -351,6 +351,62 @@ def test_full_c2_strict_sampled_bitwise(gpu):
         assert_bitwise([a[idx] for a in out], want, f"C2 strict species {s}")
 
 
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_full_c2_strict_every_particle_vs_reference(gpu):
+    """Every one of the 61,046,784 C2 particles, two STRICT steps on the GPU
+    (nonzero E), bit-identical to the UNMODIFIED reference pic::move_batch
+    run on the host's cores over the same state (oracle/_ref)."""
+    import os
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    f = gem.gem_bench_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    st = DeviceStore(g, [b.count() for b in batches], "strict")
+    st.upload_field(f)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    st.move_all(mps)
+    st.move_all(mps)
+    threads = max(1, min(32, os.cpu_count() or 1))
+    for s, b in enumerate(batches):
+        out = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, out)
+        st.sync()
+        want = [a.copy() for a in b.span()]
+        for _ in range(2):
+            oracle.ref_move_batch(want, E, B, grid, 0.1, b.qom, 3, threads=threads)
+        assert_bitwise(out, want, f"C2 strict species {s}, all particles")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_full_c2_fast_every_particle_vs_reference(gpu):
+    """Every C2 particle, one FAST step, within the 1e-12 contract of the
+    UNMODIFIED reference pic::move_batch (oracle/_ref on the host's cores),
+    cell indices exact."""
+    import os
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    f = gem.gem_bench_field(g)
+    E, B = f.E.ravel(), f.B.ravel()
+    st = DeviceStore(g, [b.count() for b in batches], "fast")
+    st.upload_field(f)
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    st.move_all([MoverParams.make(0.1, b.qom, 3) for b in batches])
+    threads = max(1, min(32, os.cpu_count() or 1))
+    for s, b in enumerate(batches):
+        out = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, out)
+        st.sync()
+        want = [a.copy() for a in b.span()]
+        oracle.ref_move_batch(want, E, B, grid, 0.1, b.qom, 3, threads=threads)
+        assert_within_contract(out, want, grid, what=f"C2 fast species {s}, all particles")
+        np.testing.assert_array_equal(cells_of(out, grid), cells_of(want, grid))
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_host_call_context_cache(gpu, mode):
     """b2m_move_batch_host keeps one context per host thread: a fault in one
