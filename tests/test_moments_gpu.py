@@ -203,3 +203,32 @@ def test_deposit_on_drifted_state(gpu, mode):
         for a, w in zip(oracle.port_deposit_moments(p, grid, b.q_per_particle, True), want):
             w += a
     assert_moments_close(mine.arrays, want, what=f"drifted {mode}")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_full_c2_moments_vs_reference(gpu):
+    """All 61,046,784 C2 particles, cell-sorted then moved once (drifted):
+    rho, J and the pressure tensor from the device deposit agree with the
+    UNMODIFIED reference deposit_moments over the same particles."""
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    grid = g.as_tuple()
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    st = DeviceStore(g, [b.count() for b in batches], "strict")
+    st.upload_field(gem.gem_bench_field(g))
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+        st.sort(s)
+    st.move_all([MoverParams.make(0.1, b.qom, 3) for b in batches])
+    st.moments_zero(with_pressure=True)
+    for s, b in enumerate(batches):
+        st.deposit(s, b.q_per_particle)
+    mine = MomentMesh.make(g, True)
+    st.moments_download(mine)
+    want = [np.zeros(g.cells()) for _ in range(10)]
+    for s, b in enumerate(batches):
+        p = [np.empty(b.count()) for _ in range(6)]
+        st.download(s, p)
+        st.sync()
+        for a, w in zip(oracle.ref_deposit_moments(p, grid, b.q_per_particle, True), want):
+            w += a
+    assert_moments_close(mine.arrays, want, what="C2 vs reference")
