@@ -90,3 +90,16 @@ def test_stub_against_the_reference_library_itself(gpu):
     Ew, Bw = oracle.ref_field_phase_stub(E, B, g.as_tuple(), 4)
     assert_bitwise(out.E.ravel(), Ew, "E")
     assert_bitwise(out.B.ravel(), Bw, "B")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_c2_default_passes_vs_reference(gpu):
+    """The C2 mesh (64x64x32, 139,425 nodes) with the reference's default 100
+    passes (sim_config field_passes), bit-identical to the unmodified
+    reference field_phase_stub."""
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    E, B = random_field(g.as_tuple(), 21)
+    out = field_phase_stub(FieldMesh(g, E, B), g, 100)
+    Ew, Bw = oracle.ref_field_phase_stub(E, B, g.as_tuple(), 100)
+    assert_bitwise(out.E.ravel(), Ew, "E")
+    assert_bitwise(out.B.ravel(), Bw, "B")
