@@ -136,6 +136,16 @@ struct b2m_ctx {
   uint64_t n_nodes = 0;
   double* dE = nullptr;
   double* dE_alt = nullptr;  // field-stub ping-pong (allocated on first use)
+  // field stub replayed as a CUDA graph: the `passes` launches are captured
+  // once per (passes, buffers, stream) and replayed with one cudaGraphLaunch
+  // (two entries: an odd pass count alternates the ping-pong buffers)
+  struct StubGraph {
+    cudaGraphExec_t exec = nullptr;
+    int passes = 0;
+    const double* in = nullptr;
+    cudaStream_t stream = nullptr;
+    double* out = nullptr;
+  } stub[2];
   double* strict_nodes = nullptr;  // STRICT per-cell corner node table
   uint64_t strict_gen = 0;
   double* dB = nullptr;
@@ -446,6 +456,8 @@ b2m_status b2m_ctx_destroy(b2m_ctx* ctx) {
   if (!ctx) return B2M_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& c : ctx->stub)
+    if (c.exec) cudaGraphExecDestroy(c.exec);
   for (void* p : ctx->allocations) cudaFree(p);
   for (Species& S : ctx->sp)
     if (S.totals_h) cudaFreeHost(S.totals_h);
@@ -557,9 +569,38 @@ b2m_status b2m_field_phase_stub(b2m_ctx* ctx, int passes) {
   if (passes <= 0) return B2M_OK;
   if (!ctx->dE_alt && (st = dalloc(ctx, &ctx->dE_alt, 3 * ctx->n_nodes, "field stub")) != B2M_OK)
     return st;
-  double* out = launch_field_stub(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
-                                  ctx->dE_alt, passes, ctx->stream);
-  if (out != ctx->dE) std::swap(ctx->dE, ctx->dE_alt);
+  // `passes` dependent launches of a ~µs kernel are launch-bound: capture them
+  // once into a CUDA graph and replay it (re-captured when the pass count,
+  // the ping-pong state or the stream changes)
+  b2m_ctx::StubGraph* sg = nullptr;
+  for (auto& c : ctx->stub)
+    if (c.exec && c.passes == passes && c.in == ctx->dE && c.stream == ctx->stream) sg = &c;
+  if (!sg) {
+    sg = &ctx->stub[ctx->stub[0].exec && ctx->stub[0].in != ctx->dE ? 1 : 0];
+    if (sg->exec) {
+      cudaGraphExecDestroy(sg->exec);
+      sg->exec = nullptr;
+    }
+    B2M_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    double* out = launch_field_stub(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
+                                    ctx->dE_alt, passes, ctx->stream);
+    note_launch(-(passes + 1));  // counted when the graph runs
+    cudaGraph_t graph = nullptr;
+    B2M_CUDA(ctx, cudaStreamEndCapture(ctx->stream, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&sg->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      sg->exec = nullptr;
+      return cuda_fail(ctx, e, "cudaGraphInstantiate (field stub)");
+    }
+    sg->passes = passes;
+    sg->in = ctx->dE;
+    sg->stream = ctx->stream;
+    sg->out = out;
+  }
+  B2M_CUDA(ctx, cudaGraphLaunch(sg->exec, ctx->stream));
+  note_launch(passes + 1);
+  if (sg->out != ctx->dE) std::swap(ctx->dE, ctx->dE_alt);
   B2M_CUDA(ctx, cudaGetLastError());
   return relayout(ctx);  // a new field: FAST tables rebuild on the next move
 }
