@@ -259,6 +259,35 @@ b2m_status b2m_outbox(b2m_ctx* ctx, int s, int dir, double** d_recs, uint64_t* c
  * (merge_incoming, runtime.cpp:64-76).  AllocError above capacity. */
 b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t n);
 
+/* ---- native slab world over NCCL ------------------------------------------
+ * Simulation's per-cycle protocol (runtime.cpp:218-288) for one rank per
+ * GPU, replacing worker_loop's mover + partition_outgoing + exchange +
+ * merge_incoming + count check (runtime.cpp:227-269).
+ * b2m_world_id: the NCCL unique id (B2M_WORLD_ID_BYTES), made on one rank and
+ * handed to all.  b2m_world_init: b2m_slab_config + ncclCommInitRank + the
+ * exchange buffers (AllocError here, never mid-run); id == NULL builds the
+ * buffers without a communicator (world of 1, or b2m_world_loopback_step).
+ * b2m_world_set_total: the global particle count, the conservation reference
+ * (runtime.cpp:150).  b2m_world_step: b2m_move_migrate_all, the outbox counts
+ * and then the records exchanged with prev / next (grouped ncclSend/ncclRecv),
+ * merge, and one all-reduce of (count, faulted): returns this rank's typed
+ * fault (NumericalFault / CflViolation / DomainError / AllocError) when it
+ * faulted -- it still completes the exchange with empty outboxes so its peers
+ * do not hang (the analogue of arrive_and_drop, runtime.cpp:283-288) --,
+ * EngineFault when a peer faulted or the global count drifted.  Two host
+ * synchronisations per step.  *sent = records this rank sent. */
+#define B2M_WORLD_ID_BYTES 128
+b2m_status b2m_world_id(void* id);
+b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world);
+b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
+b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
+                          uint64_t* global_count);
+/* The same protocol over the `world` contexts of ONE process (rank r =
+ * ctxs[r], each b2m_world_init'ed with id NULL), the exchange done by device
+ * copies: the protocol without NCCL, for tests on one GPU. */
+b2m_status b2m_world_loopback_step(b2m_ctx* const* ctxs, int world, const b2m_mover_params* mp,
+                                   uint64_t* sent);
+
 /* ---- synthetic GEM input (init.cpp:62-102, rng.hpp:12-56) ----------------
  * Bit-identical to pic::init_gem for the default GEM parameters
  * (sim_config.hpp:30-39) on grid g: the 4 species (bg e-, bg i+, sheet e-,

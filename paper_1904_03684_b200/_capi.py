@@ -98,6 +98,13 @@ SIGNATURES = {
     "b2m_move_migrate_all": (_st, [C.c_void_p, C.POINTER(b2m_mover_params)]),
     "b2m_outbox": (_st, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_u64)]),
     "b2m_inbox_append": (_st, [C.c_void_p, C.c_int, C.c_void_p, _u64]),
+    "b2m_world_id": (_st, [C.c_void_p]),
+    "b2m_world_init": (_st, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "b2m_world_set_total": (_st, [C.c_void_p, C.POINTER(_u64)]),
+    "b2m_world_step": (_st, [C.c_void_p, C.POINTER(b2m_mover_params), C.POINTER(_u64),
+                             C.POINTER(_u64)]),
+    "b2m_world_loopback_step": (_st, [C.POINTER(C.c_void_p), C.c_int,
+                                      C.POINTER(b2m_mover_params), C.POINTER(_u64)]),
     "b2m_gem_counts": (_st, [C.POINTER(b2m_grid), C.c_int, C.POINTER(_u64)]),
     "b2m_gem_species_params": (_st, [C.POINTER(b2m_grid), C.c_int, _dp, _dp]),
     "b2m_gem_fill_species": (_st, [C.POINTER(b2m_grid), C.c_int, _u64, C.c_int, C.POINTER(_dp),

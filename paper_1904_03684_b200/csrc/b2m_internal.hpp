@@ -65,6 +65,9 @@ double* launch_field_stub(int nx, int ny, int nz, double* E, double* B, double* 
                           int passes, cudaStream_t st);
 // Reset the fault words to "clean".
 void launch_fault_reset(FaultWord* fault, cudaStream_t st);
+void launch_pack_counts(const unsigned long long* const* totals, int ns,
+                        const unsigned long long* cap, const FaultWord* fault,
+                        unsigned long long* out, cudaStream_t st);
 
 // Cell keys of the current positions (cell-unit locate), for sorting.
 void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,

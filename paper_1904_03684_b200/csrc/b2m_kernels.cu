@@ -695,6 +695,33 @@ void launch_sort_pairs(void* temp, size_t temp_bytes, const uint32_t* kin, uint3
   note_launch((key_bits + 7) / 8 + 1);
 }
 
+// Native slab world (b2m_world_step): the per-species outbox counts
+// (totals[s] = {prev, next, holes}) packed into one [2][ns] send buffer for
+// the counts exchange, all zero when this rank faulted or an outbox
+// overflowed -- a faulted rank keeps running the protocol with empty
+// outboxes (runtime.cpp:283-288 drops it from the barrier instead).
+__global__ void pack_counts_kernel(const unsigned long long* const* totals, int ns,
+                                   const unsigned long long* cap, const FaultWord* fault,
+                                   unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  bool bad = fault->numerical != ~0ull || fault->cfl != ~0ull || fault->domain != ~0ull;
+  for (int s = 0; s < ns; ++s) {
+    const unsigned long long p = totals[s][0], n = totals[s][1];
+    bad = bad || p > cap[s] || n > cap[s];
+    out[s] = p;
+    out[ns + s] = n;
+  }
+  if (bad)
+    for (int i = 0; i < 2 * ns; ++i) out[i] = 0;
+}
+
+void launch_pack_counts(const unsigned long long* const* totals, int ns,
+                        const unsigned long long* cap, const FaultWord* fault,
+                        unsigned long long* out, cudaStream_t st) {
+  pack_counts_kernel<<<1, 32, 0, st>>>(totals, ns, cap, fault, out);
+  note_launch();
+}
+
 uint64_t migrate_tiles(uint64_t n) { return (n + kTileParticles - 1) / kTileParticles; }
 
 size_t scan_temp_bytes(uint64_t n_tiles) {

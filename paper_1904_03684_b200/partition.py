@@ -334,6 +334,70 @@ class SlabWorld:
         return moved
 
 
+class NativeSlabWorld:
+    """One rank of the slab-partitioned mover with the whole per-cycle
+    protocol in the native library (b2m_world_step: mover + owner scan +
+    compaction, NCCL exchange with prev / next, merge, count all-reduce --
+    two host synchronisations per step, no Python on the data path).
+
+    ``dist`` (torch.distributed, initialised) only carries the NCCL unique
+    id from rank 0 to the others; ``store`` is this rank's DeviceStore."""
+
+    def __init__(self, grid, store, rank: int, world: int, dist=None):
+        from . import _capi
+        self._capi = _capi
+        self.grid, self.store, self.rank, self.world = grid, store, rank, world
+        self.ns = store.n_species
+        self.last_exchange = {}
+        self.total = None
+        uid = (C.c_ubyte * 128)()
+        if world > 1:
+            if rank == 0:
+                _capi.check(_capi.lib().b2m_world_id(uid))
+            if dist is not None:
+                obj = [bytes(uid)]
+                dist.broadcast_object_list(obj, src=0)
+                uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+            _capi.check(_capi.lib().b2m_world_init(store.h, uid, rank, world))
+        else:
+            _capi.check(_capi.lib().b2m_world_init(store.h, None, rank, world))
+
+    def set_total(self) -> int:
+        n = C.c_uint64()
+        self._capi.check(self._capi.lib().b2m_world_set_total(self.store.h, C.byref(n)))
+        self.total = int(n.value)
+        return self.total
+
+    def step(self, mps) -> int:
+        arr = (self._capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+        sent, total = C.c_uint64(), C.c_uint64()
+        self._capi.check(self._capi.lib().b2m_world_step(self.store.h, arr, C.byref(sent),
+                                                          C.byref(total)))
+        self.last_exchange = {"sent": int(sent.value), "global_count": int(total.value)}
+        return int(sent.value)
+
+
+def loopback_world(stores, grid):
+    """b2m_world_init (no communicator) on each of ``stores`` as ranks
+    0..W-1 of one process: for b2m_world_loopback_step."""
+    from . import _capi
+    w = len(stores)
+    for r, st in enumerate(stores):
+        _capi.check(_capi.lib().b2m_world_init(st.h, None, r, w))
+        _capi.check(_capi.lib().b2m_world_set_total(st.h, None))
+
+
+def loopback_step(stores, mps) -> int:
+    """One protocol step over in-process ranks (device copies stand in for
+    NCCL; the same native phases as b2m_world_step)."""
+    from . import _capi
+    arr = (_capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+    hs = (C.c_void_p * len(stores))(*[st.h for st in stores])
+    sent = C.c_uint64()
+    _capi.check(_capi.lib().b2m_world_loopback_step(hs, len(stores), arr, C.byref(sent)))
+    return int(sent.value)
+
+
 # ---------------------------------------------------------------------------
 # multi-GPU benchmark (bench.py --gpus N under torchrun)
 # ---------------------------------------------------------------------------

@@ -1,0 +1,136 @@
+"""The native slab world (b2m_world_*: the per-cycle protocol of
+Simulation, runtime.cpp:218-288, in the library).  Several ranks as
+contexts of one process on one B200 run b2m_world_loopback_step -- the same
+native phases as b2m_world_step, device copies standing in for NCCL -- and
+must reproduce the reference multi-worker Simulation (STRICT: bitwise
+particle multiset, FAST: within contract), keep every particle on its owner
+rank, conserve the count, and surface faults typed on the faulting rank with
+EngineFault elsewhere.  A world of one runs b2m_world_step itself, through a
+real NCCL communicator."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1904_03684_b200 import _capi, gem
+from paper_1904_03684_b200.engine import DeviceStore
+from paper_1904_03684_b200.errors import CflViolation, NumericalFault
+from paper_1904_03684_b200.mover import Grid, MoverParams
+from paper_1904_03684_b200.partition import (NativeSlabWorld, loopback_step, loopback_world,
+                                             owner_of)
+from tests._util import assert_bitwise, assert_within_contract
+
+pytestmark = pytest.mark.gpu
+GRID_T = (8, 8, 8, 6.4, 6.4, 6.4)
+
+
+def _stores(mode, world, inject=None):
+    g = Grid.make(*GRID_T)
+    stores, batches_all = [], []
+    for r in range(world):
+        batches = gem.init_gem_slab(g, 8, r, world, pinned=False)
+        if inject and r == inject[0]:
+            _, s, a, val = inject
+            batches[s].arrays[a][0] = val
+        st = DeviceStore(g, [b.count() + 4096 for b in batches], mode)
+        st.upload_field(gem.gem_field(g))
+        for s, b in enumerate(batches):
+            st.upload(s, b.span())
+        stores.append(st)
+        batches_all.append(batches)
+    loopback_world(stores, g)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches_all[0]]
+    return g, stores, mps
+
+
+def _download(st):
+    out = []
+    for s in range(st.n_species):
+        p6 = [np.empty(st.count(s)) for _ in range(6)]
+        st.download(s, p6)
+        out.append(p6)
+    st.sync()
+    return out
+
+
+def _key_sorted(p6):
+    order = np.lexsort([np.round(p6[a], 6) for a in (2, 1, 0)])
+    return [a[order] for a in p6]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_loopback_world_matches_reference_simulation(gpu, world, mode):
+    g, stores, mps = _stores(mode, world)
+    sent = 0
+    for _ in range(3):
+        sent += loopback_step(stores, mps)
+    assert sent > 0   # particles did cross slab boundaries
+    res = [_download(st) for st in stores]
+    sim = oracle.RefSimulation(GRID_T, 8, workers=world, engine="cpu", field_passes=0)
+    sim.run(3)
+    for s in range(4):
+        for r in range(world):
+            assert np.all(owner_of(res[r][s][1], g, world) == r)
+        mine = [np.concatenate([res[r][s][a] for r in range(world)]) for a in range(6)]
+        ref = sim.gather(s)
+        assert len(mine[0]) == len(ref[0])
+        if mode == "strict":
+            np.testing.assert_array_equal(oracle.multiset(mine), oracle.multiset(ref))
+        else:
+            assert_within_contract(_key_sorted(mine), _key_sorted(ref), GRID_T, tol=1e-11)
+    for st in stores:
+        st.close()
+
+
+def test_loopback_world_cfl_violation(gpu):
+    g, stores, mps = _stores("fast", 4, inject=(1, 1, 4, 40.0))
+    with pytest.raises(CflViolation, match="non-neighbor slab"):
+        loopback_step(stores, mps)
+    for st in stores:
+        st.close()
+
+
+def test_loopback_world_nan_fault(gpu):
+    g, stores, mps = _stores("strict", 2, inject=(0, 0, 3, float("nan")))
+    with pytest.raises(NumericalFault, match="particle index 0"):
+        loopback_step(stores, mps)
+    for st in stores:
+        st.close()
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_world_of_one_over_nccl_equals_plain_mover(gpu, mode):
+    """b2m_world_step with a real one-rank NCCL communicator (no exchange):
+    the same particles as the plain mover, the count conserved."""
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29547")
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    g = Grid.make(*GRID_T)
+    batches = gem.init_gem_slab(g, 8, 0, 1, pinned=False)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    a = DeviceStore(g, [b.count() + 64 for b in batches], mode)
+    b_ = DeviceStore(g, [b.count() + 64 for b in batches], mode)
+    for st in (a, b_):
+        st.upload_field(gem.gem_field(g))
+        for s, b in enumerate(batches):
+            st.upload(s, b.span())
+    uid = (C.c_ubyte * 128)()
+    _capi.check(_capi.lib().b2m_world_id(uid))
+    _capi.check(_capi.lib().b2m_world_init(a.h, uid, 0, 1))
+    w = NativeSlabWorld.__new__(NativeSlabWorld)
+    w._capi, w.store, w.ns, w.last_exchange = _capi, a, a.n_species, {}
+    total = w.set_total()
+    assert total == sum(b.count() for b in batches)
+    for _ in range(3):
+        assert w.step(mps) == 0
+        assert w.last_exchange["global_count"] == total
+        b_.move_all(mps)
+    for x, y in zip(_download(a), _download(b_)):
+        assert_bitwise(x, y, mode)
+    a.close()
+    b_.close()

@@ -15,5 +15,5 @@ for v in "$@"; do
   done
   wait
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libb2m_$v$TAG.so $objs \
-       ../../build/b2m/b2m_gem.o -Xcompiler -pthread
+       ../../build/b2m/b2m_gem.o -Xcompiler -pthread -ldl
 done
