@@ -443,9 +443,24 @@ def bench_world(args) -> int:
     for s, b in enumerate(batches):
         store.upload(s, b.span())
         store.sort(s)
-    mig = DeviceMigration(store, rank, world)
-    sw = SlabWorld(grid, mig, len(batches), dist, torch.device("cuda", local))
+    # the per-cycle protocol runs in the library (b2m_world_step) over NCCL;
+    # B2M_NATIVE_WORLD=0 (or gloo) runs the Python SlabWorld over torch.distributed
+    native = backend == "nccl" and os.environ.get("B2M_NATIVE_WORLD", "1") != "0"
+    if native:
+        sw = NativeSlabWorld(grid, store, rank, world, dist)
+    else:
+        mig = DeviceMigration(store, rank, world)
+        sw = SlabWorld(grid, mig, len(batches), dist, torch.device("cuda", local))
     sw.set_total()
+
+    def all_reduce(t, op=dist.ReduceOp.SUM):  # timing and count reductions
+        if backend == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h.to(t.device))
+        else:
+            dist.all_reduce(t, op=op)
+
     # field replication: rank 0's device field is broadcast to every rank
     # (runtime.cpp:143 replicates the mesh).  The benchmark field is static,
     # like the single-GPU line's, so it is replicated once before timing; a
@@ -493,11 +508,11 @@ def bench_world(args) -> int:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    sw._all_reduce(t, op=dist.ReduceOp.MAX)
+    all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item()) / args.steps
     n_local = torch.tensor([sum(store.count(s) for s in range(len(batches)))], dtype=torch.int64,
                            device="cuda")
-    sw._all_reduce(n_local)
+    all_reduce(n_local)
     n_total = int(n_local.item())
     launches = _capi.lib().b2m_launch_count() - l0
 
@@ -520,10 +535,10 @@ def bench_world(args) -> int:
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         eng.close()
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        sw._all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
         n_here = torch.tensor([sum(b.count() for b in batches)], dtype=torch.int64, device="cuda")
-        sw._all_reduce(n_here)
+        all_reduce(n_here)
         n_e2e = int(n_here.item())
         e2e = {"value": n_e2e / e2e_s / 1e6, "unit": "MPA/s",
                "h2d_bytes_per_step": 48 * n_e2e + world * 2 * 24 * grid.nodes(),
@@ -540,7 +555,9 @@ def bench_world(args) -> int:
                            "particles": n_total, "mode": args.mode,
                            "cell_sort": f"every {args.resort} steps" if args.resort else "once",
                            "parallelism": f"y-slab x{world}, {backend} P2P migration of all "
-                                          "species per step + count all-reduce; static field "
+                                          "species per step + count all-reduce ("
+                                          + ("native b2m_world_step" if native else
+                                             "Python SlabWorld") + "); static field "
                                           "broadcast once",
                            "migrated_per_step_rank0": moved / max(1, args.steps)},
                 "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": None}

@@ -48,4 +48,19 @@ print(f"step wall {wall:.3f} ms, device {e0.elapsed_time(e1) / K:.3f} ms")
 for k, v in T.items(): print(f"  {k:28s} {v / K * 1e3:.3f} ms")
 st.record(2); st.move_all(mps); st.record(3); st.sync()
 print(f"plain move_all: {st.elapsed_ms(2, 3):.3f} ms")
+# the same step in the library (b2m_world_step over a one-rank NCCL communicator)
+from paper_1904_03684_b200.partition import NativeSlabWorld
+st2 = DeviceStore(grid, [int(b.count() * 1.05) + 65536 for b in batches], "fast")
+st2.set_stream(stream.cuda_stream)
+st2.upload_field(gem.gem_field(grid))
+for s, b in enumerate(batches): st2.upload(s, b.span()); st2.sort(s)
+nw = NativeSlabWorld(grid, st2, 0, 1, dist)
+nw.set_total()
+for _ in range(3): nw.step(mps)
+torch.cuda.synchronize()
+e0.record(); t0 = time.perf_counter()
+for _ in range(K): nw.step(mps)
+e1.record(); torch.cuda.synchronize()
+print(f"native b2m_world_step: wall {(time.perf_counter() - t0) / K * 1e3:.3f} ms, "
+      f"device {e0.elapsed_time(e1) / K:.3f} ms")
 dist.destroy_process_group()
