@@ -1521,13 +1521,21 @@ uint64_t world_sent(const b2m_ctx* ctx) {
 b2m_status world_verdict(b2m_ctx* ctx, b2m_status own, long long n, long long faulted,
                          uint64_t* global_count) {
   if (global_count) *global_count = static_cast<uint64_t>(n);
-  if (own != B2M_OK) return own;  // message already recorded
-  if (faulted > 0)
-    return fail(B2M_ENGINE_FAULT, "simulation aborted: " + std::to_string(faulted) +
-                                      " peer rank(s) faulted in this cycle");
-  if (ctx->w.total_set && static_cast<uint64_t>(n) != ctx->w.total)
-    return fail(B2M_ENGINE_FAULT, "particle count drifted: " + std::to_string(n) + " vs " +
-                                      std::to_string(ctx->w.total));
+  if (own != B2M_OK) return own;  // message already recorded, context poisoned
+  // every rank leaves a failed cycle poisoned, so none of them enters the
+  // next cycle's collectives alone
+  if (faulted > 0) {
+    ctx->poisoned = true;
+    ctx->poison_msg = "simulation aborted: " + std::to_string(faulted) +
+                      " peer rank(s) faulted in this cycle";
+    return fail(B2M_ENGINE_FAULT, ctx->poison_msg);
+  }
+  if (ctx->w.total_set && static_cast<uint64_t>(n) != ctx->w.total) {
+    ctx->poisoned = true;
+    ctx->poison_msg = "particle count drifted: " + std::to_string(n) + " vs " +
+                      std::to_string(ctx->w.total);
+    return fail(B2M_ENGINE_FAULT, ctx->poison_msg);
+  }
   return B2M_OK;
 }
 
@@ -1686,6 +1694,10 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
     B2M_NCCL(ctx, nccl().AllReduce(w.red, w.red, 2, ncclInt64, ncclSum, w.comm, ctx->stream));
     cudaMemcpyAsync(w.red_h, w.red, 2 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);  // host sync 2
+  }
+  if (own != B2M_OK && !ctx->poisoned) {  // e.g. an arrival overflowed the batch capacity
+    ctx->poisoned = true;
+    ctx->poison_msg = g_last_error;
   }
   return world_verdict(ctx, own, w.red_h[0], own == B2M_OK ? w.red_h[1] : 0, global_count);
 }
