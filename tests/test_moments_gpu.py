@@ -232,3 +232,28 @@ def test_full_c2_moments_vs_reference(gpu):
         for a, w in zip(oracle.ref_deposit_moments(p, grid, b.q_per_particle, True), want):
             w += a
     assert_moments_close(mine.arrays, want, what="C2 vs reference")
+
+
+def test_empty_species_and_batches(gpu):
+    """An empty batch deposits nothing; a store whose species are empty
+    moves, sorts and deposits without touching the mesh."""
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    p = [np.empty(0) for _ in range(6)]
+    m = gpu_deposit(p, grid, 1.0, pressure=True)
+    assert all(not np.any(a) for a in m.arrays)
+    g = Grid.make(*grid)
+    st = DeviceStore(g, [0, 16], "strict")
+    st.upload_field(gem.gem_field(g))
+    q = random_particles(grid, 16, 3)
+    st.upload(1, q)
+    mps = [MoverParams.make(0.1, -25.0, 3), MoverParams.make(0.1, 1.0, 3)]
+    st.move_all(mps)
+    st.sort(0)
+    st.sort(1)
+    st.moments_zero(with_pressure=False)
+    st.deposit(0, 1.0)
+    mine = MomentMesh.make(g, False)
+    st.moments_download(mine)
+    assert all(not np.any(a) for a in mine.arrays)
+    assert st.count(0) == 0 and st.count(1) == 16
+    st.close()
