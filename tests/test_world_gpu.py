@@ -134,3 +134,20 @@ def test_world_of_one_over_nccl_equals_plain_mover(gpu, mode):
         assert_bitwise(x, y, mode)
     a.close()
     b_.close()
+
+
+def test_world_api_misuse_is_config_error(gpu):
+    from paper_1904_03684_b200.errors import ConfigError
+    g = Grid.make(*GRID_T)
+    st = DeviceStore(g, [64], "fast")
+    arr = (_capi.b2m_mover_params * 1)(MoverParams.make(0.1, 1.0, 3).to_c())
+    with pytest.raises(ConfigError, match="world_init"):
+        _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
+    with pytest.raises(ConfigError, match="does not divide"):
+        _capi.check(_capi.lib().b2m_world_init(st.h, None, 0, 3))
+    _capi.check(_capi.lib().b2m_world_init(st.h, None, 0, 2))
+    with pytest.raises(ConfigError, match="already"):
+        _capi.check(_capi.lib().b2m_world_init(st.h, None, 0, 2))
+    with pytest.raises(ConfigError, match="NCCL communicator"):
+        _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
+    st.close()
