@@ -151,3 +151,42 @@ def test_world_api_misuse_is_config_error(gpu):
     with pytest.raises(ConfigError, match="NCCL communicator"):
         _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
     st.close()
+
+
+def test_loopback_four_ranks_equal_one_context_after_many_steps(gpu):
+    """1.2M GEM particles split over 4 slab ranks (loopback protocol) for 8
+    STRICT steps: every particle is on its owner rank, and the union is the
+    bitwise multiset of the same particles moved 8 times in one context (the
+    mover is per-particle, migration only relocates)."""
+    grid_t = (32, 32, 16, 12.8, 6.4, 3.2)
+    g = Grid.make(*grid_t)
+    world = 4
+    full = gem.init_gem_species(g, 72, pinned=False)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in full]
+    ref = DeviceStore(g, [b.count() for b in full], "strict")
+    ref.upload_field(gem.gem_field(g))
+    for s, b in enumerate(full):
+        ref.upload(s, b.span())
+    stores = []
+    for r in range(world):
+        part = gem.init_gem_slab(g, 72, r, world, pinned=False)
+        st = DeviceStore(g, [b.count() * 2 + 4096 for b in part], "strict")
+        st.upload_field(gem.gem_field(g))
+        for s, b in enumerate(part):
+            st.upload(s, b.span())
+        stores.append(st)
+    loopback_world(stores, g)
+    sent = 0
+    for _ in range(8):
+        sent += loopback_step(stores, mps)
+        ref.move_all(mps)
+    assert sent > 1000
+    want = _download(ref)
+    got = [_download(st) for st in stores]
+    for s in range(4):
+        for r in range(world):
+            assert np.all(owner_of(got[r][s][1], g, world) == r)
+        mine = [np.concatenate([got[r][s][a] for r in range(world)]) for a in range(6)]
+        np.testing.assert_array_equal(oracle.multiset(mine), oracle.multiset(want[s]))
+    for st in stores + [ref]:
+        st.close()
