@@ -1,0 +1,431 @@
+// b2m_world.cu — the native slab world (include/b2m.h, b2m_world_*):
+// Simulation's per-cycle protocol (runtime.cpp:218-288) for one rank per GPU
+// -- mover + owner scan + compaction, the outbox counts and records
+// exchanged with prev / next over NCCL, merge_incoming, the global count
+// check -- and the same phases over several in-process ranks with device
+// copies in place of NCCL (b2m_world_loopback_step, for tests).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include <dlfcn.h>
+
+#include "b2m_ctx.hpp"
+
+namespace b2m {
+
+// (see NcclApi in b2m_ctx.hpp)
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's own, if any
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+    if (!h) {
+      a.why = std::string("libnccl.so.2 not found: ") + dlerror();
+      return a;
+    }
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      return fn != nullptr;
+    };
+    a.ok = sym(a.GetUniqueId, "ncclGetUniqueId") && sym(a.CommInitRank, "ncclCommInitRank") &&
+           sym(a.CommDestroy, "ncclCommDestroy") && sym(a.AllReduce, "ncclAllReduce") &&
+           sym(a.Send, "ncclSend") && sym(a.Recv, "ncclRecv") &&
+           sym(a.GroupStart, "ncclGroupStart") && sym(a.GroupEnd, "ncclGroupEnd") &&
+           sym(a.GetErrorString, "ncclGetErrorString");
+    if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+
+
+}  // namespace b2m
+
+using namespace b2m;
+
+extern "C" {
+/* ---- native slab world ---------------------------------------------------
+ * Simulation's per-cycle protocol (runtime.cpp:227-288) for one rank per GPU:
+ * mover + owner scan + compaction (b2m_move_migrate_all), the outbox counts
+ * and then the records exchanged with prev / next, merge_incoming, and the
+ * global count check.  The NCCL form posts, in every round, sends to prev
+ * before sends to next and receives from prev before receives from next,
+ * species in order, zero-length messages skipped on both sides (each side
+ * knows every size from the counts round); NCCL matches point-to-point
+ * messages between two ranks in posting order, so with two ranks (prev ==
+ * next) the blocks pair up the same way. */
+
+namespace {
+
+b2m_status nccl_fail(b2m_ctx* ctx, ncclResult_t r, const char* what) {
+  if (ctx) {
+    ctx->poisoned = true;
+    ctx->poison_msg = std::string(what) + ": " + nccl().GetErrorString(r);
+  }
+  return fail(B2M_ENGINE_FAULT, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+#define B2M_NCCL(ctx, call)                              \
+  do {                                                   \
+    ncclResult_t r_ = (call);                            \
+    if (r_ != ncclSuccess) return nccl_fail((ctx), r_, #call); \
+  } while (0)
+
+// phase A: mover + compaction + packed counts (asynchronous)
+b2m_status world_move(b2m_ctx* ctx, const b2m_mover_params* mp) {
+  const int ns = static_cast<int>(ctx->sp.size());
+  std::vector<int> all(static_cast<size_t>(ns));
+  for (int s = 0; s < ns; ++s) all[static_cast<size_t>(s)] = s;
+  b2m_status st = move_migrate_species(ctx, all.data(), mp, ns);
+  if (st != B2M_OK) return st;
+  // species with no particles skipped the mover: their totals stay as the
+  // last step left them, so clear them first
+  for (int s = 0; s < ns; ++s)
+    if (ctx->sp[static_cast<size_t>(s)].pre_count == 0)
+      B2M_CUDA(ctx, cudaMemsetAsync(ctx->sp[static_cast<size_t>(s)].totals, 0,
+                                    3 * sizeof(unsigned long long), ctx->stream));
+  launch_pack_counts(ctx->w.totals, ns, ctx->w.cap, ctx->fault, ctx->w.cnt_send, ctx->stream);
+  B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+// phase B: counts to the host, faults evaluated (the typed error is returned
+// but the caller keeps running the protocol)
+b2m_status world_counts(b2m_ctx* ctx) {
+  const size_t ns = ctx->sp.size();
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->w.cnt_h, ctx->w.cnt_send, 2 * ns * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->w.cnt_h + 2 * ns, ctx->w.cnt_recv,
+                                2 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  b2m_status st = b2m_sync(ctx, nullptr, nullptr);  // syncs; typed fault, poisons
+  if (st != B2M_OK) return st;
+  for (size_t s = 0; s < ns; ++s) {
+    const Species& S = ctx->sp[s];
+    if (S.totals_h[0] > S.cap_out || S.totals_h[1] > S.cap_out) {
+      ctx->poisoned = true;
+      ctx->poison_msg = "outbox capacity exceeded (" +
+                        std::to_string(std::max(S.totals_h[0], S.totals_h[1])) + " > " +
+                        std::to_string(S.cap_out) + ")";
+      return fail(B2M_ALLOC_ERROR, ctx->poison_msg);
+    }
+    const uint64_t in = ctx->w.cnt_h[2 * ns + s] + ctx->w.cnt_h[3 * ns + s];
+    if (in > ctx->w.stage_cap[s]) {
+      ctx->poisoned = true;
+      ctx->poison_msg = "arrivals exceed the exchange buffer";
+      return fail(B2M_ALLOC_ERROR, ctx->poison_msg);
+    }
+  }
+  return B2M_OK;
+}
+
+// phase C: merge the arrivals (stage[s] = from prev, then from next)
+b2m_status world_merge(b2m_ctx* ctx) {
+  const size_t ns = ctx->sp.size();
+  for (size_t s = 0; s < ns; ++s) {
+    const uint64_t in = ctx->w.cnt_h[2 * ns + s] + ctx->w.cnt_h[3 * ns + s];
+    b2m_status st = b2m_inbox_append(ctx, static_cast<int>(s), ctx->w.stage[s], in);
+    if (st != B2M_OK) return st;
+  }
+  return B2M_OK;
+}
+
+uint64_t world_local_count(const b2m_ctx* ctx) {
+  uint64_t n = 0;
+  for (const Species& S : ctx->sp) n += S.count;
+  return n;
+}
+
+uint64_t world_sent(const b2m_ctx* ctx) {
+  const size_t ns = ctx->sp.size();
+  uint64_t n = 0;
+  for (size_t i = 0; i < 2 * ns; ++i) n += ctx->w.cnt_h[i];
+  return n;
+}
+
+// phase D: the global verdict from the reduced (count, faulted ranks)
+b2m_status world_verdict(b2m_ctx* ctx, b2m_status own, long long n, long long faulted,
+                         uint64_t* global_count) {
+  if (global_count) *global_count = static_cast<uint64_t>(n);
+  if (own != B2M_OK) return own;  // message already recorded, context poisoned
+  // every rank leaves a failed cycle poisoned, so none of them enters the
+  // next cycle's collectives alone
+  if (faulted > 0) {
+    ctx->poisoned = true;
+    ctx->poison_msg = "simulation aborted: " + std::to_string(faulted) +
+                      " peer rank(s) faulted in this cycle";
+    return fail(B2M_ENGINE_FAULT, ctx->poison_msg);
+  }
+  if (ctx->w.total_set && static_cast<uint64_t>(n) != ctx->w.total) {
+    ctx->poisoned = true;
+    ctx->poison_msg = "particle count drifted: " + std::to_string(n) + " vs " +
+                      std::to_string(ctx->w.total);
+    return fail(B2M_ENGINE_FAULT, ctx->poison_msg);
+  }
+  return B2M_OK;
+}
+
+b2m_status world_alloc(b2m_ctx* ctx, const std::vector<uint64_t>& stage_cap) {
+  b2m_status st;
+  auto& w = ctx->w;
+  const size_t ns = ctx->sp.size();
+  if ((st = dalloc(ctx, &w.totals, ns, "world totals")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &w.cap, ns, "world caps")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &w.cnt_send, 2 * ns, "world counts")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &w.cnt_recv, 2 * ns, "world counts")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &w.red, 2, "world reduction")) != B2M_OK) return st;
+  if (cudaMallocHost(&w.cnt_h, 4 * ns * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost(&w.red_h, 2 * sizeof(long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(B2M_ALLOC_ERROR, "pinned world buffers");
+  }
+  std::vector<unsigned long long*> tp(ns);
+  std::vector<unsigned long long> cap(ns);
+  w.stage.assign(ns, nullptr);
+  w.stage_cap = stage_cap;
+  for (size_t s = 0; s < ns; ++s) {
+    tp[s] = ctx->sp[s].totals;
+    cap[s] = ctx->sp[s].cap_out;
+    if ((st = dalloc(ctx, &w.stage[s], 6 * std::max<uint64_t>(1, stage_cap[s]),
+                     "exchange buffer")) != B2M_OK)
+      return st;
+  }
+  B2M_CUDA(ctx, cudaMemcpy(w.totals, tp.data(), ns * sizeof(void*), cudaMemcpyHostToDevice));
+  B2M_CUDA(ctx, cudaMemcpy(w.cap, cap.data(), ns * sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice));
+  B2M_CUDA(ctx, cudaMemset(w.cnt_recv, 0, 2 * ns * sizeof(unsigned long long)));
+  w.on = true;
+  return B2M_OK;
+}
+
+}  // namespace
+
+b2m_status b2m_world_id(void* id) {
+  if (!id) return fail(B2M_INVALID_ARGUMENT, "null id buffer");
+  if (!nccl().ok) return fail(B2M_CONFIG_ERROR, "NCCL unavailable: " + nccl().why);
+  static_assert(sizeof(ncclUniqueId) == B2M_WORLD_ID_BYTES, "NCCL unique id size");
+  const ncclResult_t r = nccl().GetUniqueId(static_cast<ncclUniqueId*>(id));
+  if (r != ncclSuccess) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  return B2M_OK;
+}
+
+b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_init: already initialised");
+  if ((st = b2m_slab_config(ctx, rank, world)) != B2M_OK) return st;
+  const size_t ns = ctx->sp.size();
+  std::vector<uint64_t> cap(ns);
+  for (size_t s = 0; s < ns; ++s) cap[s] = ctx->sp[s].cap_out;
+  if (id) {
+    if (!nccl().ok) return fail(B2M_CONFIG_ERROR, "NCCL unavailable: " + nccl().why);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    B2M_NCCL(ctx, nccl().CommInitRank(&ctx->w.comm, world, uid, rank));
+    // exchange buffers hold the largest outbox any rank can send
+    unsigned long long* d = nullptr;
+    if ((st = dalloc(ctx, &d, std::max<size_t>(1, ns), "world caps")) != B2M_OK) return st;
+    B2M_CUDA(ctx, cudaMemcpy(d, cap.data(), ns * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    B2M_NCCL(ctx, nccl().AllReduce(d, d, ns, ncclUint64, ncclMax, ctx->w.comm, ctx->stream));
+    B2M_CUDA(ctx, cudaMemcpyAsync(cap.data(), d, ns * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  for (auto& c : cap) c *= 2;  // from prev + from next
+  return world_alloc(ctx, cap);
+}
+
+b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_set_total: call b2m_world_init first");
+  long long n = static_cast<long long>(world_local_count(ctx));
+  if (ctx->w.comm) {
+    ctx->w.red_h[0] = n;
+    B2M_CUDA(ctx, cudaMemcpyAsync(ctx->w.red, ctx->w.red_h, sizeof(long long),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    B2M_NCCL(ctx, nccl().AllReduce(ctx->w.red, ctx->w.red, 1, ncclInt64, ncclSum, ctx->w.comm,
+                                ctx->stream));
+    B2M_CUDA(ctx, cudaMemcpyAsync(ctx->w.red_h, ctx->w.red, sizeof(long long),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    n = ctx->w.red_h[0];
+  }
+  ctx->w.total = static_cast<uint64_t>(n);
+  ctx->w.total_set = true;
+  if (total) *total = ctx->w.total;
+  return B2M_OK;
+}
+
+b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
+                          uint64_t* global_count) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_step: call b2m_world_init first");
+  if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
+  const int ns = static_cast<int>(ctx->sp.size());
+  for (int s = 0; s < ns; ++s)
+    if ((st = check_params(&mp[s])) != B2M_OK) return st;
+  auto& w = ctx->w;
+  const int prev = ctx->sl.prev, next = ctx->sl.next;
+  const bool exchange = ctx->sl.world > 1;
+  if (exchange && !w.comm) return fail(B2M_CONFIG_ERROR, "world_step: no NCCL communicator");
+  b2m_status own = world_move(ctx, mp);
+  if (own != B2M_OK && own != B2M_NUMERICAL_FAULT && own != B2M_CFL_VIOLATION) return own;
+  // counts round
+  if (exchange) {
+    B2M_NCCL(ctx, nccl().GroupStart());
+    B2M_NCCL(ctx, nccl().Send(w.cnt_send, ns, ncclUint64, prev, w.comm, ctx->stream));
+    B2M_NCCL(ctx, nccl().Send(w.cnt_send + ns, ns, ncclUint64, next, w.comm, ctx->stream));
+    B2M_NCCL(ctx, nccl().Recv(w.cnt_recv, ns, ncclUint64, prev, w.comm, ctx->stream));
+    B2M_NCCL(ctx, nccl().Recv(w.cnt_recv + ns, ns, ncclUint64, next, w.comm, ctx->stream));
+    B2M_NCCL(ctx, nccl().GroupEnd());
+  }
+  if (own == B2M_OK) own = world_counts(ctx);  // host sync 1
+  else {
+    cudaMemcpyAsync(w.cnt_h, w.cnt_send, 2 * ns * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(w.cnt_h + 2 * ns, w.cnt_recv, 2 * ns * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  const unsigned long long* c = w.cnt_h;  // [to prev][to next][from prev][from next]
+  if (exchange) {
+    B2M_NCCL(ctx, nccl().GroupStart());
+    for (int s = 0; s < ns; ++s)
+      if (c[s])
+        B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[0], 6 * c[s], ncclFloat64,
+                               prev, w.comm, ctx->stream));
+    for (int s = 0; s < ns; ++s)
+      if (c[ns + s])
+        B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[1], 6 * c[ns + s],
+                               ncclFloat64, next, w.comm, ctx->stream));
+    for (int s = 0; s < ns; ++s)
+      if (c[2 * ns + s])
+        B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)], 6 * c[2 * ns + s], ncclFloat64,
+                               prev, w.comm, ctx->stream));
+    for (int s = 0; s < ns; ++s)
+      if (c[3 * ns + s])
+        B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)] + 6 * c[2 * ns + s],
+                               6 * c[3 * ns + s], ncclFloat64, next, w.comm, ctx->stream));
+    B2M_NCCL(ctx, nccl().GroupEnd());
+  }
+  if (sent) *sent = world_sent(ctx);
+  if (own == B2M_OK) own = world_merge(ctx);
+  // count check (runtime.cpp:264-269) with the fault flag riding along
+  w.red_h[0] = own == B2M_OK ? static_cast<long long>(world_local_count(ctx)) : 0;
+  w.red_h[1] = own == B2M_OK ? 0 : 1;
+  if (w.comm) {
+    cudaMemcpyAsync(w.red, w.red_h, 2 * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream);
+    B2M_NCCL(ctx, nccl().AllReduce(w.red, w.red, 2, ncclInt64, ncclSum, w.comm, ctx->stream));
+    cudaMemcpyAsync(w.red_h, w.red, 2 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);  // host sync 2
+  }
+  if (own != B2M_OK && !ctx->poisoned) {  // e.g. an arrival overflowed the batch capacity
+    ctx->poisoned = true;
+    ctx->poison_msg = std::string(b2m_last_error());
+  }
+  return world_verdict(ctx, own, w.red_h[0], own == B2M_OK ? w.red_h[1] : 0, global_count);
+}
+
+b2m_status b2m_world_loopback_step(b2m_ctx* const* ctxs, int world, const b2m_mover_params* mp,
+                                   uint64_t* sent) {
+  if (!ctxs || world < 1 || !mp) return fail(B2M_INVALID_ARGUMENT, "loopback: bad arguments");
+  for (int r = 0; r < world; ++r) {
+    b2m_status st = check_ctx(ctxs[r]);
+    if (st != B2M_OK) return st;
+    if (!ctxs[r]->w.on || ctxs[r]->sl.world != world || ctxs[r]->sl.rank != r)
+      return fail(B2M_CONFIG_ERROR, "loopback: context " + std::to_string(r) +
+                                        " is not rank " + std::to_string(r) + " of " +
+                                        std::to_string(world));
+  }
+  const size_t ns = ctxs[0]->sp.size();
+  std::vector<b2m_status> own(static_cast<size_t>(world), B2M_OK);
+  std::vector<std::string> msg(static_cast<size_t>(world));
+  for (int r = 0; r < world; ++r) {
+    own[static_cast<size_t>(r)] = world_move(ctxs[r], mp);
+    msg[static_cast<size_t>(r)] = b2m_last_error();
+  }
+  for (int r = 0; r < world; ++r) cudaStreamSynchronize(ctxs[r]->stream);
+  // counts: from prev = prev's to-next row, from next = next's to-prev row
+  for (int r = 0; r < world; ++r) {
+    b2m_ctx* me = ctxs[r];
+    const b2m_ctx* p = ctxs[me->sl.prev];
+    const b2m_ctx* n = ctxs[me->sl.next];
+    const size_t b = ns * sizeof(unsigned long long);
+    if (world > 1) {
+      cudaMemcpyAsync(me->w.cnt_recv, p->w.cnt_send + ns, b, cudaMemcpyDeviceToDevice, me->stream);
+      cudaMemcpyAsync(me->w.cnt_recv + ns, n->w.cnt_send, b, cudaMemcpyDeviceToDevice, me->stream);
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    b2m_ctx* me = ctxs[r];
+    if (own[static_cast<size_t>(r)] == B2M_OK) {
+      own[static_cast<size_t>(r)] = world_counts(me);
+      msg[static_cast<size_t>(r)] = b2m_last_error();
+    } else {
+      cudaMemcpyAsync(me->w.cnt_h, me->w.cnt_send, 2 * ns * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost, me->stream);
+      cudaMemcpyAsync(me->w.cnt_h + 2 * ns, me->w.cnt_recv, 2 * ns * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost, me->stream);
+      cudaStreamSynchronize(me->stream);
+    }
+  }
+  // records: into stage[s] = [from prev | from next]
+  uint64_t moved = 0;
+  for (int r = 0; r < world; ++r) {
+    b2m_ctx* me = ctxs[r];
+    moved += world_sent(me);
+    if (world == 1) continue;
+    const b2m_ctx* p = ctxs[me->sl.prev];
+    const b2m_ctx* n = ctxs[me->sl.next];
+    const unsigned long long* c = me->w.cnt_h;
+    for (size_t s = 0; s < ns; ++s) {
+      const size_t rec = 6 * sizeof(double);
+      if (c[2 * ns + s])
+        cudaMemcpyAsync(me->w.stage[s], p->sp[s].out[1], c[2 * ns + s] * rec,
+                        cudaMemcpyDeviceToDevice, me->stream);
+      if (c[3 * ns + s])
+        cudaMemcpyAsync(me->w.stage[s] + 6 * c[2 * ns + s], n->sp[s].out[0], c[3 * ns + s] * rec,
+                        cudaMemcpyDeviceToDevice, me->stream);
+    }
+  }
+  for (int r = 0; r < world; ++r) cudaStreamSynchronize(ctxs[r]->stream);
+  long long total = 0, faulted = 0;
+  for (int r = 0; r < world; ++r) {
+    if (own[static_cast<size_t>(r)] == B2M_OK) {
+      own[static_cast<size_t>(r)] = world_merge(ctxs[r]);
+      msg[static_cast<size_t>(r)] = b2m_last_error();
+    }
+    if (own[static_cast<size_t>(r)] == B2M_OK)
+      total += static_cast<long long>(world_local_count(ctxs[r]));
+    else
+      ++faulted;
+  }
+  if (sent) *sent = moved;
+  for (int r = 0; r < world; ++r)
+    if (own[static_cast<size_t>(r)] != B2M_OK)
+      return fail(own[static_cast<size_t>(r)], msg[static_cast<size_t>(r)]);
+  // the conservation reference: the sum of the ranks' b2m_world_set_total
+  // counts (without a communicator each records its own)
+  uint64_t ref = 0;
+  bool ref_set = true;
+  for (int r = 0; r < world; ++r) {
+    ref += ctxs[r]->w.total;
+    ref_set = ref_set && ctxs[r]->w.total_set;
+  }
+  if (faulted > 0)
+    return fail(B2M_ENGINE_FAULT, "simulation aborted: " + std::to_string(faulted) +
+                                      " rank(s) faulted in this cycle");
+  if (ref_set && static_cast<uint64_t>(total) != ref)
+    return fail(B2M_ENGINE_FAULT, "particle count drifted: " + std::to_string(total) + " vs " +
+                                      std::to_string(ref));
+  return B2M_OK;
+}
+
+}  // extern "C"
