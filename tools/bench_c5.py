@@ -1,4 +1,5 @@
-"""Large-configuration mover measurement: 128x128x64 cells,
+"""Large-configuration mover measurement (or C4 with
+--config c4 --ppc 905): 128x128x64 cells,
 L = (51.2, 25.6, 12.8), 460 ppc -> ~1.0e9 particles (48 GB of SoA) on ONE B200.
 
 The reference GEM state is generated on the host with the bit-exact
@@ -28,8 +29,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--ppc", type=int, default=460)
     ap.add_argument("--chunk", type=int, default=1 << 24)
+    ap.add_argument("--config", choices=["c5", "c4"], default="c5",
+                    help="c4: SURVEY C4's 64x64x32 grid (run with --ppc 905: 255.8M particles)")
     a = ap.parse_args()
-    grid = Grid.make(128, 128, 64, 51.2, 25.6, 12.8)
+    grid = (Grid.make(128, 128, 64, 51.2, 25.6, 12.8) if a.config == "c5"
+            else Grid.make(64, 64, 32, 25.6, 12.8, 6.4))
     counts = gem.gem_counts(grid, a.ppc)
     qom, _ = gem.gem_species_params(grid, a.ppc)
     n_total = sum(counts)
@@ -55,7 +59,9 @@ def main():
     for s in range(4):
         st.sort(s)
     st.sync()
-    out = {"config": "C5 128x128x64, L=(51.2,25.6,12.8), ppc %d" % a.ppc, "particles": n_total,
+    label = ("C5 128x128x64, L=(51.2,25.6,12.8)" if a.config == "c5"
+             else "C4 64x64x32, L=(25.6,12.8,6.4)")
+    out = {"config": "%s, ppc %d" % (label, a.ppc), "particles": n_total,
            "soa_gb": n_total * 48 / 1e9, "init_s": t_init, "runs": []}
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(
         os.path.abspath(__file__))), "MEASURED_PEAKS.json"))).get("hbm_gbs", 6450.3)
