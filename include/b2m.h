@@ -280,6 +280,9 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
 b2m_status b2m_world_id(void* id);
 b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world);
 b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
+/* Replicate the root rank's device field on every rank (ncclBroadcast of E
+ * and B): runtime.cpp:143 gives every worker the whole mesh. */
+b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count);
 /* The same protocol over the `world` contexts of ONE process (rank r =

@@ -34,6 +34,7 @@ const NcclApi& nccl() {
     a.ok = sym(a.GetUniqueId, "ncclGetUniqueId") && sym(a.CommInitRank, "ncclCommInitRank") &&
            sym(a.CommDestroy, "ncclCommDestroy") && sym(a.AllReduce, "ncclAllReduce") &&
            sym(a.Send, "ncclSend") && sym(a.Recv, "ncclRecv") &&
+           sym(a.Broadcast, "ncclBroadcast") &&
            sym(a.GroupStart, "ncclGroupStart") && sym(a.GroupEnd, "ncclGroupEnd") &&
            sym(a.GetErrorString, "ncclGetErrorString");
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
@@ -238,6 +239,27 @@ b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world) {
   }
   for (auto& c : cap) c *= 2;  // from prev + from next
   return world_alloc(ctx, cap);
+}
+
+b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_broadcast_field: call b2m_world_init first");
+  if (root < 0 || root >= ctx->sl.world) return fail(B2M_CONFIG_ERROR, "root rank out of range");
+  if (ctx->sl.rank == root && !ctx->field_ready)
+    return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no field uploaded on the root");
+  if (ctx->w.comm) {
+    const size_t n = 3 * ctx->n_nodes;
+    B2M_NCCL(ctx, nccl().GroupStart());
+    B2M_NCCL(ctx, nccl().Broadcast(ctx->dE, ctx->dE, n, ncclFloat64, root, ctx->w.comm,
+                                   ctx->stream));
+    B2M_NCCL(ctx, nccl().Broadcast(ctx->dB, ctx->dB, n, ncclFloat64, root, ctx->w.comm,
+                                   ctx->stream));
+    B2M_NCCL(ctx, nccl().GroupEnd());
+  }
+  ++ctx->field_gen;  // a new field: FAST tables and the STRICT node table rebuild
+  ctx->field_ready = true;
+  return B2M_OK;
 }
 
 b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total) {

@@ -362,6 +362,10 @@ class NativeSlabWorld:
         else:
             _capi.check(_capi.lib().b2m_world_init(store.h, None, rank, world))
 
+    def broadcast_field(self, root: int = 0) -> None:
+        """Replicate the root rank's device field on every rank (NCCL)."""
+        self._capi.check(self._capi.lib().b2m_world_broadcast_field(self.store.h, root))
+
     def set_total(self) -> int:
         n = C.c_uint64()
         self._capi.check(self._capi.lib().b2m_world_set_total(self.store.h, C.byref(n)))
@@ -473,6 +477,9 @@ def bench_world(args) -> int:
         fB.copy_(torch.from_numpy(field.B.ravel()))
 
     def replicate_field():
+        if native:  # ncclBroadcast of the device field inside the library
+            sw.broadcast_field(0)
+            return
         if backend == "nccl":
             dist.broadcast(fE, 0)
             dist.broadcast(fB, 0)

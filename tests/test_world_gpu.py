@@ -126,6 +126,7 @@ def test_world_of_one_over_nccl_equals_plain_mover(gpu, mode):
     w._capi, w.store, w.ns, w.last_exchange = _capi, a, a.n_species, {}
     total = w.set_total()
     assert total == sum(b.count() for b in batches)
+    w.broadcast_field(0)   # a one-rank broadcast: the field (and its tables) unchanged
     for _ in range(3):
         assert w.step(mps) == 0
         assert w.last_exchange["global_count"] == total
