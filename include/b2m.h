@@ -283,6 +283,10 @@ b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
 /* Replicate the root rank's device field on every rank (ncclBroadcast of E
  * and B): runtime.cpp:143 gives every worker the whole mesh. */
 b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
+/* Sum every rank's moment mesh (b2m_moments_zero + b2m_deposit per rank) into
+ * every rank's mesh, in place (ncclAllReduce): the reference adds the
+ * per-worker meshes (runtime.cpp:251-262). */
+b2m_status b2m_world_reduce_moments(b2m_ctx* ctx);
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count);
 /* The same protocol over the `world` contexts of ONE process (rank r =

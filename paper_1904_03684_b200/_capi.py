@@ -102,6 +102,7 @@ SIGNATURES = {
     "b2m_world_init": (_st, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "b2m_world_set_total": (_st, [C.c_void_p, C.POINTER(_u64)]),
     "b2m_world_broadcast_field": (_st, [C.c_void_p, C.c_int]),
+    "b2m_world_reduce_moments": (_st, [C.c_void_p]),
     "b2m_world_step": (_st, [C.c_void_p, C.POINTER(b2m_mover_params), C.POINTER(_u64),
                              C.POINTER(_u64)]),
     "b2m_world_loopback_step": (_st, [C.POINTER(C.c_void_p), C.c_int,

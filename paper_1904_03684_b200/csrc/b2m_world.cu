@@ -262,6 +262,19 @@ b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
   return B2M_OK;
 }
 
+b2m_status b2m_world_reduce_moments(b2m_ctx* ctx) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_reduce_moments: call b2m_world_init first");
+  double* mesh = nullptr;
+  uint64_t n = 0;
+  if ((st = b2m_moments_device_ptr(ctx, &mesh, &n)) != B2M_OK) return st;
+  if (ctx->w.comm)
+    B2M_NCCL(ctx, nccl().AllReduce(mesh, mesh, n, ncclFloat64, ncclSum, ctx->w.comm,
+                                   ctx->stream));
+  return B2M_OK;
+}
+
 b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total) {
   b2m_status st = check_ctx(ctx);
   if (st != B2M_OK) return st;

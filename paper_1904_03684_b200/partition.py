@@ -362,6 +362,19 @@ class NativeSlabWorld:
         else:
             _capi.check(_capi.lib().b2m_world_init(store.h, None, rank, world))
 
+    def deposit_moments(self, q_per_particle, with_pressure: bool = False):
+        """Moments of every rank's particles summed over the ranks into every
+        rank's device mesh (runtime.cpp:251-262); returns the mesh as a tensor."""
+        st = self.store
+        st.moments_zero(with_pressure)
+        for s in range(self.ns):
+            st.deposit(s, q_per_particle[s])
+        self._capi.check(self._capi.lib().b2m_world_reduce_moments(st.h))
+        st.sync()   # DomainError, as the reference raises it
+        import torch
+        ptr, n = st.moments_device()
+        return torch.as_tensor(_CudaArray(ptr, (n,)), device="cuda")
+
     def broadcast_field(self, root: int = 0) -> None:
         """Replicate the root rank's device field on every rank (NCCL)."""
         self._capi.check(self._capi.lib().b2m_world_broadcast_field(self.store.h, root))

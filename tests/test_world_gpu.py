@@ -133,6 +133,17 @@ def test_world_of_one_over_nccl_equals_plain_mover(gpu, mode):
         b_.move_all(mps)
     for x, y in zip(_download(a), _download(b_)):
         assert_bitwise(x, y, mode)
+    # moments through the world (a one-rank all-reduce) equal the plain deposit
+    qpp = [b.q_per_particle for b in batches]
+    mine = w.deposit_moments(qpp).cpu().numpy().copy()
+    b_.moments_zero(False)
+    for s, q in enumerate(qpp):
+        b_.deposit(s, q)
+    ptr, n = b_.moments_device()
+    from paper_1904_03684_b200.partition import _CudaArray
+    import torch
+    want = torch.as_tensor(_CudaArray(ptr, (n,)), device="cuda").cpu().numpy()
+    np.testing.assert_allclose(mine, want, rtol=0, atol=1e-12 * float(np.max(np.abs(want))))
     a.close()
     b_.close()
 
