@@ -349,8 +349,7 @@ b2m_status b2m_ctx_destroy(b2m_ctx* ctx) {
   for (auto& c : ctx->stub)
     if (c.exec) cudaGraphExecDestroy(c.exec);
   for (void* p : ctx->allocations) cudaFree(p);
-  for (Species& S : ctx->sp)
-    if (S.totals_h) cudaFreeHost(S.totals_h);
+  if (ctx->mig_totals_h) cudaFreeHost(ctx->mig_totals_h);
   if (ctx->w.cnt_h) cudaFreeHost(ctx->w.cnt_h);
   if (ctx->w.red_h) cudaFreeHost(ctx->w.red_h);
   if (ctx->w.comm) nccl().CommDestroy(ctx->w.comm);
@@ -1083,43 +1082,75 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
   range(ctx->sl.prev, ctx->sl.prev_lo, ctx->sl.prev_hi);
   range(ctx->sl.next, ctx->sl.next_lo, ctx->sl.next_hi);
   ctx->slab_on = true;
-  // migration scratch per species
-  for (Species& S : ctx->sp) {
-    if (S.flags) continue;
+  // migration scratch (once per context)
+  if (ctx->mig_tcnt) return B2M_OK;
+  const size_t ns = ctx->sp.size();
+  if (ns > static_cast<size_t>(kMaxCompactSpecies))
+    return fail(B2M_CONFIG_ERROR, "migration: at most " + std::to_string(kMaxCompactSpecies) +
+                                      " species");
+  ctx->mig_tile0.assign(ns, 0);
+  uint64_t tiles = 0;
+  for (size_t s = 0; s < ns; ++s) {
+    ctx->mig_tile0[s] = tiles;
+    tiles += std::max<uint64_t>(1, migrate_tiles(ctx->sp[s].capacity));
+  }
+  if ((st = dalloc(ctx, &ctx->mig_tcnt, tiles, "tile counts")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &ctx->mig_toff, tiles, "tile offsets")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &ctx->mig_totals, 3 * ns, "migration totals")) != B2M_OK) return st;
+  B2M_CUDA(ctx, cudaMemset(ctx->mig_tcnt, 0, tiles * sizeof(unsigned long long)));
+  if (cudaMallocHost(&ctx->mig_totals_h, 3 * ns * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(B2M_ALLOC_ERROR, "pinned migration totals");
+  }
+  std::memset(ctx->mig_totals_h, 0, 3 * ns * sizeof(unsigned long long));
+  for (size_t s = 0; s < ns; ++s) {
+    Species& S = ctx->sp[s];
     const uint64_t cap = S.capacity;
-    const uint64_t nt = std::max<uint64_t>(1, migrate_tiles(cap));
     S.cap_out = std::max<uint64_t>(std::min<uint64_t>(cap, 1u << 16), cap / 8);
     if ((st = dalloc(ctx, &S.flags, cap, "migration flags")) != B2M_OK) return st;
-    if ((st = dalloc(ctx, &S.tcnt, nt, "tile counts")) != B2M_OK) return st;
-    if ((st = dalloc(ctx, &S.toff, nt, "tile offsets")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[0], 6 * S.cap_out, "outbox prev")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[1], 6 * S.cap_out, "outbox next")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.holes, cap, "hole list")) != B2M_OK) return st;
-    if ((st = dalloc(ctx, &S.totals, 3, "migration totals")) != B2M_OK) return st;
-    if (cudaMallocHost(&S.totals_h, 3 * sizeof(unsigned long long)) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(B2M_ALLOC_ERROR, "pinned migration totals");
-    }
-    const size_t need = scan_temp_bytes(nt);
-    if (need > ctx->scan_temp_bytes) {
-      char* tmp = nullptr;
-      if ((st = dalloc(ctx, &tmp, need, "scan temp")) != B2M_OK) return st;
-      ctx->scan_temp = tmp;
-      ctx->scan_temp_bytes = need;
-    }
+    S.tcnt = ctx->mig_tcnt + ctx->mig_tile0[s];
+    S.toff = ctx->mig_toff + ctx->mig_tile0[s];
+    S.totals = ctx->mig_totals + 3 * s;
+    S.totals_h = ctx->mig_totals_h + 3 * s;
+  }
+  const size_t need = scan_temp_bytes(tiles);
+  if (need > ctx->scan_temp_bytes) {
+    char* tmp = nullptr;
+    if ((st = dalloc(ctx, &tmp, need, "scan temp")) != B2M_OK) return st;
+    ctx->scan_temp = tmp;
+    ctx->scan_temp_bytes = need;
   }
   return B2M_OK;
 }
 
-// Migration bookkeeping after the mover wrote species s's flags: per-block
-// counts, scan, outbox scatter, totals to the host.
-static b2m_status migrate_compact(b2m_ctx* ctx, int s, const SpeciesLaunch& L) {
-  Species& S = ctx->sp[static_cast<size_t>(s)];
-  launch_scan_tiles(ctx->scan_temp, ctx->scan_temp_bytes, S.tcnt, S.toff,
-                    migrate_tiles(S.count), S.totals, ctx->stream);
-  launch_scatter_tiles(L, S.flags, S.tcnt, S.toff, S.out[0], S.out[1], S.cap_out, S.holes,
-                       ctx->stream);
-  B2M_CUDA(ctx, cudaMemcpyAsync(S.totals_h, S.totals, 3 * sizeof(unsigned long long),
+// Migration bookkeeping after the mover wrote the flags and tile counts of
+// the given species: one scan over their (side by side) tile counts, every
+// species' totals, the outbox + hole scatter, and one copy of all totals back.
+static b2m_status migrate_compact(b2m_ctx* ctx, const int* species, const SpeciesLaunch* L,
+                                  int n) {
+  CompactSet C{};
+  C.n = n;
+  for (int m = 0; m < n; ++m) {
+    const int s = species[m];
+    Species& S = ctx->sp[static_cast<size_t>(s)];
+    CompactSpecies& c = C.s[m];
+    c.sp = L[m];
+    c.flags = S.flags;
+    c.out_prev = S.out[0];
+    c.out_next = S.out[1];
+    c.cap_out = S.cap_out;
+    c.holes = S.holes;
+    c.totals = S.totals;
+    c.tile0 = ctx->mig_tile0[static_cast<size_t>(s)];
+    c.n_tiles = migrate_tiles(S.count);  // 0 for an empty species: zero totals
+  }
+  launch_compact(C, ctx->scan_temp, ctx->scan_temp_bytes, ctx->mig_tcnt, ctx->mig_toff,
+                 ctx->stream);
+  B2M_CUDA(ctx, cudaMemcpyAsync(ctx->mig_totals_h, ctx->mig_totals,
+                                3 * ctx->sp.size() * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
   return B2M_OK;
 }
@@ -1135,25 +1166,26 @@ b2m_status b2m::move_migrate_species(b2m_ctx* ctx, const int* species,
   if (!ctx->slab_on) return fail(B2M_CONFIG_ERROR, "move_migrate: call b2m_slab_config first");
   if (!ctx->field_ready) return fail(B2M_CONFIG_ERROR, "move: no field uploaded");
   ensure_tables(ctx, species, mp, n);
-  std::vector<SpeciesLaunch> L;
+  std::vector<SpeciesLaunch> L, all;
   std::vector<uint8_t*> fl;
   std::vector<unsigned long long*> tc;
-  std::vector<int> live;
   for (int m = 0; m < n; ++m) {
     const int s = species[m];
     Species& S = ctx->sp[static_cast<size_t>(s)];
     S.pre_count = S.count;
     S.migrate_pending = true;
-    if (S.count == 0) {
-      std::memset(S.totals_h, 0, 3 * sizeof(unsigned long long));
-      continue;
-    }
-    L.push_back(make_launch(ctx, s, mp[m], 0, S.count));
+    all.push_back(make_launch(ctx, s, mp[m], 0, S.count));
+    if (S.count == 0) continue;  // no mover work; its totals come back zero
+    L.push_back(all.back());
     fl.push_back(S.flags);
     tc.push_back(S.tcnt);
-    live.push_back(s);
   }
-  if (L.empty()) return B2M_OK;
+  if (L.empty()) {
+    for (int m = 0; m < n; ++m)
+      std::memset(ctx->sp[static_cast<size_t>(species[m])].totals_h, 0,
+                  3 * sizeof(unsigned long long));
+    return B2M_OK;
+  }
   const int nl = static_cast<int>(L.size());
   const bool ok =
       ctx->mode == B2M_MODE_STRICT
@@ -1163,10 +1195,7 @@ b2m_status b2m::move_migrate_species(b2m_ctx* ctx, const int* species,
           : launch_move_fast(to_fast(ctx->grid), L.data(), nl, ctx->fault, ctx->stream, &ctx->sl,
                              fl.data(), tc.data());
   if (!ok) return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-  for (int m = 0; m < nl; ++m)
-    if ((st = migrate_compact(ctx, live[static_cast<size_t>(m)], L[static_cast<size_t>(m)])) !=
-        B2M_OK)
-      return st;
+  if ((st = migrate_compact(ctx, species, all.data(), n)) != B2M_OK) return st;
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
 }

@@ -128,6 +128,13 @@ struct b2m_ctx {
   // slab partition
   bool slab_on = false;
   b2m::SlabLaunch sl{};
+  // migration: every species' tile counts / offsets side by side (one scan),
+  // their totals in one device block and one pinned block (one copy back)
+  unsigned long long* mig_tcnt = nullptr;
+  unsigned long long* mig_toff = nullptr;
+  unsigned long long* mig_totals = nullptr;
+  unsigned long long* mig_totals_h = nullptr;
+  std::vector<uint64_t> mig_tile0;
   // native slab world (b2m_world_init / b2m_world_step)
   struct World {
     bool on = false;

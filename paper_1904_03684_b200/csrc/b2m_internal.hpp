@@ -102,17 +102,29 @@ struct SlabLaunch {
 // scan: flags[i] (0 stay, 1 prev, 2 next) and, per 128-particle tile t,
 // tcnt[t] = next << 32 | prev.
 uint64_t migrate_tiles(uint64_t n);
-// Exclusive scan of the packed tile counts -> per-tile offsets; totals[3] =
-// prev, next, all leavers.
+// one species of a fused migration compaction (its tile counts start at
+// tile0 of the shared count array)
+constexpr int kMaxCompactSpecies = 16;
+struct CompactSpecies {
+  SpeciesLaunch sp;
+  const uint8_t* flags;
+  double* out_prev;
+  double* out_next;
+  unsigned long long cap_out;
+  unsigned long long* holes;
+  unsigned long long* totals;  // device [3]: prev, next, holes
+  unsigned long long tile0, n_tiles;
+};
+struct CompactSet {
+  CompactSpecies s[kMaxCompactSpecies];
+  int n;
+};
+// scan of the shared tile counts, every species' totals, outbox + hole scatter
+void launch_compact(const CompactSet& C, void* temp, size_t temp_bytes,
+                    const unsigned long long* cnt, unsigned long long* off, cudaStream_t st);
+// CUB temp bytes of the tile-count scan
 size_t scan_temp_bytes(uint64_t n_tiles);
-void launch_scan_tiles(void* temp, size_t temp_bytes, const unsigned long long* cnt,
-                       unsigned long long* off, uint64_t n_tiles, unsigned long long* totals,
-                       cudaStream_t st);
-// Leavers -> outboxes (AoS PartRec, scan order); hole list (ascending).
-void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
-                          const unsigned long long* cnt, const unsigned long long* off,
-                          double* out_prev, double* out_next, uint64_t cap_out,
-                          unsigned long long* holes, cudaStream_t st);
+
 // Fill holes with incoming records, then append / compact the tail.
 void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
                  const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st);

@@ -9,9 +9,10 @@
 //                         trilinear polynomial for the FAST gather
 //   bin_count / bin_scatter   the cell sort (a counting sort by cell; the CUB
 //                         radix sort + gather is the low-memory fallback)
-//   scatter_tiles / fill_*   outbox compaction (scan of the mover's per-tile
+//   compact_* / fill_*       outbox compaction (scan of the mover's per-tile
 //                         counts) and hole filling (merge_incoming,
 //                         runtime.cpp:64-76)
+#include <algorithm>
 #include <cstdlib>
 
 #include <cub/cub.cuh>
@@ -371,74 +372,6 @@ __global__ void gather_kernel(const double* __restrict__ in, const uint32_t* __r
 // scan order.  Tiles without leavers (most of them) return after one load.
 constexpr int kTileParticles = 32 * B2M_FAST_PPT;
 
-__global__ void tile_totals_kernel(const unsigned long long* cnt, const unsigned long long* off,
-                                   unsigned long long n_tiles, unsigned long long* totals) {
-  if (threadIdx.x == 0) {
-    const unsigned long long t = off[n_tiles - 1] + cnt[n_tiles - 1];
-    totals[0] = t & 0xffffffffull;  // prev
-    totals[1] = t >> 32;            // next
-    totals[2] = totals[0] + totals[1];
-  }
-}
-
-__global__ void __launch_bounds__(kTileParticles)
-    scatter_tiles_kernel(const __grid_constant__ SpeciesLaunch sp, const uint8_t* __restrict__ flags,
-                         const unsigned long long* __restrict__ cnt,
-                         const unsigned long long* __restrict__ off, unsigned long long n_tiles,
-                         double* __restrict__ out_prev, double* __restrict__ out_next,
-                         unsigned long long cap_out, unsigned long long* __restrict__ holes) {
-  __shared__ int warp_tot[2][kTileParticles / 32];
-  __shared__ unsigned active[kTileParticles];  // tiles of this group with leavers
-  __shared__ int n_active;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  // grid-stride over groups of kTileParticles tiles: one coalesced load of
-  // the group's counts, then only the tiles with leavers
-  for (unsigned long long g0 = static_cast<unsigned long long>(blockIdx.x) * kTileParticles;
-       g0 < n_tiles; g0 += static_cast<unsigned long long>(gridDim.x) * kTileParticles) {
-    __syncthreads();  // the previous group's list has been consumed
-    if (threadIdx.x == 0) n_active = 0;
-    __syncthreads();
-    const unsigned long long tt = g0 + threadIdx.x;
-    if (tt < n_tiles && cnt[tt] != 0) active[atomicAdd(&n_active, 1)] = threadIdx.x;
-    __syncthreads();
-    const int na = n_active;
-    for (int a = 0; a < na; ++a) {
-      const unsigned long long t = g0 + active[a];
-      const unsigned long long i = t * kTileParticles + threadIdx.x;
-      const int flag = i < sp.n ? flags[i] : 0;
-      const unsigned bp = __ballot_sync(~0u, flag == 1);
-      const unsigned bn = __ballot_sync(~0u, flag == 2);
-      __syncthreads();  // warp_tot of the previous tile has been read
-      if (lane == 0) {
-        warp_tot[0][wid] = __popc(bp);
-        warp_tot[1][wid] = __popc(bn);
-      }
-      __syncthreads();
-      if (flag == 0) continue;
-      int rp = __popc(bp & lt), rn = __popc(bn & lt);
-      for (int w = 0; w < wid; ++w) {
-        rp += warp_tot[0][w];
-        rn += warp_tot[1][w];
-      }
-      const unsigned long long o = off[t];
-      const unsigned long long op = o & 0xffffffffull, on = o >> 32;
-      const unsigned long long hp = op + rp, hn = on + rn;
-      holes[op + on + rp + rn] = i;  // all leavers in index order
-      double* dst = nullptr;
-      if (flag == 1 && hp < cap_out) dst = out_prev + 6 * hp;
-      if (flag == 2 && hn < cap_out) dst = out_next + 6 * hn;
-      if (dst) {
-        double p[6];
-        load6(sp, i, p);
-#pragma unroll
-        for (int a6 = 0; a6 < 6; ++a6) dst[a6] = p[a6];
-      }
-    }
-  }
-}
-
-// Phase A (incoming -> holes / tail append).
 __global__ void fill_in_kernel(const __grid_constant__ SpeciesLaunch sp,
                                const unsigned long long* __restrict__ holes,
                                unsigned long long n_holes, const double* __restrict__ in_recs,
@@ -731,27 +664,109 @@ size_t scan_temp_bytes(uint64_t n_tiles) {
   return bytes;
 }
 
-void launch_scan_tiles(void* temp, size_t temp_bytes, const unsigned long long* cnt,
-                       unsigned long long* off, uint64_t n_tiles, unsigned long long* totals,
-                       cudaStream_t st) {
-  size_t b = temp_bytes;
-  cub::DeviceScan::ExclusiveSum(temp, b, cnt, off, n_tiles, st);
-  note_launch();
-  tile_totals_kernel<<<1, 32, 0, st>>>(cnt, off, n_tiles, totals);
-  note_launch();
+
+
+namespace {
+
+// Fused compaction of several species whose tile counts sit side by side in
+// one array: one scan over all of them, then every species' offsets are taken
+// relative to the scan value at its first tile (unsigned arithmetic, so
+// whatever the tiles before it hold cancels exactly).
+__device__ __forceinline__ int compact_species_of(const CompactSet& C, unsigned long long t) {
+  for (int i = 0; i < C.n; ++i)
+    if (t >= C.s[i].tile0 && t < C.s[i].tile0 + C.s[i].n_tiles) return i;
+  return -1;
 }
 
-void launch_scatter_tiles(const SpeciesLaunch& sp, const uint8_t* flags,
-                          const unsigned long long* cnt, const unsigned long long* off,
-                          double* out_prev, double* out_next, uint64_t cap_out,
-                          unsigned long long* holes, cudaStream_t st) {
-  const uint64_t nt = migrate_tiles(sp.n);
-  if (nt == 0) return;
-  const uint64_t groups = (nt + kTileParticles - 1) / kTileParticles;
+__global__ void compact_totals_kernel(const __grid_constant__ CompactSet C,
+                                      const unsigned long long* __restrict__ cnt,
+                                      const unsigned long long* __restrict__ off) {
+  const int i = threadIdx.x;
+  if (i >= C.n) return;
+  const CompactSpecies& c = C.s[i];
+  unsigned long long t = 0;
+  if (c.n_tiles) {
+    const unsigned long long last = c.tile0 + c.n_tiles - 1;
+    t = off[last] + cnt[last] - off[c.tile0];
+  }
+  c.totals[0] = t & 0xffffffffull;  // prev
+  c.totals[1] = t >> 32;            // next
+  c.totals[2] = c.totals[0] + c.totals[1];
+}
+
+__global__ void __launch_bounds__(kTileParticles)
+    compact_scatter_kernel(const __grid_constant__ CompactSet C,
+                           const unsigned long long* __restrict__ cnt,
+                           const unsigned long long* __restrict__ off, unsigned long long t_end) {
+  __shared__ int warp_tot[2][kTileParticles / 32];
+  __shared__ unsigned active[kTileParticles];
+  __shared__ int n_active;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (unsigned long long g0 = static_cast<unsigned long long>(blockIdx.x) * kTileParticles;
+       g0 < t_end; g0 += static_cast<unsigned long long>(gridDim.x) * kTileParticles) {
+    __syncthreads();
+    if (threadIdx.x == 0) n_active = 0;
+    __syncthreads();
+    const unsigned long long tt = g0 + threadIdx.x;
+    if (tt < t_end && compact_species_of(C, tt) >= 0 && cnt[tt] != 0)
+      active[atomicAdd(&n_active, 1)] = threadIdx.x;
+    __syncthreads();
+    const int na = n_active;
+    for (int a = 0; a < na; ++a) {
+      const unsigned long long t = g0 + active[a];
+      const CompactSpecies& c = C.s[compact_species_of(C, t)];
+      const unsigned long long i = (t - c.tile0) * kTileParticles + threadIdx.x;
+      const int flag = i < c.sp.n ? c.flags[i] : 0;
+      const unsigned bp = __ballot_sync(~0u, flag == 1);
+      const unsigned bn = __ballot_sync(~0u, flag == 2);
+      __syncthreads();
+      if (lane == 0) {
+        warp_tot[0][wid] = __popc(bp);
+        warp_tot[1][wid] = __popc(bn);
+      }
+      __syncthreads();
+      if (flag == 0) continue;
+      int rp = __popc(bp & lt), rn = __popc(bn & lt);
+      for (int w = 0; w < wid; ++w) {
+        rp += warp_tot[0][w];
+        rn += warp_tot[1][w];
+      }
+      const unsigned long long o = off[t] - off[c.tile0];
+      const unsigned long long op = o & 0xffffffffull, on = o >> 32;
+      const unsigned long long hp = op + rp, hn = on + rn;
+      c.holes[op + on + rp + rn] = i;  // all leavers in index order
+      double* dst = nullptr;
+      if (flag == 1 && hp < c.cap_out) dst = c.out_prev + 6 * hp;
+      if (flag == 2 && hn < c.cap_out) dst = c.out_next + 6 * hn;
+      if (dst) {
+        double p[6];
+        load6(c.sp, i, p);
+#pragma unroll
+        for (int a6 = 0; a6 < 6; ++a6) dst[a6] = p[a6];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_compact(const CompactSet& C, void* temp, size_t temp_bytes,
+                    const unsigned long long* cnt, unsigned long long* off, cudaStream_t st) {
+  unsigned long long t_end = 0;
+  for (int i = 0; i < C.n; ++i) t_end = std::max(t_end, C.s[i].tile0 + C.s[i].n_tiles);
+  if (t_end > 0) {
+    size_t b = temp_bytes;
+    cub::DeviceScan::ExclusiveSum(temp, b, cnt, off, t_end, st);
+    note_launch();
+  }
+  compact_totals_kernel<<<1, 32, 0, st>>>(C, cnt, off);
+  note_launch();
+  if (t_end == 0) return;
+  const uint64_t groups = (t_end + kTileParticles - 1) / kTileParticles;
   const uint64_t cap = static_cast<uint64_t>(device_sms()) * 16;
-  scatter_tiles_kernel<<<static_cast<unsigned>(groups < cap ? groups : cap), kTileParticles, 0,
-                         st>>>(
-      sp, flags, cnt, off, nt, out_prev, out_next, cap_out, holes);
+  compact_scatter_kernel<<<static_cast<unsigned>(groups < cap ? groups : cap), kTileParticles, 0,
+                           st>>>(C, cnt, off, t_end);
   note_launch();
 }
 
