@@ -202,3 +202,31 @@ def test_loopback_four_ranks_equal_one_context_after_many_steps(gpu):
         np.testing.assert_array_equal(oracle.multiset(mine), oracle.multiset(want[s]))
     for st in stores + [ref]:
         st.close()
+
+
+def test_loopback_with_an_empty_species(gpu):
+    """A species with no particles on any rank rides through the protocol
+    (zero counts, zero totals) while the others migrate; counts conserved."""
+    g = Grid.make(*GRID_T)
+    world = 2
+    stores = []
+    for r in range(world):
+        batches = gem.init_gem_slab(g, 8, r, world, pinned=False)
+        st = DeviceStore(g, [b.count() + 4096 for b in batches], "fast")
+        st.upload_field(gem.gem_field(g))
+        for s, b in enumerate(batches):
+            if s != 2:   # species 2 (the electron sheet) left empty everywhere
+                st.upload(s, b.span())
+        stores.append(st)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    loopback_world(stores, g)
+    total0 = sum(st.count(s) for st in stores for s in range(4))
+    for _ in range(4):
+        loopback_step(stores, mps)
+    assert sum(st.count(2) for st in stores) == 0
+    assert sum(st.count(s) for st in stores for s in range(4)) == total0
+    for r, st in enumerate(stores):
+        for s in range(4):
+            y = _download(st)[s][1]
+            assert np.all(owner_of(y, g, world) == r)
+        st.close()
