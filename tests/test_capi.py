@@ -92,3 +92,19 @@ def test_compute_without_gpu_fails_loudly(built):
     p = [np.ones(4) for _ in range(6)]
     with pytest.raises(MinipicError):
         move_batch(p, (E, B), g, MoverParams.make(0.1, 1.0, 3))
+
+
+def test_world_entry_points_validate_before_touching_a_gpu(built):
+    """The native world's argument checks (no GPU needed): null id buffer,
+    null / non-world contexts, bad loopback arguments."""
+    lib = _capi.lib()
+    INVALID = 9  # B2M_INVALID_ARGUMENT
+    assert lib.b2m_world_id(None) == INVALID
+    arr = (_capi.b2m_mover_params * 1)(MoverParams.make(0.1, 1.0, 3).to_c())
+    assert lib.b2m_world_step(None, arr, None, None) == INVALID
+    assert lib.b2m_world_init(None, None, 0, 1) == INVALID
+    assert lib.b2m_world_set_total(None, None) == INVALID
+    assert lib.b2m_world_broadcast_field(None, 0) == INVALID
+    assert lib.b2m_world_reduce_moments(None) == INVALID
+    assert lib.b2m_world_loopback_step(None, 2, arr, None) == INVALID
+    assert "null" in _capi.last_error() or "bad arguments" in _capi.last_error()
