@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -739,7 +740,9 @@ b2m_status b2m_sort_species(b2m_ctx* ctx, int s) {
       for (int a = 0; a < 6; ++a) S.alt[a] = blk + a * S.stride;
     }
   }
-  if (S.alt[0]) {
+  // B2M_SORT_FALLBACK=1 forces the low-memory path below (tests)
+  const char* fb = std::getenv("B2M_SORT_FALLBACK");
+  if (S.alt[0] && !(fb && fb[0] == '1')) {
     // counting sort straight into the ping-pong set, then swap
     if (n > ctx->bin_keys_cap) {
       if (ctx->bin_keys) {

@@ -193,8 +193,13 @@ def test_uniform_field_pc_fixed_point(gpu, mode):
     check(b, port_move(p0, E, B, grid, 0.1, -25.0, 3), grid, mode, "pc3")
 
 
+@pytest.mark.parametrize("path", ["counting", "radix_fallback"])
 @pytest.mark.parametrize("mode", MODES)
-def test_device_store_sort_preserves_multiset(gpu, mode):
+def test_device_store_sort_preserves_multiset(gpu, mode, path, monkeypatch):
+    """Both cell sorts: the counting sort into the ping-pong set, and the
+    low-memory radix sort + gather used when no second set fits."""
+    if path == "radix_fallback":
+        monkeypatch.setenv("B2M_SORT_FALLBACK", "1")
     g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
     grid = g.as_tuple()
     p0 = random_particles(grid, 100000, 21)
