@@ -108,3 +108,20 @@ def test_world_entry_points_validate_before_touching_a_gpu(built):
     assert lib.b2m_world_reduce_moments(None) == INVALID
     assert lib.b2m_world_loopback_step(None, 2, arr, None) == INVALID
     assert "null" in _capi.last_error() or "bad arguments" in _capi.last_error()
+
+
+def test_integration_world_example_compiles(built, tmp_path):
+    """INTEGRATION.md's native-world cycle compiles against include/b2m.h and
+    links against libb2m.so (compile only: running it needs GPUs)."""
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if not gxx:
+        pytest.skip("no g++")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = tmp_path / "libexample.so"
+    r = subprocess.run([gxx, "-std=c++17", "-fPIC", "-shared", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "integration", "world_example.cpp"), "-o", str(so),
+                        "-L", os.path.dirname(_capi.LIB_PATH), "-lb2m"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
