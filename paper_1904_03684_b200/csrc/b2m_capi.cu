@@ -177,7 +177,7 @@ void ensure_tables(b2m_ctx* ctx, const int* species, const b2m_mover_params* mp,
   if (!tables.empty())
     launch_field_to_cells(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
                           scale.data(), tables.data(), static_cast<int>(tables.size()),
-                          ctx->stream);
+                          ctx->stream, ctx->zvar);
 }
 
 b2m_status check_params(const b2m_mover_params* mp) {
@@ -319,6 +319,11 @@ b2m_status b2m_ctx_create(int device, const b2m_grid* g, int n_species, const ui
   if ((st = dalloc(ctx, &ctx->strict_nodes, 48 * ncell, "strict node table")) != B2M_OK)
     return bail(st);
   if ((st = dalloc(ctx, &ctx->fault, 1, "fault word")) != B2M_OK) return bail(st);
+  {
+    const char* e3 = std::getenv("B2M_FAST_3D");  // diagnostics: general kernel only
+    if (!(e3 && e3[0] == '1') && (st = dalloc(ctx, &ctx->zvar, 1, "z flag")) != B2M_OK)
+      return bail(st);
+  }
   if (cudaMallocHost(&ctx->fault_h, sizeof(FaultWord)) != cudaSuccess) {
     cudaGetLastError();
     return bail(fail(B2M_ALLOC_ERROR, "pinned fault word"));
@@ -618,7 +623,8 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
     if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-  } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream)) {
+  } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, nullptr,
+                                      nullptr, nullptr, ctx->zvar)) {
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   }
   B2M_CUDA(ctx, cudaGetLastError());
@@ -651,8 +657,8 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
     if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), L.data(), ns, ctx->fault,
                                   ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-  } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault,
-                             ctx->stream))
+  } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault, ctx->stream,
+                               nullptr, nullptr, nullptr, ctx->zvar))
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaGetLastError());
   return B2M_OK;
@@ -708,7 +714,8 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
         if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
                                       ctx->stream))
           return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
-      } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream))
+      } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, nullptr,
+                                      nullptr, nullptr, ctx->zvar))
         return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       B2M_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], ctx->stream));
       B2M_CUDA(ctx, cudaStreamWaitEvent(ctx->down, ev[2 * c + 1], 0));
@@ -1196,7 +1203,7 @@ b2m_status b2m::move_migrate_species(b2m_ctx* ctx, const int* species,
                                      L.data(), nl, ctx->fault, ctx->stream, &ctx->sl, fl.data(),
                                      tc.data())
           : launch_move_fast(to_fast(ctx->grid), L.data(), nl, ctx->fault, ctx->stream, &ctx->sl,
-                             fl.data(), tc.data());
+                             fl.data(), tc.data(), ctx->zvar);
   if (!ok) return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   if ((st = migrate_compact(ctx, species, all.data(), n)) != B2M_OK) return st;
   B2M_CUDA(ctx, cudaGetLastError());

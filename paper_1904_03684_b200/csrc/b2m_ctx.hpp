@@ -91,6 +91,9 @@ struct b2m_ctx {
     double* out = nullptr;
   } stub[2];
   double* strict_nodes = nullptr;  // STRICT per-cell corner node table
+  // FAST: device flag, 0 when the field is z-invariant (set with every table
+  // build); null when the z-invariant kernel is disabled (B2M_FAST_3D=1)
+  int* zvar = nullptr;
   uint64_t strict_gen = 0;
   double* dB = nullptr;
   bool field_ready = false;

@@ -35,7 +35,7 @@ struct SlabLaunch;
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st,
                       const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr,
-                      unsigned long long* const* tcnt = nullptr);
+                      unsigned long long* const* tcnt = nullptr, const int* zvar = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
@@ -49,9 +49,13 @@ void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* 
 // scale[m]*B) into tables[m] (48 doubles per cell), one field read per
 // kMaxTables tables.
 constexpr int kMaxTables = 8;
+// With `zvar` (device int): first set it to 0 when the field is z-invariant
+// (every node plane k equal to plane 0 bit for bit), else 1; when 0, the tables
+// are written in the column layout of the z-invariant kernel (nx*ny columns
+// of 24 doubles: per component p0..p3 of the bilinear polynomial).
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
                            const double* scale, double2* const* tables, int n_tables,
-                           cudaStream_t st);
+                           cudaStream_t st, int* zvar = nullptr);
 // Moment deposition (b2m_moments.cu, deposit_moments kernels.cpp:147-183) of
 // one species span, qv = q_per_particle / cell volume, accumulated into
 // mesh[0..3] = rho, jx, jy, jz (+ mesh[4..9] = pxx..pzz with pressure).

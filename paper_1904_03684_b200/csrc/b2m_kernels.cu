@@ -54,20 +54,25 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
 #ifndef B2M_ABL_STREAM_ONLY
 #define B2M_ABL_STREAM_ONLY 0
 #endif
+#ifndef B2M_FAST_V
+#define B2M_FAST_V 2   // FAST body: 2 = cached-cell frame (fast_particle_v2), 1 = round-1 kernel
+#endif
 #ifndef B2M_J_UNROLL
 #define B2M_J_UNROLL 1
 #endif
 constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
-#ifdef B2M_MAXNREG
-#define B2M_WARP_BOUNDS __maxnreg__(B2M_MAXNREG)
-#else
-#define B2M_WARP_BOUNDS __launch_bounds__(kWarpThreads, B2M_FAST_MINBLOCKS)
+#ifndef B2M_2D_MINBLOCKS
+#define B2M_2D_MINBLOCKS 4     // z-invariant FAST kernel: 24-double column cache
 #endif
-template <int P, bool STRICT>
-__global__ void B2M_WARP_BOUNDS
+// DIM: 3 = general FAST (or STRICT), 2 = z-invariant FAST.  The two FAST
+// kernels are launched back to back; each reads the field's z-invariance
+// flag (zinv_check_kernel) and the one that does not apply exits at once.
+template <int P, bool STRICT, int DIM>
+__global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2M_FAST_MINBLOCKS)
     warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
                      const __grid_constant__ SlabLaunch sl, unsigned long long total_tiles,
                      FaultWord* fault) {
+  if (!STRICT && F.zvar && ((*F.zvar == 0) != (DIM == 2))) return;
   constexpr int WT = 32 * P;
   constexpr int WARPS = kWarpThreads / 32;
   extern __shared__ __align__(128) unsigned char wt_smem[];
@@ -146,6 +151,60 @@ __global__ void B2M_WARP_BOUNDS
     } else if (B2M_ABL_STREAM_ONLY) {
       // ablation: the tile pipeline without the mover arithmetic
       if (lane < cnt) buf[st][0][lane] += 0.0;
+    } else if (DIM == 2) {
+      // z-invariant field (b2m_tile.cuh): bilinear column gather
+      FastCol C;
+      fast_col_reset(C);
+      uint8_t* flags = S.flags[s];
+      const double* cols = reinterpret_cast<const double*>(sp.cells);
+#pragma unroll 1
+      for (int j = 0; j < P; ++j) {
+        const int p = lane + 32 * j;
+        const unsigned bad =
+            F.U.rounds == 3 ? fast_particle_2d<WT, 3>(F.fg, F.U, cols, buf[st], p, cnt, C)
+                            : fast_particle_2d<WT, 0>(F.fg, F.U, cols, buf[st], p, cnt, C);
+        if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (flags && p < cnt) {
+          int flag = 0;
+          if (!bad) {
+            flag = slab_flag(buf[st][1][p], sl);
+            if (flag == 3) {
+              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+              flag = 0;
+            }
+          }
+          flags[off + p] = static_cast<uint8_t>(flag);
+          n_prev += flag == 1;
+          n_next += flag == 2;
+        }
+      }
+    } else if (B2M_FAST_V == 2) {
+      // FAST v2 (b2m_tile.cuh): fractions relative to the lane's cached cell
+      FastCell C;
+      fast_cell_reset(C);
+      uint8_t* flags = S.flags[s];
+      const double2* cells = sp.cells;
+#pragma unroll 1
+      for (int j = 0; j < P; ++j) {
+        const int p = lane + 32 * j;
+        const unsigned bad =
+            F.U.rounds == 3 ? fast_particle_v2<WT, 3>(F.fg, F.U, cells, buf[st], p, cnt, C)
+                            : fast_particle_v2<WT, 0>(F.fg, F.U, cells, buf[st], p, cnt, C);
+        if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (flags && p < cnt) {
+          int flag = 0;
+          if (!bad) {
+            flag = slab_flag(buf[st][1][p], sl);
+            if (flag == 3) {
+              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+              flag = 0;
+            }
+          }
+          flags[off + p] = static_cast<uint8_t>(flag);
+          n_prev += flag == 1;
+          n_next += flag == 2;
+        }
+      }
     } else {
       const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
@@ -245,9 +304,22 @@ struct CellTables {
   int n;
 };
 
+// Is the field z-invariant: every node plane k >= 1 of E and B equal to plane
+// 0 bit for bit?  *flag must be 0 on entry; any difference sets it.
+__global__ void zinv_check_kernel(long long plane, long long nodes, const double* __restrict__ E,
+                                  const double* __restrict__ B, int* flag) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= 3 * (nodes - plane)) return;
+  const long long a = 3 * plane + t, b = t % (3 * plane);
+  const bool same = __double_as_longlong(E[a]) == __double_as_longlong(E[b]) &&
+                    __double_as_longlong(B[a]) == __double_as_longlong(B[b]);
+  if (!same) *flag = 1;
+}
+
 __global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __restrict__ E,
                                       const double* __restrict__ B,
-                                      const __grid_constant__ CellTables T) {
+                                      const __grid_constant__ CellTables T,
+                                      const int* __restrict__ zvar) {
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long ncell = static_cast<long long>(nx) * ny * nz;
   if (t >= 6 * ncell) return;
@@ -256,6 +328,24 @@ __global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __re
   const int i = static_cast<int>(cell % nx);
   const int j = static_cast<int>((cell / nx) % ny);
   const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
+  if (zvar && *zvar == 0) {
+    // z-invariant: the bilinear column polynomial of plane k = 0 (the same
+    // P values as the 3-D table below, whose Q are all exactly zero)
+    if (k != 0) return;
+    const long long sx = nx + 1;
+    const double* F = (q < 3 ? E : B) + q % 3;
+    const double f00 = __ldg(F + 3 * (i + sx * j)), f10 = __ldg(F + 3 * (i + 1 + sx * j));
+    const double f01 = __ldg(F + 3 * (i + sx * (j + 1))),
+                 f11 = __ldg(F + 3 * (i + 1 + sx * (j + 1)));
+    for (int m = 0; m < T.n; ++m) {
+      const double c = T.scale[m];
+      const double g00 = c * f00, g10 = c * f10, g01 = c * f01, g11 = c * f11;
+      double* out = reinterpret_cast<double*>(T.out[m]) + cell * 24 + 4 * q;
+      reinterpret_cast<double4*>(out)[0] =
+          make_double4(g00, g01 - g00, g10 - g00, (g11 - g10) - (g01 - g00));
+    }
+    return;
+  }
   const long long sx = nx + 1, sy = ny + 1;
   const double* F = (q < 3 ? E : B) + q % 3;
   auto f = [&](int di, int dj, int dk) {
@@ -468,7 +558,7 @@ bool encode_species_map(CUtensorMap* map, const SpeciesLaunch& sp, int box_cols)
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool STRICT>
+template <bool STRICT, int DIM>
 bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                        cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
                        unsigned long long* const* tcnt) {
@@ -482,9 +572,9 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(warp_tile_kernel<P, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT>,
+    cudaFuncSetAttribute(warp_tile_kernel<P, STRICT, DIM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT, DIM>,
                                                   kWarpThreads, smem);
     int cap = sms * (per_sm > 0 ? per_sm : 1);
     // diagnostics: B2M_BLOCKS_PER_SM=k runs the persistent grid with k blocks per SM
@@ -494,10 +584,24 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     }
     return cap;
   }();
-  for (int base = 0; base < n_spans; base += kMaxTileSpans) {
+  // FAST launches share dt / pc_iterations across their spans (FastUniform):
+  // a batch whose species differ there is launched in runs of equal values
+  auto same_uniform = [&](int a, int b) {
+    return sp[a].dt == sp[b].dt && sp[a].rounds == sp[b].rounds &&
+           sp[a].dto2_cell[0] == sp[b].dto2_cell[0] && sp[a].dto2_cell[1] == sp[b].dto2_cell[1] &&
+           sp[a].dto2_cell[2] == sp[b].dto2_cell[2];
+  };
+  for (int base = 0; base < n_spans;) {
     TensorSpans S{};
     unsigned long long tiles = 0;
-    for (int s = base; s < n_spans && S.n < kMaxTileSpans; ++s) {
+    TileField FL = F;
+    FL.U.dt = sp[base].dt;
+    FL.U.dc[0] = sp[base].dto2_cell[0];
+    FL.U.dc[1] = sp[base].dto2_cell[1];
+    FL.U.dc[2] = sp[base].dto2_cell[2];
+    FL.U.rounds = sp[base].rounds;
+    int s = base;
+    for (; s < n_spans && S.n < kMaxTileSpans && (STRICT || same_uniform(base, s)); ++s) {
       if (sp[s].n == 0) continue;
       if (sp[s].col0 + sp[s].n > 0x7fffffffull) return false;  // 32-bit TMA coordinates
       S.sp[S.n] = sp[s];
@@ -508,12 +612,13 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
       tiles += (sp[s].n + WT - 1) / WT;
       ++S.n;
     }
+    base = s;
     S.tile_start[S.n] = tiles;
     if (S.n == 0) continue;
     constexpr unsigned long long WPB = kWarpThreads / 32;
     const unsigned long long blocks = (tiles + WPB - 1) / WPB;
     const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
-    warp_tile_kernel<P, STRICT><<<grid, kWarpThreads, smem, st>>>(F, S, sl ? *sl : SlabLaunch{},
+    warp_tile_kernel<P, STRICT, DIM><<<grid, kWarpThreads, smem, st>>>(FL, S, sl ? *sl : SlabLaunch{},
                                                                    tiles, fault);
     note_launch();
   }
@@ -522,10 +627,15 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
 
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                       cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
-                      unsigned long long* const* tcnt) {
+                      unsigned long long* const* tcnt, const int* zvar) {
   TileField F{};
   F.fg = g;
-  return launch_warp_tiles<false>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+  F.zvar = zvar;
+  // both FAST kernels; the one the field's z-invariance flag rules out exits
+  // at its first instruction (no host round trip to decide)
+  if (zvar && !launch_warp_tiles<false, 2>(F, sp, n_spans, fault, st, sl, flags, tcnt))
+    return false;
+  return launch_warp_tiles<false, 3>(F, sp, n_spans, fault, st, sl, flags, tcnt);
 }
 
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
@@ -536,7 +646,7 @@ bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double
   F.dg = g;
   F.fg = fg;  // wrap thresholds (WrapAxis)
   F.nodes = nodes;
-  return launch_warp_tiles<true>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+  return launch_warp_tiles<true, 3>(F, sp, n_spans, fault, st, sl, flags, tcnt);
 }
 
 void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* B, double* out,
@@ -548,15 +658,22 @@ void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* 
 
 void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double* B,
                            const double* scale, double2* const* tables, int n_tables,
-                           cudaStream_t st) {
+                           cudaStream_t st, int* zvar) {
   const long long ncell = static_cast<long long>(nx) * ny * nz;
+  if (zvar) {
+    const long long plane = static_cast<long long>(nx + 1) * (ny + 1);
+    const long long nodes = plane * (nz + 1);
+    cudaMemsetAsync(zvar, 0, sizeof(int), st);
+    zinv_check_kernel<<<grid_for(3 * (nodes - plane), 256), 256, 0, st>>>(plane, nodes, E, B, zvar);
+    note_launch();
+  }
   for (int base = 0; base < n_tables; base += kMaxTables) {
     CellTables T{};
     for (T.n = 0; T.n < kMaxTables && base + T.n < n_tables; ++T.n) {
       T.out[T.n] = tables[base + T.n];
       T.scale[T.n] = scale[base + T.n];
     }
-    field_to_cells_kernel<<<grid_for(6 * ncell, 192), 192, 0, st>>>(nx, ny, nz, E, B, T);
+    field_to_cells_kernel<<<grid_for(6 * ncell, 192), 192, 0, st>>>(nx, ny, nz, E, B, T, zvar);
     note_launch();
   }
 }

@@ -26,7 +26,7 @@ namespace b2m {
 #define B2M_TPB 128            // threads per block of the warp-tile kernel
 #endif
 #ifndef B2M_WARP_STAGES
-#define B2M_WARP_STAGES 3      // TMA ring depth per warp
+#define B2M_WARP_STAGES 2      // TMA ring depth per warp (2: larger L1, profiles/README.md)
 #endif
 #ifndef B2M_FAST_PPT
 #define B2M_FAST_PPT 4         // particles per lane per tile (sequential)
@@ -123,10 +123,21 @@ __device__ __forceinline__ void fence_proxy_async() {
 // launch parameters
 // ---------------------------------------------------------------------------
 
+// FAST: the per-launch scalars every span of the launch shares (the launcher
+// splits a batch whose spans differ), so the hot loop reads them as
+// constant-bank operands instead of per-species registers.
+struct FastUniform {
+  double dt;          // MoverParams::dt
+  double dc[3];       // 0.5*dt/d per axis: cell-unit predictor step
+  int rounds;         // pc_iterations
+};
+
 struct TileField {
   FastGrid fg;
   DevGrid dg;
   const double* nodes;   // STRICT: per-cell corner node values (strict_nodes_kernel)
+  FastUniform U;
+  const int* zvar;       // FAST: device flag, 0 = field z-invariant (null: general kernel only)
 };
 
 // FAST launch: per span a 2-D tensor map over the species' [6][stride]
@@ -372,6 +383,330 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
   }
   return p < cnt ? 1u : 0u;
 }
+// ---------------------------------------------------------------------------
+// FAST v2: fractions relative to the cached cell
+// ---------------------------------------------------------------------------
+//
+// The lane's cache also holds its cell's integer corner (ci, cj, ck) as
+// doubles.  A particle's fractions are taken relative to that corner --
+// f0 = x0/d - c at the start, f = f0 + vbar*dt/(2d) for a predictor -- and
+// when all three lie in [+0, 1) (one integer compare of the high word each)
+// the position is inside the cached cell: no truncation, no conversions, no
+// periodic fold, no reload.  Only a lane that left the cell (a few % of
+// rounds) takes the slow path: fold, locate, reload.  The trilinear field is
+// continuous across faces and seams, so which of two touching cells a
+// boundary position is evaluated in only changes rounding.
+
+#ifndef B2M_V2_R1_LOCATE
+#define B2M_V2_R1_LOCATE 0  // 1: every particle's start is located (no frame test)
+#endif
+
+// f in [+0, 1): the high word of +0..1-ulp is below that of 1.0; negatives
+// (sign bit), -0, NaN and everything >= 1 are not
+__device__ __forceinline__ bool in_unit(double f) {
+  return static_cast<unsigned>(__double2hiint(f)) < 0x3ff00000u;
+}
+
+// x in [+0, l): the fast-path form of in_range (-0 takes the slow path)
+__device__ __forceinline__ bool below_bits(double x, unsigned long long lbits) {
+  return dbits(x) < lbits;
+}
+
+// a shared-memory load the compiler cannot merge with an earlier one (so the
+// value need not stay live in a register in between)
+__device__ __forceinline__ double lds_f64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
+// High word of a double through an opaque move, so that exponent tests stay
+// integer ALU work (the compiler turns a visible bit test into DSETP, FP64 pipe)
+__device__ __forceinline__ unsigned hi_word(double x) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  return hi;
+}
+
+// all three finite: no exponent field all ones
+__device__ __forceinline__ bool finite3(double a, double b, double c) {
+  constexpr unsigned kE = 0x7ff00000u;
+  const unsigned m = max(max(hi_word(a) & kE, hi_word(b) & kE), hi_word(c) & kE);
+  return m != kE;
+}
+
+struct FastCell {
+  Coef8 K[6];
+  double ci, cj, ck;  // the cached cell's corner in cell units
+  int cell;
+};
+
+__device__ __forceinline__ void fast_cell_reset(FastCell& C) {
+  C.cell = -1;
+  C.ci = C.cj = C.ck = -4.0;  // no fraction relative to it is in [0, 1)
+}
+
+// Locate a folded cell-unit position (indices clamped: a flagged NaN reads a
+// valid cell), load its coefficients when it is not the cached cell, and
+// return the fractions relative to it.
+__device__ __forceinline__ void fast_enter(const FastGrid& g, const double2* __restrict__ cells,
+                                           FastCell& C, double tx, double ty, double tz,
+                                           double& fx, double& fy, double& fz) {
+  const int i = max(min(__double2int_rz(tx), g.nx - 1), 0);
+  const int j = max(min(__double2int_rz(ty), g.ny - 1), 0);
+  const int m = max(min(__double2int_rz(tz), g.nz - 1), 0);
+  const double di = static_cast<double>(i), dj = static_cast<double>(j),
+               dk = static_cast<double>(m);
+  fx = tx - di;
+  fy = ty - dj;
+  fz = tz - dk;
+  const int cell = i + g.nx * (j + g.ny * m);
+  if (cell != C.cell) {
+    const double2* c = cells + static_cast<long long>(cell) * 24;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) C.K[q] = load_coef8(c + 4 * q);
+    C.cell = cell;
+  }
+  C.ci = di;
+  C.cj = dj;
+  C.ck = dk;
+}
+
+// Implicit velocity (kernels.cpp:83-90) up to its last product: returns the
+// numerator (vt + vt x W + (vt.W) W) and rc = 1/(1 + |W|^2), vbar = num*rc.
+__device__ __forceinline__ void implicit_num(double u0, double v0, double w0, const double* F,
+                                             double& nx, double& ny, double& nz, double& rc) {
+  const double ox = F[3], oy = F[4], oz = F[5];
+  const double vtx = u0 + F[0];
+  const double vty = v0 + F[1];
+  const double vtz = w0 + F[2];
+  const double den = fma(oz, oz, fma(oy, oy, fma(ox, ox, 1.0)));
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+  const double e = fma(-den, r, 1.0);
+  rc = fma(r, fma(e, e, e), r);  // r * (1 + e + e^2)
+  const double vdot = fma(vtz, oz, fma(vty, oy, vtx * ox));
+  nx = fma(vdot, ox, fma(vty, oz, fma(-vtz, oy, vtx)));
+  ny = fma(vdot, oy, fma(vtz, ox, fma(-vtx, oz, vty)));
+  nz = fma(vdot, oz, fma(vtx, oy, fma(-vty, ox, vtz)));
+}
+
+// One FAST particle (kernels.cpp:52-104 in FMA form).  buf[a][p] holds input
+// a of particle p and receives its result when it finishes clean; returns 1
+// for a particle to report as faulted.
+template <int TILE, int ROUNDS>
+__device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const FastUniform& U,
+                                                     const double2* __restrict__ cells,
+                                                     double (*buf)[TILE], int p, int cnt,
+                                                     FastCell& C) {
+  const double x0 = buf[0][p], y0 = buf[1][p], z0 = buf[2][p];
+  const double u0 = buf[3][p], v0 = buf[4][p], w0 = buf[5][p];
+  double fx0, fy0, fz0;
+  unsigned bad = 0u;
+  {
+    const double cx = x0 * g.rdx, cy = y0 * g.rdy, cz = z0 * g.rdz;
+    fx0 = cx - C.ci; fy0 = cy - C.cj; fz0 = cz - C.ck;
+  if (B2M_V2_R1_LOCATE || !((p < cnt) & below_bits(x0, dbits(g.lx)) & below_bits(y0, dbits(g.ly)) &
+        below_bits(z0, dbits(g.lz)) & in_unit(fx0) & in_unit(fy0) & in_unit(fz0))) {
+    // another cell, or a position the reference rejects (outside [0, l))
+    const bool inside = (p < cnt) && in_range(x0, dbits(g.lx)) && in_range(y0, dbits(g.ly)) &&
+                        in_range(z0, dbits(g.lz));
+    bad = inside ? 0u : 1u;
+    fast_enter(g, cells, C, inside ? cx : 0.0, inside ? cy : 0.0, inside ? cz : 0.0, fx0, fy0,
+               fz0);
+  }
+  }
+  double fx = fx0, fy = fy0, fz = fz0;
+  double nx, ny, nz, rc;
+  const int rounds = ROUNDS > 0 ? ROUNDS : U.rounds;
+#pragma unroll
+  for (int r = 0; r < rounds; ++r) {
+    double F[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) F[q] = poly8(C.K[q], fx, fy, fz);
+    implicit_num(u0, v0, w0, F, nx, ny, nz, rc);
+    if (r + 1 < rounds) {
+      // predictor x0 + vbar*dt/2 in the cached cell's frame (kernels.cpp:92)
+      fx = fma(nx * U.dc[0], rc, fx0);
+      fy = fma(ny * U.dc[1], rc, fy0);
+      fz = fma(nz * U.dc[2], rc, fz0);
+      if (!(in_unit(fx) & in_unit(fy) & in_unit(fz))) {
+        // left the cell: fold the absolute cell-unit position, locate, reload
+        const double bx = nx * rc, by = ny * rc, bz = nz * rc;
+        // (x0 re-read from the tile rather than kept live across the rounds)
+        const double cx = lds_f64(&buf[0][p]) * g.rdx, cy = lds_f64(&buf[1][p]) * g.rdy,
+                     cz = lds_f64(&buf[2][p]) * g.rdz;
+        double tx = fma(bx, U.dc[0], cx), ty = fma(by, U.dc[1], cy), tz = fma(bz, U.dc[2], cz);
+        if ((dbits(tx) >= dbits(g.nxd)) | (dbits(ty) >= dbits(g.nyd)) |
+            (dbits(tz) >= dbits(g.nzd))) {
+          tx = fold_fast(tx, g.nxd, dbits(g.nxd), g.rnx, bad);
+          ty = fold_fast(ty, g.nyd, dbits(g.nyd), g.rny, bad);
+          tz = fold_fast(tz, g.nzd, dbits(g.nzd), g.rnz, bad);
+        }
+        fast_enter(g, cells, C, tx, ty, tz, fx, fy, fz);
+        // the start position in the new cell's (folded) frame
+        fx0 = fma(-bx, U.dc[0], fx);
+        fy0 = fma(-by, U.dc[1], fy);
+        fz0 = fma(-bz, U.dc[2], fz);
+      }
+    }
+  }
+  // kernels.cpp:95-99
+  const double bx = nx * rc, by = ny * rc, bz = nz * rc;
+  double x1 = fma(bx, U.dt, lds_f64(&buf[0][p]));
+  double y1 = fma(by, U.dt, lds_f64(&buf[1][p]));
+  double z1 = fma(bz, U.dt, lds_f64(&buf[2][p]));
+  const double u1 = fma(2.0, bx, -u0);
+  const double v1 = fma(2.0, by, -v0);
+  const double w1 = fma(2.0, bz, -w0);
+  const bool fin_v = finite3(u1, v1, w1);
+  if (!((dbits(x1) <= dbits(g.ax.hi0)) & (dbits(y1) <= dbits(g.ay.hi0)) &
+        (dbits(z1) <= dbits(g.az.hi0)))) {
+    x1 = wrap_exact_bits(x1, g.ax, dbits(g.ax.hi0), dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
+    y1 = wrap_exact_bits(y1, g.ay, dbits(g.ay.hi0), dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
+    z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+    if (!finite3(x1, y1, z1)) bad = 1u;
+  }
+  if ((bad == 0u) & fin_v) {
+    buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
+    buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;
+    return 0u;
+  }
+  return p < cnt ? 1u : 0u;
+}
+
+// ---------------------------------------------------------------------------
+// FAST, z-invariant field ("2-D in 3-D", the GEM configurations)
+// ---------------------------------------------------------------------------
+//
+// When every node plane k of E and B equals plane 0 bit for bit (checked on
+// the device whenever the field changes, zinv_check_kernel), the z
+// coefficients Q of every cell polynomial are exactly zero: P + fz*Q == P, so
+// the gather is the bilinear (p0 + fy*p1) + fx*(p2 + fy*p3) of the same P
+// values -- the 3-D FAST result up to the sign of an exact zero -- from a
+// table of nx*ny columns (24 doubles each).  z crossings need no reload and
+// the z predictor feeds nothing but the gather, so it is not formed (a
+// non-finite vbar_z is still flagged, and z1 is checked at the end).
+
+struct Coef4 {
+  double p0, p1, p2, p3;
+};
+
+__device__ __forceinline__ Coef4 load_coef4(const double* c) {
+  Coef4 k;
+  const uint64_t pol = policy_evict_last();
+  asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(k.p0), "=d"(k.p1), "=d"(k.p2), "=d"(k.p3)
+      : "l"(c), "l"(pol));
+  return k;
+}
+
+__device__ __forceinline__ double poly4(const Coef4& k, double fx, double fy) {
+  return fma(fx, fma(fy, k.p3, k.p2), fma(fy, k.p1, k.p0));
+}
+
+struct FastCol {
+  Coef4 K[6];
+  double ci, cj;
+  int col;
+};
+
+__device__ __forceinline__ void fast_col_reset(FastCol& C) {
+  C.col = -1;
+  C.ci = C.cj = -4.0;
+}
+
+__device__ __forceinline__ void fast_enter2(const FastGrid& g, const double* __restrict__ cols,
+                                            FastCol& C, double tx, double ty, double& fx,
+                                            double& fy) {
+  const int i = max(min(__double2int_rz(tx), g.nx - 1), 0);
+  const int j = max(min(__double2int_rz(ty), g.ny - 1), 0);
+  const double di = static_cast<double>(i), dj = static_cast<double>(j);
+  fx = tx - di;
+  fy = ty - dj;
+  const int col = i + g.nx * j;
+  if (col != C.col) {
+    const double* c = cols + static_cast<long long>(col) * 24;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) C.K[q] = load_coef4(c + 4 * q);
+    C.col = col;
+  }
+  C.ci = di;
+  C.cj = dj;
+}
+
+template <int TILE, int ROUNDS>
+__device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const FastUniform& U,
+                                                     const double* __restrict__ cols,
+                                                     double (*buf)[TILE], int p, int cnt,
+                                                     FastCol& C) {
+  const double x0 = buf[0][p], y0 = buf[1][p], z0 = buf[2][p];
+  const double u0 = buf[3][p], v0 = buf[4][p], w0 = buf[5][p];
+  double fx0, fy0;
+  unsigned bad = 0u;
+  {
+    const double cx = x0 * g.rdx, cy = y0 * g.rdy;
+    fx0 = cx - C.ci;
+    fy0 = cy - C.cj;
+    if (!((p < cnt) & below_bits(x0, dbits(g.lx)) & below_bits(y0, dbits(g.ly)) &
+          below_bits(z0, dbits(g.lz)) & in_unit(fx0) & in_unit(fy0))) {
+      const bool inside = (p < cnt) && in_range(x0, dbits(g.lx)) && in_range(y0, dbits(g.ly)) &&
+                          in_range(z0, dbits(g.lz));
+      bad = inside ? 0u : 1u;
+      fast_enter2(g, cols, C, inside ? cx : 0.0, inside ? cy : 0.0, fx0, fy0);
+    }
+  }
+  double fx = fx0, fy = fy0;
+  double nx, ny, nz, rc;
+  const int rounds = ROUNDS > 0 ? ROUNDS : U.rounds;
+#pragma unroll
+  for (int r = 0; r < rounds; ++r) {
+    double F[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) F[q] = poly4(C.K[q], fx, fy);
+    implicit_num(u0, v0, w0, F, nx, ny, nz, rc);
+    if (r + 1 < rounds) {
+      // kernels.cpp:92: a non-finite predictor is a fault (z included)
+      if (!finite3(nz, rc, rc)) bad = 1u;
+      fx = fma(nx * U.dc[0], rc, fx0);
+      fy = fma(ny * U.dc[1], rc, fy0);
+      if (!(in_unit(fx) & in_unit(fy))) {
+        const double bx = nx * rc, by = ny * rc;
+        const double cx = lds_f64(&buf[0][p]) * g.rdx, cy = lds_f64(&buf[1][p]) * g.rdy;
+        double tx = fma(bx, U.dc[0], cx), ty = fma(by, U.dc[1], cy);
+        if ((dbits(tx) >= dbits(g.nxd)) | (dbits(ty) >= dbits(g.nyd))) {
+          tx = fold_fast(tx, g.nxd, dbits(g.nxd), g.rnx, bad);
+          ty = fold_fast(ty, g.nyd, dbits(g.nyd), g.rny, bad);
+        }
+        fast_enter2(g, cols, C, tx, ty, fx, fy);
+        fx0 = fma(-bx, U.dc[0], fx);
+        fy0 = fma(-by, U.dc[1], fy);
+      }
+    }
+  }
+  const double bx = nx * rc, by = ny * rc, bz = nz * rc;
+  double x1 = fma(bx, U.dt, lds_f64(&buf[0][p]));
+  double y1 = fma(by, U.dt, lds_f64(&buf[1][p]));
+  double z1 = fma(bz, U.dt, lds_f64(&buf[2][p]));
+  const double u1 = fma(2.0, bx, -u0);
+  const double v1 = fma(2.0, by, -v0);
+  const double w1 = fma(2.0, bz, -w0);
+  const bool fin_v = finite3(u1, v1, w1);
+  if (!((dbits(x1) <= dbits(g.ax.hi0)) & (dbits(y1) <= dbits(g.ay.hi0)) &
+        (dbits(z1) <= dbits(g.az.hi0)))) {
+    x1 = wrap_exact_bits(x1, g.ax, dbits(g.ax.hi0), dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
+    y1 = wrap_exact_bits(y1, g.ay, dbits(g.ay.hi0), dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
+    z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+    if (!finite3(x1, y1, z1)) bad = 1u;
+  }
+  if ((bad == 0u) & fin_v) {
+    buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
+    buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;
+    return 0u;
+  }
+  return p < cnt ? 1u : 0u;
+}
+
 // ---------------------------------------------------------------------------
 // STRICT: the reference's operation order, every rounding separate
 // ---------------------------------------------------------------------------

@@ -125,12 +125,21 @@ def gem_like_field(grid: Grid) -> FieldMesh:
     return f
 
 
-def gem_bench_field(grid: Grid) -> FieldMesh:
+def gem_bench_field(grid: Grid, z_varying: bool = False) -> FieldMesh:
     """Benchmark field: init_gem's B plus the gem_like_field E (nonzero, so
-    the mover's E path is exercised)."""
+    the mover's E path is exercised).  Both are z-invariant (the
+    GEM problem is 2-D in 3-D).  z_varying=True adds a small z-dependent Ez,
+    1e-3 sin(2 pi z / lz), so the general 3-D gather is measured too."""
     f = gem_field(grid)
     E = gem_like_field(grid).E
     f.E[:] = E
+    if z_varying:
+        nz = grid.nz
+        z = np.arange(nz + 1) * (grid.lz / nz)
+        dz = 1e-3 * np.sin(2.0 * np.pi * z / grid.lz)
+        dz[nz] = dz[0]  # the mirrored seam plane equals plane 0 bit for bit
+        Ev = f.E.reshape(nz + 1, grid.ny + 1, grid.nx + 1, 3)
+        Ev[..., 2] += dz[:, None, None]
     return f
 
 

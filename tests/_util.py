@@ -33,8 +33,12 @@ def assert_bitwise(got, want, what=""):
 
 # The north-star contract (BASELINE.json): positions and velocities within
 # 1e-12 relative, FMA reordering only.  Per SURVEY §8c the relative measure is
-#   velocity: per-particle vector-relative |dv| <= 1e-12 * max(|v|, 1)
-#             (the reference's own max(1,|ref|) form, test_kernels.cpp:177-179)
+#   velocity: per-particle vector-relative |dv| <= 1e-12 * |v|, with an
+#             absolute floor of 1e-3 x the batch's median |v| (only a
+#             particle whose new velocity cancels to ~0 -- v1 = 2 vbar - v0
+#             -- can reach it; GEM |v| is 0.01..0.05, so the reference's own
+#             max(1, |ref|) form, test_kernels.cpp:177-179, would be an
+#             absolute 1e-12 bound, 20-100x looser)
 #   position: periodic |dx| <= 1e-12 * L per axis
 # with particle count and cell indices exact.
 TOL = 1e-12
@@ -53,10 +57,11 @@ def assert_within_contract(got, want, grid, tol=TOL, what=""):
         assert m <= tol * L, f"{what} position axis {a}: max |dx| = {m:.3e} > {tol * L:.3e}"
     dv = np.sqrt(sum((got[a] - want[a]) ** 2 for a in range(3, 6)))
     vn = np.sqrt(sum(want[a] ** 2 for a in range(3, 6)))
-    lim = tol * np.maximum(vn, 1.0)
     if len(dv):
-        worst = float(np.max(dv / np.maximum(vn, 1.0)))
-        assert np.all(dv <= lim), f"{what} velocity: max |dv|/max(|v|,1) = {worst:.3e}"
+        floor = max(1e-3 * float(np.median(vn)), 1e-300)
+        scale = np.maximum(vn, floor)
+        worst = float(np.max(dv / scale))
+        assert np.all(dv <= tol * scale), f"{what} velocity: max |dv|/|v| = {worst:.3e}"
 
 
 def cells_of(p6, grid):
