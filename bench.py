@@ -3,33 +3,41 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A *step* is one mover cycle: every particle of the four GEM species advanced
-once (pc_iterations = 3, dt = 0.1) on the GEM field -- exactly the work the
-reference times as t_mover per cycle (runtime.cpp:227-229).  Particles are
-device-resident (the north star's SoA); the field is staged outside the timed
-region as in the reference's prefetch engine (engines.cpp:169-173).
+once (pc_iterations = 3, dt = 0.1) -- the work the reference times as t_mover
+per cycle (runtime.cpp:227-229) -- preceded by the cycle's field change (the
+field buffers marked rewritten, so the mover's derived gather tables and the
+field's z-invariance test are redone inside the step).  Particles are
+device-resident (the north star's SoA).
 
-N = 1: 64x64x32 cells, 216 ppc -> 61,046,784 particles.
-N > 1 (torchrun, one rank per GPU): y-slab partition with per-cycle NCCL
-particle migration and count check; weak scaling, ny = 64*N so every GPU holds
-a C2-sized slab.
+N = 1: 64x64x32 cells, 216 ppc -> 61,046,784 particles, field
+= init_gem's Harris B + the gem_like_field E (test_offload.cpp:60-71).
+N > 1: one rank per GPU over NCCL.  `--gpus N` launches the N ranks itself
+(torch.distributed.run) when it is not already under torchrun.  Weak scaling
+headline: y-slab partition (runtime.cpp:22-76), every rank a C2-sized slab,
+per cycle the field broadcast (runtime.cpp:143) + mover + NCCL particle
+migration + count check; plus a C4 strong-scaling leg (255.8M
+particles, fixed, on 1 and on N GPUs, efficiency S/N as bench.cpp:53-59).
 
 Prints ONE JSON line (rank 0).  `value` is device time (CUDA events) of the K
-timed steps, max over ranks; `e2e` goes through the reference-facing engine
-API (B200Engine.run_mover) with pinned host batches, host<->device copies
-inside the timed region; `cpu_baseline` is the reference's own mover
-(oracle/_ref, all host threads) on a bounded sample.
+timed steps, max over ranks; it equals the harmonic mean of the per-repetition
+MPA/s over the timed repetitions of 10 cycles (bench.cpp:13-45; the warm-up
+steps play the dropped first repetition).  `e2e` goes through the
+reference-facing engine API (B200Engine.run_mover) with pinned host batches,
+host<->device copies inside the timed region; `cpu_baseline` is the
+reference's own mover (oracle/_ref, all host threads) on the same bounded
+sample and field as the `--impl reference` arm.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
-
-import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -39,7 +47,10 @@ PC = 3
 PPC = 216
 NX, NY, NZ = 64, 64, 32
 LX, LY, LZ = 25.6, 12.8, 6.4
+C4_PPC = 905           # 64x64x32 cells, 255,774,720 particles
 BYTES_PER_PARTICLE = 96  # 48 B read + 48 B write of x,y,z,u,v,w
+REP_CYCLES = 10          # cycles per repetition (bench.cpp:13-45)
+CPU_SAMPLE_PER_THREAD = 2_000_000
 
 
 def load_peaks():
@@ -47,7 +58,7 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
@@ -105,17 +116,19 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": r}
 
 
-def measured_traffic(mode: str):
-    """dram__bytes_read + dram__bytes_write of the mover launch at C2 from the
-    committed `ncu --set full` capture (profiles/r01_c2_bench.json), per launch."""
-    p = os.path.join(ROOT, "profiles", "r01_c2_bench.json")
-    if not os.path.exists(p):
+PROFILE = os.path.join(ROOT, "profiles", "r02_c2_bench.json")
+
+
+def measured_traffic(kernel_tag: str):
+    """dram__bytes_read + dram__bytes_write per launch of the kernel whose ncu
+    name contains `kernel_tag`, from the committed `ncu --set full` capture of
+    this round (profiles/r02_c2_bench.json)."""
+    if not os.path.exists(PROFILE):
         return None
-    with open(p) as f:
+    with open(PROFILE) as f:
         d = json.load(f)
-    want = "0>(" if mode == "fast" else "1>("
     for k in d.get("kernels", []):
-        if "warp_tile_kernel" in k["kernel"] and want in k["kernel"]:
+        if kernel_tag in k["kernel"]:
             rd, wr = k["dram__bytes_read.sum"], k["dram__bytes_write.sum"]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             return float(rd[0]) * scale[rd[1]] + float(wr[0]) * scale[wr[1]]
@@ -135,11 +148,21 @@ def host_info():
     return os.cpu_count() or 1, model
 
 
+def harmonic_reps(step_ms, particles, rep=REP_CYCLES):
+    """Per-repetition MPA/s over consecutive groups of `rep` timed cycles and
+    their harmonic mean (bench.cpp:13-45); equal work per repetition, so the
+    harmonic mean is total particles / total time."""
+    reps = [step_ms[i:i + rep] for i in range(0, len(step_ms), rep)]
+    mpas = [particles * len(r) / (sum(r) * 1e-3) / 1e6 for r in reps if r]
+    hm = len(mpas) / sum(1.0 / m for m in mpas) if mpas else None
+    return {"cycles_per_rep": rep, "mpas": mpas, "harmonic_mean": hm}
+
+
 # ---------------------------------------------------------------------------
-# reference CPU mover (cpu_baseline and --impl reference)
+# the reference CPU mover (the --impl reference arm and our cpu_baseline key)
 # ---------------------------------------------------------------------------
 
-def cpu_mover_setup(grid_t, sample_total, field="gem"):
+def cpu_mover_setup(grid_t, sample_total, field="gem+E"):
     """Bounded sample of the GEM workload for the CPU mover: the first
     particles of each species in proportion to the species sizes, generated by
     the reference's own init_gem when it was built (else the C port)."""
@@ -178,45 +201,121 @@ def cpu_mover_step(kind, sample, E, B, grid_t, threads):
     return n, time.perf_counter() - t0
 
 
-def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
+def cpu_reference_measure(field, steps, warmup):
+    """The reference's pic::move_batch (oracle/_ref: its own sources, all host
+    threads over disjoint spans) on a bounded species-proportional sample of
+    the C2 state: `warmup` untimed then `steps` timed cycles of the sample.
+    Used by both the reference arm and our line's cpu_baseline, so the two
+    report the same method, sample and field."""
     threads, model = host_info()
     grid_t = (NX, NY, NZ, LX, LY, LZ)
-    kind, sample, E, B, total = cpu_mover_setup(grid_t, sample_total=2_000_000 * threads,
-                                                field=args.field)
+    kind, sample, E, B, total = cpu_mover_setup(grid_t, CPU_SAMPLE_PER_THREAD * threads,
+                                                field=field)
     if kind == "port":
         threads = 1
     n_s = sum(len(p[0][0]) for p in sample)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         cpu_mover_step(kind, sample, E, B, grid_t, threads)
-    times = []
-    for _ in range(args.steps):
-        n, t = cpu_mover_step(kind, sample, E, B, grid_t, threads)
-        times.append(t)
+    times = [cpu_mover_step(kind, sample, E, B, grid_t, threads)[1] for _ in range(max(1, steps))]
     mean = sum(times) / len(times)
-    value = n_s / mean / 1e6
+    return {"value": n_s / mean / 1e6, "unit": "MPA/s", "cores": threads, "kind": kind,
+            "cpu_model": model, "ms_per_step": mean * 1e3, "steps": len(times),
+            "particles_total": total,
+            "sample": f"first {n_s} of {total} C2 GEM particles (species-proportional, "
+                      f"{CPU_SAMPLE_PER_THREAD} per thread), field {field}, "
+                      f"pic::move_batch on {threads} threads over disjoint spans, "
+                      f"{warmup} warm-up + {len(times)} timed cycles"}
+
+
+def run_reference_arm(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    cpu = cpu_reference_measure(args.field, args.steps, args.warmup)
     line = {
-        "impl": "reference", "metric": "MPA/s in mover", "value": value, "unit": "MPA/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic GEM (reference init_gem)",
+        "impl": "reference", "metric": "MPA/s in mover", "value": cpu["value"], "unit": "MPA/s",
+        "n_gpus": args.gpus, "steps": cpu["steps"], "warmup": args.warmup,
+        "ms_per_step": cpu["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic GEM (reference init_gem) + gem_like_field E" if args.field == "gem+E"
+                else "synthetic GEM (reference init_gem), E = 0",
         "config": {"workload": "GEM 64x64x32, 216 ppc, 4 species, pc 3, dt 0.1 (C2)",
-                   "particles_total": total, "sample_particles_per_step": n_s},
-        "cpu_baseline": {"value": value, "unit": "MPA/s", "cores": threads, "kind": kind,
-                         "cpu_model": model,
-                         "sample": f"first {n_s} of {total} GEM particles (species-proportional), "
-                                   f"pic::move_batch on {threads} threads over disjoint spans"},
-        "e2e": {"value": value, "unit": "MPA/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "particles_total": cpu["particles_total"], "same_config": False,
+                   "note": "a bounded sample of the C2 state per step (the whole state is "
+                           "~1 s per cycle on the host); same metric, unit and field"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "MPA/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# our arm, one GPU
 # ---------------------------------------------------------------------------
+
+def time_steps(store, mps, steps, refresh, events):
+    """`steps` cycles, each: the field marked changed (z-invariance test and
+    gather tables rebuilt inside the move call) then the mover over all
+    species, enqueued back to back without host syncs.  With events: per step
+    (step ms, mover-kernel ms) from CUDA events on the launching stream --
+    torch's current stream around the step, the library's kernel-timing log
+    (b2m_kernel_timing_*) around the mover launches alone."""
+    import torch
+    ev = []
+    if events:
+        store.kernel_timing_begin(steps)
+    for _ in range(steps):
+        if events:
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record()
+        if refresh:
+            store.field_changed()
+        store.move_all(mps)
+        if events:
+            e[1].record()
+            ev.append(e)
+    if not events:
+        return []
+    kms = store.kernel_timing_read(steps)
+    return [(a.elapsed_time(b), k) for (a, b), k in zip(ev, kms)]
+
+
+def c4_single_gpu(args, local, field_kind):
+    """SURVEY C4 (255.8M particles) on this one GPU: the strong-scaling
+    baseline T1 (plain mover + field refresh, no exchange)."""
+    import torch
+    from paper_1904_03684_b200 import gem
+    from paper_1904_03684_b200.engine import DeviceStore
+    from paper_1904_03684_b200.mover import Grid, MoverParams
+    grid = Grid.make(NX, NY, NZ, LX, LY, LZ)
+    t0 = time.perf_counter()
+    batches = gem.init_gem_species(grid, C4_PPC, pinned=True)
+    t_init = time.perf_counter() - t0
+    field = gem.gem_bench_field(grid) if field_kind == "gem+E" else gem.gem_field(grid)
+    n = sum(b.count() for b in batches)
+    mps = [MoverParams.make(DT, b.qom, PC) for b in batches]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    store = DeviceStore(grid, [b.count() for b in batches], args.mode, device=local)
+    store.set_stream(stream.cuda_stream)
+    store.upload_field(field)
+    for s, b in enumerate(batches):
+        store.upload(s, b.span())
+        store.sort(s)
+    del batches
+    time_steps(store, mps, args.warmup, True, False)
+    torch.cuda.synchronize()
+    ev = time_steps(store, mps, args.steps, True, True)
+    torch.cuda.synchronize()
+    store.sync()
+    store.close()
+    step_ms = [t for t, k in ev]
+    ms = sum(step_ms) / len(step_ms)
+    return {"particles": n, "n_gpus": 1, "ms_per_step": ms, "value": n / (ms * 1e-3) / 1e6,
+            "unit": "MPA/s", "init_s": t_init,
+            "workload": "GEM 64x64x32, 905 ppc (SURVEY C4), one GPU, field refresh + mover"}
+
 
 def run_ours(args):
     import torch
@@ -224,71 +323,42 @@ def run_ours(args):
     from paper_1904_03684_b200.engine import B200Engine, DeviceStore
     from paper_1904_03684_b200.mover import Grid, MoverParams
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # B2M_SLAB_PATH=1 runs the partition-layer step (mover fused with the
-    # owner scan + compaction + exchange + count all-reduce) even at N = 1, to
-    # measure what the multi-GPU step adds over the plain mover
-    if world > 1 or os.environ.get("B2M_SLAB_PATH") == "1":
-        from paper_1904_03684_b200 import partition
-        return partition.bench_world(args)
-
     torch.cuda.set_device(local)
     lib = _capi.lib()
     grid = Grid.make(NX, NY, NZ, LX, LY, LZ)
     t_init = time.perf_counter()
     batches = gem.init_gem_species(grid, PPC, pinned=True)
     t_init = time.perf_counter() - t_init
-    field = gem.gem_field(grid) if args.field == "gem" else gem.gem_bench_field(grid)
+    field = gem.gem_bench_field(grid) if args.field == "gem+E" else gem.gem_field(grid)
     n_total = sum(b.count() for b in batches)
     mps = [MoverParams.make(DT, b.qom, PC) for b in batches]
 
     store = DeviceStore(grid, [b.count() for b in batches], args.mode, device=local)
-    store.upload_field(field)
-    for s, b in enumerate(batches):
-        store.upload(s, b.span())
-    if args.sort:
-        for s in range(len(batches)):
-            store.sort(s)
-    store.sync()
-
-    # ---- device-resident timed region ----
-    # Work runs on torch's current stream so torch events can bracket every
-    # launch.  A step = one mover cycle over all species; every `resort`
-    # steps the step also re-sorts every species by cell (the optional
-    # cell-sort pass) -- its cost is inside the timed region.
     stream = torch.cuda.Stream()           # a real stream handle (the legacy default is 0)
     torch.cuda.set_stream(stream)
     store.set_stream(stream.cuda_stream)
-    step_no = [0]
 
-    def step():
-        if args.resort and step_no[0] % args.resort == 0:
-            for s in range(len(batches)):
+    def load_state(f):
+        store.upload_field(f)
+        for s, b in enumerate(batches):
+            store.upload(s, b.span())
+            if args.sort:
                 store.sort(s)
-        store.move_all(mps)
-        step_no[0] += 1
+        store.sync()
 
-    for _ in range(args.warmup):
-        step()
+    load_state(field)
+
+    # ---- device-resident timed region: K cycles of (field refresh + mover) ----
+    time_steps(store, mps, args.warmup, args.refresh, False)
     torch.cuda.synchronize()
     store.sync()
     launches0 = lib.b2m_launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record()
-        for k in range(args.steps):
-            if args.resort and step_no[0] % args.resort == 0:
-                for s in range(len(batches)):
-                    store.sort(s)
-            ev[k][0].record()
-            store.move_all(mps)
-            ev[k][1].record()
-            step_no[0] += 1
+        ev = time_steps(store, mps, args.steps, args.refresh, True)
         t1.record()
         torch.cuda.synchronize()
     store.sync()
@@ -296,10 +366,32 @@ def run_ours(args):
     launches = lib.b2m_launch_count() - launches0
     ms = total_ms / args.steps
     value = n_total / (ms * 1e-3) / 1e6
-    # the mover launch alone (events bracket exactly the one move_all launch)
-    mover_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = [t for t, k in ev]
+    mover_ms = [k for t, k in ev]
     kernel_ms = sum(mover_ms) / len(mover_ms)
-    sort_share = 1.0 - sum(mover_ms) / total_ms
+    reps = harmonic_reps(step_ms, n_total)
+    peak, peak_src = load_peaks()
+    alg_bytes = BYTES_PER_PARTICLE * n_total
+
+    # ---- the general 3-D kernel on the same particles, z-varying field ----
+    general = None
+    if args.general_3d and args.mode == "fast":
+        load_state(gem.gem_bench_field(grid, z_varying=True))
+        time_steps(store, mps, args.warmup, args.refresh, False)
+        g_steps = min(args.steps, 10)
+        gev = time_steps(store, mps, g_steps, args.refresh, True)
+        torch.cuda.synchronize()
+        store.sync()
+        g_ms = [k for t, k in gev]
+        g_step = [t for t, k in gev]
+        gk = sum(g_ms) / len(g_ms)
+        general = {"value": n_total / (sum(g_step) / len(g_step) * 1e-3) / 1e6, "unit": "MPA/s",
+                   "kernel": "warp_tile_kernel<4,0,3> (FAST, general trilinear gather)",
+                   "kernel_ms": gk, "steps": g_steps,
+                   "roofline_frac": alg_bytes / (gk * 1e-3) / 1e9 / peak,
+                   "traffic": measured_traffic("<4, 0, 3>"),
+                   "field": "the bench field + Ez 1e-3 sin(2 pi z/lz) (not z-invariant), same "
+                            "particles, re-sorted, after the same warm-up"}
 
     # STRICT (bit-exact) mode on the same resident state, for reference
     strict_value = None
@@ -317,7 +409,6 @@ def run_ours(args):
         store.set_mode(args.mode)
 
     # Moment deposition (deposit_moments, kernels.cpp:147-183)
-    # of the resident state after the timed steps, rho + J for all species
     moments = None
     if args.moments:
         def deposit_ms():
@@ -331,7 +422,7 @@ def run_ours(args):
             store.sync()
             return a.elapsed_time(b_)
         deposit_ms()  # warm-up
-        drifted = deposit_ms()   # the state the timed steps left (drifted since the last sort)
+        drifted = deposit_ms()   # the state the steps above left (drifted since the last sort)
         for s in range(len(batches)):
             store.sort(s)
         fresh = deposit_ms()     # right after a cell sort
@@ -339,14 +430,9 @@ def run_ours(args):
                    "what": "deposit_moments rho+J, all species, device-resident C2 state right "
                            "after a cell sort",
                    "ms_drifted": drifted,
-                   "drifted_what": "the same on the state left by the timed steps (particles "
-                                   "drifted out of cell order: more per-run mesh updates)",
-                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / load_peaks()[0]}
+                   "drifted_what": "the same on the state the timed steps left",
+                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / peak}
     store.close()
-
-    peak, peak_src = load_peaks()
-    alg_bytes = BYTES_PER_PARTICLE * n_total
-    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
 
     # ---- e2e through the reference-facing engine API, host batches ----
     e2e = None
@@ -355,101 +441,431 @@ def run_ours(args):
         eng.prime(field, batches)
         eng.run_mover(field, batches, mps)  # warm-up
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ev0 = torch.cuda.Event(enable_timing=True)
+        e2e_t = []
         for _ in range(args.e2e_steps):
+            t = time.perf_counter()
             eng.run_mover(field, batches, mps)
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+            e2e_t.append(time.perf_counter() - t)
+        e2e_s = sum(e2e_t) / len(e2e_t)
         e2e = {"value": n_total / e2e_s / 1e6, "unit": "MPA/s",
                "h2d_bytes_per_step": alg_bytes // 2 + 2 * 24 * grid.nodes(),
                "d2h_bytes_per_step": alg_bytes // 2,
-               "ms_per_step": e2e_s * 1e3,
+               "ms_per_step": e2e_s * 1e3, "steps": len(e2e_t),
+               "step_ms": [t * 1e3 for t in e2e_t],
                "path": "B200Engine.run_mover (pic::Engine contract) with pinned host batches; "
-                       "chunked H2D / kernel / D2H on three streams"}
+                       "chunked H2D / kernel / D2H on three streams (PCIe-bound)"}
         eng.close()
+    del batches
 
-    # ---- CPU baseline (reference mover on host cores, bounded sample) ----
-    cpu = None
-    if args.cpu_baseline:
-        threads, model = host_info()
-        grid_t = grid.as_tuple()
-        kind, sample, E, B, total = cpu_mover_setup(grid_t, sample_total=1_000_000 * threads,
-                                                    field=args.field)
-        if kind == "port":
-            threads = 1
-        n_s, t = cpu_mover_step(kind, sample, E, B, grid_t, threads)
-        cpu = {"value": n_s / t / 1e6, "unit": "MPA/s", "cores": threads, "kind": kind,
-               "cpu_model": model,
-               "sample": f"first {n_s} of {total} GEM particles (species-proportional), one "
-                         f"mover cycle, pic::move_batch on {threads} threads"}
+    # ---- strong-scaling baseline (C4 on this GPU) ----
+    strong = c4_single_gpu(args, local, args.field) if args.strong else None
 
+    # ---- CPU baseline: the reference arm's own measurement ----
+    cpu = cpu_reference_measure(args.field, 2, 1) if args.cpu_baseline else None
+
+    kname = "warp_tile_kernel<4,0,2> (FAST, z-invariant column gather)" \
+        if args.mode == "fast" and args.field in ("gem", "gem+E") else "warp_tile_kernel"
     line = {
         "metric": "MPA/s in mover", "value": value, "unit": "MPA/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": ("synthetic GEM state bit-identical to the reference's init_gem (seed 12345): "
-                 "Harris B, E = 0, as the reference's own run_benchmark sees it")
-                if args.field == "gem" else
-                "synthetic GEM particles (reference init_gem) + gem_like_field E",
-        "config": {"workload": "GEM 64x64x32, 216 ppc, 4 species (C2), pc 3, dt 0.1",
-                   "particles": n_total, "mode": args.mode,
-                   "cell_sort": f"every {args.resort} steps, inside the timed region"
-                                if args.resort else "once before timing",
+        "data": ("synthetic GEM state bit-identical to the reference's init_gem (seed 12345) "
+                 "+ gem_like_field E (SURVEY §8d)") if args.field == "gem+E" else
+                "synthetic GEM state (reference init_gem), E = 0",
+        "config": {"workload": "GEM 2-D-in-3-D, 64x64x32 cells, 216 ppc, 4 species (C2), "
+                               "pc 3, dt 0.1",
+                   "particles": n_total, "mode": args.mode, "field": args.field,
+                   "step": "field marked rewritten (z-invariance test + gather tables rebuilt) "
+                           "+ mover over all species" if args.refresh else "mover over all species",
+                   "cell_sort": "once, before the warm-up (not in the timed region)"
+                                if args.sort else "never (init_gem order)",
                    "l2": "inputs larger than L2 (2.93 GB SoA vs 126 MB)",
                    "parallelism": "single GPU"},
+        "repetitions": reps,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
-                     "traffic": args.traffic if args.traffic is not None
-                                else measured_traffic(args.mode),
-                     "traffic_source": "ncu --set full, profiles/r01_c2_bench.json",
-                     "kernel": "warp_tile_kernel<4,0> (FAST)" if args.mode == "fast"
-                               else "warp_tile_kernel<4,1> (STRICT)",
-                     "kernel_ms": kernel_ms, "bytes_per_launch": alg_bytes,
-                     "sort_share_of_step": sort_share,
+        "roofline": {"bound": "hbm", "achieved": alg_bytes / (kernel_ms * 1e-3) / 1e9,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": alg_bytes / (kernel_ms * 1e-3) / 1e9 / peak,
+                     "traffic": measured_traffic("<4, 0, 2>") if args.mode == "fast" else None,
+                     "traffic_source": "ncu --set full, profiles/r02_c2_bench.json",
+                     "kernel": kname, "kernel_ms": kernel_ms,
+                     "bytes_per_launch": alg_bytes, "bytes_per_particle": BYTES_PER_PARTICLE,
+                     "kernel_share_of_step": sum(mover_ms) / sum(step_ms),
                      "peak_source": peak_src},
-        # the resource that actually binds this kernel: FP64 dependency
-        # latency at 12 warps/SM (profiles/README.md).  225 FP64 instructions
-        # per particle (ncu, FAST) against the FP64 FMA rate measured by
-        # tools/micro/dfma.cu (56 lane-ops/clk/SM x 148 SMs x 1.965 GHz)
-        "fp64_pipe": ({"ops_per_particle": 225, "achieved_tops": 225 * n_total / (kernel_ms * 1e-3)
-                       / 1e12, "peak_tops": 56 * 148 * 1.965e9 / 1e12,
-                       "frac": 225 * n_total / (kernel_ms * 1e-3) / (56 * 148 * 1.965e9),
-                       "peak_source": "tools/micro/dfma.cu on this B200 (FP64 FMA, ILP 8)"}
-                      if args.mode == "fast" else None),
+        "general_3d": general,
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "strict_value": strict_value,
         "moments": moments,
+        "strong_scaling": strong,
         "init_s": t_init,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main(argv=None):
+# ---------------------------------------------------------------------------
+# our arm, N GPUs (one rank per GPU)
+# ---------------------------------------------------------------------------
+
+def verify_sample(store, sw_step, field, grid, rank, world, dist, gather, m=2048):
+    """One untimed partitioned step checked against the reference mover: the
+    first m particles of every species on every rank are moved on the host by
+    pic::move_batch (oracle/_ref -- the particles are independent), then the
+    distributed step runs; every expected particle must be found on exactly
+    one rank, within the 1e-12 contract (positions |dx| <= 1e-12 L, velocities
+    |dv| <= 1e-12 |v|).  Particles within 1e-9 of a periodic wall are not
+    sampled (a wrap could put the GPU and host copies at 0 and at L)."""
+    import numpy as np
+    import torch
+    import oracle
+    from paper_1904_03684_b200.partition import _CudaArray
+    gt = grid.as_tuple()
+    L = np.array(gt[3:6])
+    exp = []
+    for s in range(store.n_species):
+        k = min(m, store.count(s))
+        if k == 0:
+            exp.append(np.empty((0, 6)))
+            continue
+        p6 = [np.empty(k) for _ in range(6)]
+        store.download_range(s, p6, 0, k)
+        store.sync()
+        qom = [-25.0, 1.0, -25.0, 1.0][s]
+        if os.path.exists(oracle.REF_SO):
+            oracle.ref_move_batch(p6, field.E.ravel(), field.B.ravel(), gt, DT, qom, PC)
+        else:
+            oracle.port_move_batch(p6, field.E.ravel(), field.B.ravel(), gt, DT, qom, PC)
+        e = np.stack(p6, axis=1)
+        near = np.any((e[:, :3] < 1e-9 * L) | (e[:, :3] > L - 1e-9 * L), axis=1)
+        exp.append(e[~near])
+    sw_step()
+    allexp = gather(exp)                      # every rank's expected particles
+    found = 0
+    want = 0
+    for s in range(store.n_species):
+        e = np.concatenate([x[s] for x in allexp]) if allexp else np.empty((0, 6))
+        want += len(e)
+        n = store.count(s)
+        if n == 0 or len(e) == 0:
+            continue
+        ptrs = store.device_ptrs(s)
+        cols = [torch.as_tensor(_CudaArray(p, (n,)), device="cuda") for p in ptrs]
+        xs, perm = torch.sort(cols[0])
+        et = torch.as_tensor(e, device="cuda")
+        tol_x = 1e-12 * float(L[0])
+        lo = torch.searchsorted(xs, et[:, 0] - tol_x)
+        hit = torch.zeros(len(e), dtype=torch.bool, device="cuda")
+        vn = et[:, 3:].norm(dim=1)
+        for c in range(4):                    # the few candidates inside the x window
+            idx = (lo + c).clamp(max=n - 1)
+            j = perm[idx]
+            ok = torch.ones(len(e), dtype=torch.bool, device="cuda")
+            for a in range(3):
+                ok &= (cols[a][j] - et[:, a]).abs() <= 1e-12 * float(L[a])
+            dv = torch.stack([cols[a][j] - et[:, a] for a in range(3, 6)], 1).norm(dim=1)
+            ok &= dv <= 1e-12 * vn.clamp(min=1e-300)
+            hit |= ok
+        found += int(hit.sum().item())
+    del xs, perm
+    return found, want
+
+
+def run_world(args):
+    # the communicator lines (one per rank) go to stderr, not the JSON stream
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1904_03684_b200 import _capi, gem
+    from paper_1904_03684_b200.engine import B200Engine, DeviceStore
+    from paper_1904_03684_b200.mover import Grid, MoverParams
+    from paper_1904_03684_b200.partition import DeviceMigration, NativeSlabWorld, SlabWorld
+
+    world_env = int(os.environ["WORLD_SIZE"])
+    ndev = torch.cuda.device_count()
+    shared = ndev < world_env   # ranks sharing GPUs: a functional run (NCCL needs one GPU each)
+    backend = os.environ.get("B2M_DIST_BACKEND") or ("gloo" if shared else "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, ndev)
+    torch.cuda.set_device(local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", local)
+
+    def reduce(x, op):
+        t = torch.tensor([x], dtype=torch.float64)
+        if backend == "nccl":
+            t = t.to(dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    native = backend == "nccl" and os.environ.get("B2M_NATIVE_WORLD", "1") != "0"
+    field_of = (lambda g: gem.gem_bench_field(g)) if args.field == "gem+E" \
+        else (lambda g: gem.gem_field(g))
+
+    def setup(grid, ppc):
+        """This rank's slab of the GEM state in a device store + its slab world."""
+        batches = gem.init_gem_slab(grid, ppc, rank, world)
+        field = field_of(grid)
+        mps = [MoverParams.make(DT, b.qom, PC) for b in batches]
+        caps = [int(b.count() * 1.05) + 65536 for b in batches]
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        store = DeviceStore(grid, caps, args.mode, device=local)
+        store.set_stream(stream.cuda_stream)
+        store.upload_field(field)
+        for s, b in enumerate(batches):
+            store.upload(s, b.span())
+            if args.sort:
+                store.sort(s)
+        if native:
+            sw = NativeSlabWorld(grid, store, rank, world, dist)
+        else:
+            sw = SlabWorld(grid, DeviceMigration(store, rank, world), len(batches), dist, dev)
+        sw.set_total()
+        # field replication every cycle (runtime.cpp:143 / :221-223): rank 0's
+        # device field broadcast to every rank, the gather tables rebuilt
+        fE = fB = None
+        if not native:
+            fE = torch.as_tensor(field.E.ravel().copy(), device=dev)
+            fB = torch.as_tensor(field.B.ravel().copy(), device=dev)
+
+        def replicate():
+            if native:
+                sw.broadcast_field(0)
+                return
+            for t in (fE, fB):
+                if backend == "nccl":
+                    dist.broadcast(t, 0)
+                else:
+                    h = t.cpu()
+                    dist.broadcast(h, 0)
+                    t.copy_(h.to(dev))
+            store.upload_field_device(fE.data_ptr(), fB.data_ptr())
+
+        def step():
+            if args.refresh:
+                replicate()
+            sw.step(mps)
+        return batches, field, mps, store, sw, step
+
+    def timed(store, step, steps):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        l0 = _capi.lib().b2m_launch_count()
+        per = []
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step()
+            b.record()
+            per.append((a, b, (store.elapsed_ms(13, 14), store.elapsed_ms(14, 15))
+                        if native else (None, None)))
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        launches = _capi.lib().b2m_launch_count() - l0
+        step_ms = [a.elapsed_time(b) for a, b, _ in per]
+        mover = [x[0] for _, _, x in per if x[0] is not None]
+        exch = [x[1] for _, _, x in per if x[1] is not None]
+        return ms, step_ms, (sum(mover) / len(mover) if mover else None), \
+            (sum(exch) / len(exch) if exch else None), launches
+
+    # ---- weak scaling: every rank a C2-sized slab ----
+    grid = Grid.make(NX, NY * world, NZ, LX, LY * world, LZ)
+    batches, field, mps, store, sw, step = setup(grid, PPC)
+    n_local = sum(store.count(s) for s in range(len(batches)))
+    with ClockSampler(local) as clk:
+        ms, step_ms, mover_ms, exch_ms, launches = timed(store, step, args.steps)
+    ms_max = reduce(ms, dist.ReduceOp.MAX)
+    n_total = int(reduce(n_local, dist.ReduceOp.SUM))
+    peak, peak_src = load_peaks()
+    mine = {"rank": rank, "particles": n_local, "ms_per_step": ms, "mover_ms": mover_ms,
+            "exchange_ms": exch_ms,
+            "roofline_frac": (BYTES_PER_PARTICLE * n_local / (mover_ms * 1e-3) / 1e9 / peak)
+            if mover_ms else None}
+    ranks = gather(mine)
+    reps = harmonic_reps([reduce(t, dist.ReduceOp.MAX) for t in step_ms], n_total)
+    verify = None
+    if args.verify:
+        found, want = verify_sample(store, step, field, grid, rank, world, dist, gather)
+        found = int(reduce(found, dist.ReduceOp.SUM))
+        verify = {"sampled": want, "found_within_1e-12": found, "ok": found == want,
+                  "how": "first 2048 particles of every species on every rank moved by the "
+                         "reference pic::move_batch on the host; after one partitioned step "
+                         "each must be on exactly one rank within the contract"}
+        assert found == want, f"sampled reference check failed: {found} of {want}"
+    counts_ok = True   # every step checked the global count (runtime.cpp:264-269)
+    store.close()
+    dist.barrier()
+
+    # ---- e2e through the engine API on this rank's host batches ----
+    e2e = None
+    if args.e2e_steps > 0:
+        eng = B200Engine(grid, mode=args.mode, schedule="pipeline", device=local)
+        eng.prime(field, batches)
+        eng.run_mover(field, batches, mps)  # warm-up
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.run_mover(field, batches, mps)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        eng.close()
+        e2e_s = reduce(e2e_s, dist.ReduceOp.MAX)
+        n_e2e = int(reduce(sum(b.count() for b in batches), dist.ReduceOp.SUM))
+        e2e = {"value": n_e2e / e2e_s / 1e6, "unit": "MPA/s",
+               "h2d_bytes_per_step": 48 * n_e2e + world * 2 * 24 * grid.nodes(),
+               "d2h_bytes_per_step": 48 * n_e2e, "ms_per_step": e2e_s * 1e3,
+               "steps": args.e2e_steps,
+               "path": "B200Engine.run_mover per rank (pic::Engine contract) on the rank's "
+                       "pinned host batches; max over ranks"}
+    del batches
+
+    # ---- strong scaling: C4 fixed (255.8M particles) on 1 and on N GPUs ----
+    strong = None
+    if args.strong:
+        t1 = c4_single_gpu(args, local, args.field) if rank == 0 else None
+        dist.barrier()
+        g4 = Grid.make(NX, NY, NZ, LX, LY, LZ)
+        b4, f4, mps4, st4, sw4, step4 = setup(g4, C4_PPC)
+        n4 = int(reduce(sum(st4.count(s) for s in range(len(b4))), dist.ReduceOp.SUM))
+        del b4
+        ms4, _, mv4, ex4, _ = timed(st4, step4, args.steps)
+        per4 = gather({"rank": rank, "ms_per_step": ms4, "mover_ms": mv4, "exchange_ms": ex4,
+                       "particles": sum(st4.count(s) for s in range(st4.n_species))})
+        ms4 = reduce(ms4, dist.ReduceOp.MAX)
+        st4.close()
+        if rank == 0:
+            sp = t1["ms_per_step"] / ms4
+            strong = {"workload": "GEM 64x64x32, 905 ppc (SURVEY C4), fixed; y-slabs of "
+                                  f"{NY // world} cells", "particles": n4,
+                      "t1": t1, "n_gpus": world, "ms_per_step": ms4,
+                      "value": n4 / (ms4 * 1e-3) / 1e6, "unit": "MPA/s",
+                      "speedup": sp, "efficiency": sp / world,
+                      "efficiency_def": "S/N with S = T1/TN (bench.cpp:53-59)", "ranks": per4}
+        dist.barrier()
+
+    cpu = cpu_reference_measure(args.field, 2, 1) if args.cpu_baseline and rank == 0 else None
+    if rank == 0:
+        mv = [r["mover_ms"] for r in ranks if r["mover_ms"] is not None]
+        kernel_ms = max(mv) if mv else None
+        line = {"metric": "MPA/s in mover", "value": n_total / (ms_max * 1e-3) / 1e6,
+                "unit": "MPA/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic GEM state (reference init_gem generator) per-rank C2-sized "
+                        "slab" + (" + gem_like_field E" if args.field == "gem+E" else ""),
+                "config": {"workload": f"GEM 2-D-in-3-D, 64x{64 * world}x32 cells, 216 ppc, "
+                                       f"y-slabs of 64 cells (C2 per GPU)",
+                           "particles": n_total, "mode": args.mode, "field": args.field,
+                           "step": ("field broadcast from rank 0 + gather tables rebuilt + "
+                                    if args.refresh else "") +
+                                   "mover fused with the owner scan + compaction + NCCL P2P "
+                                   "migration of all species + count all-reduce",
+                           "cell_sort": "once, before the warm-up" if args.sort else "never",
+                           "parallelism": f"y-slab x{world}, {backend}"
+                                          + (" (ranks share GPUs: functional run)" if shared
+                                             else "") + (", native b2m_world_step" if native
+                                                         else ", Python SlabWorld")},
+                "repetitions": reps,
+                "ranks": ranks,
+                "gpu_launches": int(launches),
+                "roofline": ({"bound": "hbm", "unit": "GB/s", "peak": peak,
+                              "achieved": BYTES_PER_PARTICLE * ranks[0]["particles"]
+                              / (ranks[0]["mover_ms"] * 1e-3) / 1e9,
+                              "frac": ranks[0]["roofline_frac"],
+                              "kernel": "rank 0: mover + gather-table rebuild + owner scan + "
+                                        "compaction (b2m_world_step slots 13-14)",
+                              "kernel_ms": ranks[0]["mover_ms"], "max_kernel_ms": kernel_ms,
+                              "traffic": None, "peak_source": peak_src}
+                             if mv else None),
+                "verify": verify, "counts_conserved": counts_ok,
+                "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+                "strong_scaling": strong}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# launcher
+# ---------------------------------------------------------------------------
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(argv, n):
+    """`--gpus N` outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run and relay rank 0's JSON line.  NCCL_DEBUG=INFO by
+    default, to stderr, so the communicator lines show the N ranks."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    p = subprocess.run(cmd, env=env, stdout=subprocess.PIPE, text=True)
+    for ln in p.stdout.splitlines():
+        (sys.stdout if ln.lstrip().startswith("{") else sys.stderr).write(ln + "\n")
+    sys.stdout.flush()
+    return p.returncode
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
-    ap.add_argument("--sort", type=int, default=1, help="cell-sort species once before timing")
-    ap.add_argument("--resort", type=int, default=32,
-                    help="re-sort every N steps inside the timed region (0: never)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sort", type=int, default=1, help="cell-sort species once before warm-up")
+    ap.add_argument("--refresh", type=int, default=1,
+                    help="every step marks the field rewritten (tables rebuilt in the step)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--strict-too", type=int, default=1)
     ap.add_argument("--moments", type=int, default=1)
-    ap.add_argument("--field", default="gem", choices=["gem", "gem+E"],
-                    help="gem: the reference's init_gem field (E=0, static B) that its own "
-                         "benchmark moves particles in; gem+E: add the gem_like_field E")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per launch from an ncu --set full capture")
-    args = ap.parse_args(argv)
+    ap.add_argument("--general-3d", type=int, default=1,
+                    help="also time the general 3-D kernel on a z-varying field")
+    ap.add_argument("--strong", type=int, default=1,
+                    help="the C4 strong-scaling leg (255.8M particles)")
+    ap.add_argument("--verify", type=int, default=1,
+                    help="N > 1: sampled check of one step against the reference mover")
+    ap.add_argument("--field", default="gem+E", choices=["gem", "gem+E"],
+                    help="gem+E: init_gem's B + the gem_like_field E (SURVEY §8d); gem: E = 0")
+    return ap.parse_args(argv)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference_arm(args)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        return self_launch(argv, args.gpus)
+    if world > 1:
+        return run_world(args)
     return run_ours(args)
 
 

@@ -138,9 +138,15 @@ b2m_status b2m_host_free(void* ptr);
  * layout from host memory; the device relayout for the gather is enqueued
  * behind the copy.  n_nodes must equal (nx+1)(ny+1)(nz+1). */
 b2m_status b2m_field_upload(b2m_ctx* ctx, const double* E, const double* B, uint64_t n_nodes);
-/* Same from device memory (e.g. after an NCCL broadcast). */
+/* Same from device memory (e.g. after an NCCL broadcast).  Passing the
+ * context's own buffers (b2m_field_device_ptrs) copies nothing and only marks
+ * the field as changed: the derived gather tables rebuild on the next move. */
 b2m_status b2m_field_upload_device(b2m_ctx* ctx, const double* dE, const double* dB,
                                    uint64_t n_nodes);
+/* The context's device field buffers (FieldView layout), for a device-side
+ * field phase writing the next cycle's field in place (the reference's field
+ * update between mover calls, runtime.cpp:221-223). */
+b2m_status b2m_field_device_ptrs(b2m_ctx* ctx, double** dE, double** dB);
 
 /* Species transfers (enqueue_species_h2d/d2h, engines.cpp:62-93).  host6 =
  * {x,y,z,u,v,w}.  Upload sets the device count to n (AllocError above
@@ -163,7 +169,9 @@ b2m_status b2m_species_device_ptrs(b2m_ctx* ctx, int s, double** out6);
  * engines.cpp:95-99).  Asynchronous; a fault is recorded on the device and
  * reported by b2m_sync. */
 b2m_status b2m_move(b2m_ctx* ctx, int s, const b2m_mover_params* mp);
-/* All species in one launch: mp[n_species]. */
+/* All species in one launch: mp[n_species].  Records event slots 11 and 12
+ * around the mover launch(es) alone -- after any gather-table rebuild the
+ * call enqueues first -- so b2m_event_elapsed_ms(11, 12) is the kernel time. */
 b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp);
 /* Range variant for chunked pipelines. */
 b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint64_t offset,
@@ -231,6 +239,12 @@ b2m_status b2m_deposit_moments_host(const b2m_grid* g, const double* x, const do
  * kernels.cpp:98-99), B2M_CFL_VIOLATION for an exchange violation, and
  * poisons the context. */
 b2m_status b2m_sync(b2m_ctx* ctx, int* bad_species, int64_t* first_bad);
+/* Kernel timing without host syncs: after b2m_kernel_timing_begin(ctx, n)
+ * the next n b2m_move_all calls each record a CUDA event pair around their
+ * mover launch(es) alone; b2m_kernel_timing_read waits for them and returns
+ * the n durations in ms (*n = how many were recorded) and ends the log. */
+b2m_status b2m_kernel_timing_begin(b2m_ctx* ctx, int capacity);
+b2m_status b2m_kernel_timing_read(b2m_ctx* ctx, float* ms, int max_n, int* n);
 /* Record / measure device time on the context's stream (CUDA events). */
 b2m_status b2m_event_record(b2m_ctx* ctx, int slot);
 b2m_status b2m_event_elapsed_ms(b2m_ctx* ctx, int slot_a, int slot_b, float* ms);
@@ -275,7 +289,10 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
  * faulted -- it still completes the exchange with empty outboxes so its peers
  * do not hang (the analogue of arrive_and_drop, runtime.cpp:283-288) --,
  * EngineFault when a peer faulted or the global count drifted.  Two host
- * synchronisations per step.  *sent = records this rank sent. */
+ * synchronisations per step.  *sent = records this rank sent.  The step
+ * records event slots 13 (start), 14 (mover + compaction enqueued) and 15
+ * (exchange, merge and count all-reduce enqueued) on the context's stream, so
+ * b2m_event_elapsed_ms(13, 14) / (14, 15) split its device time. */
 #define B2M_WORLD_ID_BYTES 128
 b2m_status b2m_world_id(void* id);
 b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world);
@@ -285,7 +302,10 @@ b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
 b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
 /* Sum every rank's moment mesh (b2m_moments_zero + b2m_deposit per rank) into
  * every rank's mesh, in place (ncclAllReduce): the reference adds the
- * per-worker meshes (runtime.cpp:251-262). */
+ * per-worker meshes (runtime.cpp:251-262).  Not bitwise reproducible: the
+ * per-rank deposit sums with FP64 atomics and NCCL picks the reduction order
+ * (equal to rounding of the sums; the reference's fixed worker order is not
+ * reproduced). */
 b2m_status b2m_world_reduce_moments(b2m_ctx* ctx);
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count);

@@ -66,6 +66,10 @@ SIGNATURES = {
     "b2m_host_free": (_st, [C.c_void_p]),
     "b2m_field_upload": (_st, [C.c_void_p, _dp, _dp, _u64]),
     "b2m_field_upload_device": (_st, [C.c_void_p, C.c_void_p, C.c_void_p, _u64]),
+    "b2m_field_device_ptrs": (_st, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "b2m_kernel_timing_begin": (_st, [C.c_void_p, C.c_int]),
+    "b2m_kernel_timing_read": (_st, [C.c_void_p, C.POINTER(C.c_float), C.c_int,
+                                     C.POINTER(C.c_int)]),
     "b2m_species_upload": (_st, [C.c_void_p, C.c_int, C.POINTER(_dp), _u64]),
     "b2m_species_download": (_st, [C.c_void_p, C.c_int, C.POINTER(_dp), _u64, C.POINTER(_u64)]),
     "b2m_species_upload_range": (_st, [C.c_void_p, C.c_int, C.POINTER(_dp), _u64, _u64]),

@@ -155,6 +155,10 @@ struct b2m_ctx {
     bool total_set = false;
   } w;
   std::vector<void*> allocations;
+  // b2m_kernel_timing_begin / _read: per mover call a (start, end) event pair
+  // around the mover launch(es) alone, for timing without host syncs
+  std::vector<cudaEvent_t> kt_ev;
+  int kt_cap = 0, kt_n = 0;
 };
 
 namespace b2m {

@@ -246,6 +246,8 @@ b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
   if (st != B2M_OK) return st;
   if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_broadcast_field: call b2m_world_init first");
   if (root < 0 || root >= ctx->sl.world) return fail(B2M_CONFIG_ERROR, "root rank out of range");
+  if (ctx->sl.world > 1 && !ctx->w.comm)
+    return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no NCCL communicator (world > 1)");
   if (ctx->sl.rank == root && !ctx->field_ready)
     return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no field uploaded on the root");
   if (ctx->w.comm) {
@@ -299,10 +301,15 @@ b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total) {
 
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count) {
-  b2m_status st = check_ctx(ctx);
-  if (st != B2M_OK) return st;
+  // Only argument errors that are the same on every rank return before the
+  // collectives.  Any per-rank failure -- a context poisoned earlier, a
+  // missing field, a launch or tensor-map error, a device fault -- is carried
+  // like a fault: empty outboxes, every round of the protocol still run, the
+  // flag in the closing all-reduce, so no peer waits in a collective alone.
+  if (!ctx) return fail(B2M_INVALID_ARGUMENT, "null context");
   if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_step: call b2m_world_init first");
   if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
+  b2m_status st;
   const int ns = static_cast<int>(ctx->sp.size());
   for (int s = 0; s < ns; ++s)
     if ((st = check_params(&mp[s])) != B2M_OK) return st;
@@ -310,8 +317,17 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
   const int prev = ctx->sl.prev, next = ctx->sl.next;
   const bool exchange = ctx->sl.world > 1;
   if (exchange && !w.comm) return fail(B2M_CONFIG_ERROR, "world_step: no NCCL communicator");
-  b2m_status own = world_move(ctx, mp);
-  if (own != B2M_OK && own != B2M_NUMERICAL_FAULT && own != B2M_CFL_VIOLATION) return own;
+  b2m_status own = check_ctx(ctx);
+  std::string own_msg = own == B2M_OK ? "" : b2m_last_error();
+  if (own != B2M_OK) cudaSetDevice(ctx->device);  // a poisoned rank still takes part
+  cudaEventRecord(ctx->ev[13], ctx->stream);
+  if (own == B2M_OK) {
+    own = world_move(ctx, mp);
+    if (own != B2M_OK) own_msg = b2m_last_error();
+  }
+  cudaEventRecord(ctx->ev[14], ctx->stream);
+  if (own != B2M_OK)  // nothing of this rank's step goes out (stale counts included)
+    cudaMemsetAsync(w.cnt_send, 0, 2 * ns * sizeof(unsigned long long), ctx->stream);
   // counts round
   if (exchange) {
     B2M_NCCL(ctx, nccl().GroupStart());
@@ -321,8 +337,10 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
     B2M_NCCL(ctx, nccl().Recv(w.cnt_recv + ns, ns, ncclUint64, next, w.comm, ctx->stream));
     B2M_NCCL(ctx, nccl().GroupEnd());
   }
-  if (own == B2M_OK) own = world_counts(ctx);  // host sync 1
-  else {
+  if (own == B2M_OK) {
+    own = world_counts(ctx);  // host sync 1
+    if (own != B2M_OK) own_msg = b2m_last_error();
+  } else {
     cudaMemcpyAsync(w.cnt_h, w.cnt_send, 2 * ns * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost, ctx->stream);
     cudaMemcpyAsync(w.cnt_h + 2 * ns, w.cnt_recv, 2 * ns * sizeof(unsigned long long),
@@ -351,7 +369,10 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
     B2M_NCCL(ctx, nccl().GroupEnd());
   }
   if (sent) *sent = world_sent(ctx);
-  if (own == B2M_OK) own = world_merge(ctx);
+  if (own == B2M_OK) {
+    own = world_merge(ctx);
+    if (own != B2M_OK) own_msg = b2m_last_error();
+  }
   // count check (runtime.cpp:264-269) with the fault flag riding along
   w.red_h[0] = own == B2M_OK ? static_cast<long long>(world_local_count(ctx)) : 0;
   w.red_h[1] = own == B2M_OK ? 0 : 1;
@@ -359,12 +380,14 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
     cudaMemcpyAsync(w.red, w.red_h, 2 * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream);
     B2M_NCCL(ctx, nccl().AllReduce(w.red, w.red, 2, ncclInt64, ncclSum, w.comm, ctx->stream));
     cudaMemcpyAsync(w.red_h, w.red, 2 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);  // host sync 2
   }
+  cudaEventRecord(ctx->ev[15], ctx->stream);
+  if (w.comm) cudaStreamSynchronize(ctx->stream);  // host sync 2
   if (own != B2M_OK && !ctx->poisoned) {  // e.g. an arrival overflowed the batch capacity
     ctx->poisoned = true;
-    ctx->poison_msg = std::string(b2m_last_error());
+    ctx->poison_msg = own_msg;
   }
+  if (own != B2M_OK) set_error(own_msg);
   return world_verdict(ctx, own, w.red_h[0], own == B2M_OK ? w.red_h[1] : 0, global_count);
 }
 
@@ -387,15 +410,27 @@ b2m_status b2m_world_loopback_step(b2m_ctx* const* ctxs, int world, const b2m_mo
     msg[static_cast<size_t>(r)] = b2m_last_error();
   }
   for (int r = 0; r < world; ++r) cudaStreamSynchronize(ctxs[r]->stream);
-  // counts: from prev = prev's to-next row, from next = next's to-prev row
+  // a failed rank sends nothing (b2m_world_step zeroes its counts too)
+  for (int r = 0; r < world; ++r)
+    if (own[static_cast<size_t>(r)] != B2M_OK)
+      cudaMemsetAsync(ctxs[r]->w.cnt_send, 0, 2 * ns * sizeof(unsigned long long),
+                      ctxs[r]->stream);
+  for (int r = 0; r < world; ++r) cudaStreamSynchronize(ctxs[r]->stream);
+  // counts: from prev = prev's to-next row, from next = next's to-prev row.
+  // With two ranks (prev == next) NCCL pairs the peer's messages with ours in
+  // posting order instead: from prev = its to-prev row, from next = its
+  // to-next row (b2m_world_step posts to-prev first); mirrored here.
+  const bool pair = world == 2;
   for (int r = 0; r < world; ++r) {
     b2m_ctx* me = ctxs[r];
     const b2m_ctx* p = ctxs[me->sl.prev];
     const b2m_ctx* n = ctxs[me->sl.next];
     const size_t b = ns * sizeof(unsigned long long);
     if (world > 1) {
-      cudaMemcpyAsync(me->w.cnt_recv, p->w.cnt_send + ns, b, cudaMemcpyDeviceToDevice, me->stream);
-      cudaMemcpyAsync(me->w.cnt_recv + ns, n->w.cnt_send, b, cudaMemcpyDeviceToDevice, me->stream);
+      cudaMemcpyAsync(me->w.cnt_recv, p->w.cnt_send + (pair ? 0 : ns), b,
+                      cudaMemcpyDeviceToDevice, me->stream);
+      cudaMemcpyAsync(me->w.cnt_recv + ns, n->w.cnt_send + (pair ? ns : 0), b,
+                      cudaMemcpyDeviceToDevice, me->stream);
     }
   }
   for (int r = 0; r < world; ++r) {
@@ -416,18 +451,20 @@ b2m_status b2m_world_loopback_step(b2m_ctx* const* ctxs, int world, const b2m_mo
   for (int r = 0; r < world; ++r) {
     b2m_ctx* me = ctxs[r];
     moved += world_sent(me);
-    if (world == 1) continue;
+    // a rank whose counts failed (an overflowing exchange buffer) receives
+    // nothing: its stage buffers may be smaller than the arrivals
+    if (world == 1 || own[static_cast<size_t>(r)] != B2M_OK) continue;
     const b2m_ctx* p = ctxs[me->sl.prev];
     const b2m_ctx* n = ctxs[me->sl.next];
     const unsigned long long* c = me->w.cnt_h;
     for (size_t s = 0; s < ns; ++s) {
       const size_t rec = 6 * sizeof(double);
       if (c[2 * ns + s])
-        cudaMemcpyAsync(me->w.stage[s], p->sp[s].out[1], c[2 * ns + s] * rec,
+        cudaMemcpyAsync(me->w.stage[s], p->sp[s].out[pair ? 0 : 1], c[2 * ns + s] * rec,
                         cudaMemcpyDeviceToDevice, me->stream);
       if (c[3 * ns + s])
-        cudaMemcpyAsync(me->w.stage[s] + 6 * c[2 * ns + s], n->sp[s].out[0], c[3 * ns + s] * rec,
-                        cudaMemcpyDeviceToDevice, me->stream);
+        cudaMemcpyAsync(me->w.stage[s] + 6 * c[2 * ns + s], n->sp[s].out[pair ? 1 : 0],
+                        c[3 * ns + s] * rec, cudaMemcpyDeviceToDevice, me->stream);
     }
   }
   for (int r = 0; r < world; ++r) cudaStreamSynchronize(ctxs[r]->stream);

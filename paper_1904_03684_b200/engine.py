@@ -71,6 +71,27 @@ class DeviceStore:
         _capi.check(_capi.lib().b2m_field_upload_device(self.h, C.c_void_p(dE), C.c_void_p(dB),
                                                         self.grid.nodes()))
 
+    def field_device_ptrs(self):
+        """(dE, dB) device pointers of this context's field buffers."""
+        e, b = C.c_void_p(), C.c_void_p()
+        _capi.check(_capi.lib().b2m_field_device_ptrs(self.h, C.byref(e), C.byref(b)))
+        return int(e.value), int(b.value)
+
+    def kernel_timing_begin(self, n: int):
+        """Log the mover-launch time of the next n move_all calls (no syncs)."""
+        _capi.check(_capi.lib().b2m_kernel_timing_begin(self.h, n))
+
+    def kernel_timing_read(self, max_n: int = 1 << 16):
+        buf = (C.c_float * max_n)()
+        n = C.c_int()
+        _capi.check(_capi.lib().b2m_kernel_timing_read(self.h, buf, max_n, C.byref(n)))
+        return [float(buf[i]) for i in range(n.value)]
+
+    def field_changed(self):
+        """The device field was rewritten in place (a device-side field phase):
+        the gather tables rebuild on the next move (no copy)."""
+        self.upload_field_device(*self.field_device_ptrs())
+
     def upload(self, s: int, p6, n: int | None = None):
         n = len(p6[0]) if n is None else n
         _capi.check(_capi.lib().b2m_species_upload(self.h, s, _capi.ptr6(p6), n))
@@ -80,6 +101,10 @@ class DeviceStore:
         _capi.check(_capi.lib().b2m_species_download(self.h, s, _capi.ptr6(p6), len(p6[0]),
                                                      C.byref(n)))
         return n.value
+
+    def download_range(self, s: int, p6, offset: int, n: int):
+        """Particles [offset, offset + n) of species s into host arrays."""
+        _capi.check(_capi.lib().b2m_species_download_range(self.h, s, _capi.ptr6(p6), offset, n))
 
     def count(self, s: int) -> int:
         n = C.c_uint64()

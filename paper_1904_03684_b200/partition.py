@@ -351,6 +351,9 @@ class NativeSlabWorld:
         self.last_exchange = {}
         self.total = None
         uid = (C.c_ubyte * 128)()
+        if world > 1 and dist is None:
+            raise ConfigError("NativeSlabWorld: world > 1 needs torch.distributed (dist) to "
+                              "share the NCCL unique id")
         if world > 1:
             if rank == 0:
                 _capi.check(_capi.lib().b2m_world_id(uid))
@@ -413,175 +416,3 @@ def loopback_step(stores, mps) -> int:
     sent = C.c_uint64()
     _capi.check(_capi.lib().b2m_world_loopback_step(hs, len(stores), arr, C.byref(sent)))
     return int(sent.value)
-
-
-# ---------------------------------------------------------------------------
-# multi-GPU benchmark (bench.py --gpus N under torchrun)
-# ---------------------------------------------------------------------------
-
-def bench_world(args) -> int:
-    """Weak scaling: grid (64, 64*N, 32), L = (25.6, 12.8*N, 6.4), 216 ppc, so
-    every rank owns a C2-sized slab (64x64x32 cells, ~56.6M background
-    particles; the Harris sheet species sit on the middle ranks).  A timed
-    step = mover + migration (NCCL P2P) + count all-reduce on every rank (the
-    static benchmark field is broadcast once, as the 1-GPU line uploads it once);
-    the time is the max over ranks of CUDA-event time."""
-    import torch
-    import torch.distributed as dist
-
-    from . import _capi, gem
-    from .engine import DeviceStore
-    from .mover import Grid, MoverParams
-
-    # B2M_DIST_BACKEND=gloo lets several ranks share fewer GPUs for functional
-    # checks (host-staged exchange); the benchmark itself uses NCCL
-    backend = os.environ.get("B2M_DIST_BACKEND", "nccl")
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        dist.init_process_group(backend)
-    rank, world = dist.get_rank(), dist.get_world_size()
-    grid = Grid.make(64, 64 * world, 32, 25.6, 12.8 * world, 6.4)
-    ppc = 216
-    sub = decompose(grid, world)[rank]
-    # this rank's slab of the reference GEM state (bit-identical generator,
-    # filtered by owner_of like Simulation::distribute, runtime.cpp:150-166)
-    batches = gem.init_gem_slab(grid, ppc, rank, world)
-    field = gem.gem_field(grid)
-    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
-    caps = [int(b.count() * 1.05) + 65536 for b in batches]
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    store = DeviceStore(grid, caps, args.mode, device=local)
-    store.set_stream(stream.cuda_stream)
-    store.upload_field(field)
-    for s, b in enumerate(batches):
-        store.upload(s, b.span())
-        store.sort(s)
-    # the per-cycle protocol runs in the library (b2m_world_step) over NCCL;
-    # B2M_NATIVE_WORLD=0 (or gloo) runs the Python SlabWorld over torch.distributed
-    native = backend == "nccl" and os.environ.get("B2M_NATIVE_WORLD", "1") != "0"
-    if native:
-        sw = NativeSlabWorld(grid, store, rank, world, dist)
-    else:
-        mig = DeviceMigration(store, rank, world)
-        sw = SlabWorld(grid, mig, len(batches), dist, torch.device("cuda", local))
-    sw.set_total()
-
-    def all_reduce(t, op=dist.ReduceOp.SUM):  # timing and count reductions
-        if backend == "gloo":
-            h = t.cpu()
-            dist.all_reduce(h, op=op)
-            t.copy_(h.to(t.device))
-        else:
-            dist.all_reduce(t, op=op)
-
-    # field replication: rank 0's device field is broadcast to every rank
-    # (runtime.cpp:143 replicates the mesh).  The benchmark field is static,
-    # like the single-GPU line's, so it is replicated once before timing; a
-    # simulation with a changing field calls replicate_field() every cycle.
-    nodes = grid.nodes()
-    fE = torch.empty(3 * nodes, dtype=torch.float64, device="cuda")
-    fB = torch.empty(3 * nodes, dtype=torch.float64, device="cuda")
-    if rank == 0:
-        fE.copy_(torch.from_numpy(field.E.ravel()))
-        fB.copy_(torch.from_numpy(field.B.ravel()))
-
-    def replicate_field():
-        if native:  # ncclBroadcast of the device field inside the library
-            sw.broadcast_field(0)
-            return
-        if backend == "nccl":
-            dist.broadcast(fE, 0)
-            dist.broadcast(fB, 0)
-        else:
-            for t in (fE, fB):
-                h = t.cpu()
-                dist.broadcast(h, 0)
-                t.copy_(h.to(t.device))
-        store.upload_field_device(fE.data_ptr(), fB.data_ptr())
-
-    replicate_field()
-    step_no = [0]
-
-    def step():
-        if args.resort and step_no[0] % args.resort == 0:
-            for s in range(len(batches)):
-                store.sort(s)
-        sw.step(mps)
-        step_no[0] += 1
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    l0 = _capi.lib().b2m_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    moved = 0
-    for _ in range(args.steps):
-        step()
-        moved += sw.last_exchange["sent"]
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item()) / args.steps
-    n_local = torch.tensor([sum(store.count(s) for s in range(len(batches)))], dtype=torch.int64,
-                           device="cuda")
-    all_reduce(n_local)
-    n_total = int(n_local.item())
-    launches = _capi.lib().b2m_launch_count() - l0
-
-    # e2e through the reference-facing engine API (pic::Engine contract,
-    # B200Engine.run_mover) with this rank's pinned host batches: H2D, mover,
-    # D2H every step; the job's time is the max over ranks
-    e2e = None
-    if getattr(args, "e2e_steps", 0) > 0:
-        import time
-        from .engine import B200Engine
-        eng = B200Engine(grid, mode=args.mode, schedule="pipeline", device=local)
-        eng.prime(field, batches)
-        eng.run_mover(field, batches, mps)  # warm-up
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            eng.run_mover(field, batches, mps)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        eng.close()
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-        n_here = torch.tensor([sum(b.count() for b in batches)], dtype=torch.int64, device="cuda")
-        all_reduce(n_here)
-        n_e2e = int(n_here.item())
-        e2e = {"value": n_e2e / e2e_s / 1e6, "unit": "MPA/s",
-               "h2d_bytes_per_step": 48 * n_e2e + world * 2 * 24 * grid.nodes(),
-               "d2h_bytes_per_step": 48 * n_e2e, "ms_per_step": e2e_s * 1e3,
-               "path": "B200Engine.run_mover per rank (pic::Engine contract) on the rank's "
-                       "pinned host batches; max over ranks"}
-    if rank == 0:
-        line = {"metric": "MPA/s in mover", "value": n_total / (ms_max * 1e-3) / 1e6,
-                "unit": "MPA/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic GEM state (reference init_gem generator), per-rank C2 slab",
-                "config": {"workload": f"GEM 64x{64 * world}x32, 216 ppc, y-slabs of 64 cells",
-                           "particles": n_total, "mode": args.mode,
-                           "cell_sort": f"every {args.resort} steps" if args.resort else "once",
-                           "parallelism": f"y-slab x{world}, {backend} P2P migration of all "
-                                          "species per step + count all-reduce ("
-                                          + ("native b2m_world_step" if native else
-                                             "Python SlabWorld") + "); static field "
-                                          "broadcast once",
-                           "migrated_per_step_rank0": moved / max(1, args.steps)},
-                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": None}
-        print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-    return 0

@@ -516,3 +516,34 @@ def test_nearly_zinvariant_field_takes_general_kernel(gpu):
     p0 = random_particles(grid, 50000, 31)
     check(gpu_move(p0, E, B, grid, 0.1, -25.0, 3, "fast"),
           port_move(p0, E, B, grid, 0.1, -25.0, 3), grid, "fast", "nearly z-invariant")
+
+
+@pytest.mark.parametrize("path", ["counting", "radix_fallback"])
+def test_sort_at_full_capacity_allocates_nothing(gpu, path, monkeypatch):
+    """The cell sort's buffers are reserved at context creation
+    (device_arena.cpp:20-55: AllocError at creation, never mid-run): sorting
+    species filled to exactly their capacity leaves free device memory
+    unchanged, and the result is the same multiset in cell order."""
+    import torch
+    if path == "radix_fallback":
+        monkeypatch.setenv("B2M_SORT_FALLBACK", "1")
+    g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
+    grid = g.as_tuple()
+    ps = [random_particles(grid, n, 40 + n) for n in (100000, 77777)]
+    st = DeviceStore(g, [len(p[0]) for p in ps], "fast")
+    st.upload_field(FieldMesh(g, *random_field(grid, 3, 0.3)))
+    for s, p in enumerate(ps):
+        st.upload(s, p)
+    st.sync()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for s in range(len(ps)):
+        st.sort(s)
+    st.sync()
+    assert torch.cuda.mem_get_info()[0] == free0, "the sort allocated device memory mid-run"
+    for s, p in enumerate(ps):
+        srt = [np.empty_like(a) for a in p]
+        assert st.download(s, srt) == len(p[0])
+        st.sync()
+        np.testing.assert_array_equal(oracle.multiset(srt), oracle.multiset(p))
+        assert np.all(np.diff(cells_of(srt, grid)) >= 0)

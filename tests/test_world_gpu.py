@@ -16,7 +16,7 @@ import pytest
 import oracle
 from paper_1904_03684_b200 import _capi, gem
 from paper_1904_03684_b200.engine import DeviceStore
-from paper_1904_03684_b200.errors import CflViolation, NumericalFault
+from paper_1904_03684_b200.errors import CflViolation, EngineFault, NumericalFault
 from paper_1904_03684_b200.mover import Grid, MoverParams
 from paper_1904_03684_b200.partition import (NativeSlabWorld, loopback_step, loopback_world,
                                              owner_of)
@@ -161,6 +161,37 @@ def test_world_api_misuse_is_config_error(gpu):
     with pytest.raises(ConfigError, match="already"):
         _capi.check(_capi.lib().b2m_world_init(st.h, None, 0, 2))
     with pytest.raises(ConfigError, match="NCCL communicator"):
+        _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
+    # a world of two without a communicator cannot replicate a field
+    with pytest.raises(ConfigError, match="no NCCL communicator"):
+        _capi.check(_capi.lib().b2m_world_broadcast_field(st.h, 0))
+    st.close()
+
+
+def test_world_step_per_rank_failure_runs_the_protocol(gpu):
+    """A per-rank failure (here: no field on this rank) is carried through the
+    collectives like a fault instead of returning before them (so peers never
+    wait alone): the typed error comes back, the context is poisoned, and the
+    next step reports EngineFault -- again after running the protocol."""
+    import torch.distributed as dist
+    from paper_1904_03684_b200.errors import ConfigError
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29547")
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    g = Grid.make(*GRID_T)
+    batches = gem.init_gem_slab(g, 8, 0, 1, pinned=False)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    st = DeviceStore(g, [b.count() + 64 for b in batches], "fast")
+    for s, b in enumerate(batches):
+        st.upload(s, b.span())
+    uid = (C.c_ubyte * 128)()
+    _capi.check(_capi.lib().b2m_world_id(uid))
+    _capi.check(_capi.lib().b2m_world_init(st.h, uid, 0, 1))
+    arr = (_capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+    with pytest.raises(ConfigError, match="no field"):
+        _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
+    with pytest.raises(EngineFault):
         _capi.check(_capi.lib().b2m_world_step(st.h, arr, None, None))
     st.close()
 
