@@ -45,6 +45,10 @@ def _load_state(grid, ppc, field):
     st.upload_field(field)
     g = grid.to_c()
     for s in range(4):
+        if s >= 2:  # the current-sheet species: generated whole (range fill is background-only)
+            b = gem.init_gem_species(grid, ppc, species=(s,))[0]
+            st.upload(s, b.span())
+            continue
         for m0 in range(0, counts[s], CHUNK):
             m1 = min(counts[s], m0 + CHUNK)
             arrs = [np.empty(m1 - m0) for _ in range(6)]
