@@ -281,6 +281,60 @@ def time_steps(store, mps, steps, refresh, events):
     return [(a.elapsed_time(b), k) for (a, b), k in zip(ev, kms)]
 
 
+def fused_cycle(store, mps, qs, ns, reps=3, drift=32):
+    """Mover + moment deposition (rho, J) of all species: one fused launch
+    (b2m_move_deposit_all: the deposit from the mover's shared-memory tile
+    through FP64 DMMA) against b2m_move_all + b2m_deposit per species and
+    against the plain mover, right after a cell sort and `drift` cycles
+    later.  Every call advances the state one cycle; the three are
+    interleaved so they see the same drift."""
+    import torch
+
+    def timed(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    def mover():
+        store.move_all(mps)
+
+    def separate():
+        store.moments_zero(False)
+        store.move_all(mps)
+        for s in range(ns):
+            store.deposit(s, qs[s])
+
+    def fused():
+        store.moments_zero(False)
+        store.move_deposit_all(mps, qs)
+
+    def measure():
+        t = {"mover": [], "separate": [], "fused": []}
+        for _ in range(reps):
+            t["mover"].append(timed(mover))
+            t["separate"].append(timed(separate))
+            t["fused"].append(timed(fused))
+        store.sync()
+        return {k: sum(v) / len(v) for k, v in t.items()}
+
+    for s in range(ns):
+        store.sort(s)
+    fused()  # warm-up
+    store.sync()
+    fresh = measure()
+    for _ in range(drift):
+        store.move_all(mps)
+    drifted = measure()
+    return {"fresh_ms": fresh, f"after_{drift}_cycles_ms": drifted,
+            "what": "ms per cycle of all C2 species: 'mover' = b2m_move_all alone; "
+                    "'separate' = b2m_move_all + b2m_deposit (rho, J) per species; 'fused' = "
+                    "b2m_move_deposit_all (one launch, deposit from the mover's tile via FP64 "
+                    "DMMA); fresh = right after a cell sort"}
+
+
 def c4_single_gpu(args, local, field_kind):
     """SURVEY C4 (255.8M particles) on this one GPU: the strong-scaling
     baseline T1 (plain mover + field refresh, no exchange)."""
@@ -431,7 +485,9 @@ def run_ours(args):
                            "after a cell sort",
                    "ms_drifted": drifted,
                    "drifted_what": "the same on the state the timed steps left",
-                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / peak}
+                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / peak,
+                   "fused": fused_cycle(store, mps, [b.q_per_particle for b in batches],
+                                        len(batches)) if args.mode == "fast" else None}
     store.close()
 
     # ---- e2e through the reference-facing engine API, host batches ----

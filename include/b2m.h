@@ -219,6 +219,17 @@ b2m_status b2m_field_phase_stub_host(const b2m_grid* g, double* E, double* B, in
  * reference's particle order: equal to rounding. */
 b2m_status b2m_moments_zero(b2m_ctx* ctx, int with_pressure);
 b2m_status b2m_deposit(b2m_ctx* ctx, int s, double q_per_particle);
+/* One mover cycle of all species followed by the deposition of their new
+ * state: the reference's move_batch per species then deposit_moments per
+ * species (runtime.cpp:227-229, :251-262; kernels.cpp:52-104, :147-183).
+ * FAST without pressure: ONE fused launch -- rho and J are deposited from the
+ * tile the mover just wrote, in shared memory, by FP64 DMMA (b2m_fused.cuh),
+ * so the particles are not re-read from HBM.  STRICT (bit-identical
+ * per-particle terms) or with pressure: b2m_move_all then b2m_deposit per
+ * species.  mp[n_species], q_per_particle[n_species]; b2m_moments_zero
+ * first.  Event slots 11 / 12 bracket the launch(es) as in b2m_move_all. */
+b2m_status b2m_move_deposit_all(b2m_ctx* ctx, const b2m_mover_params* mp,
+                                const double* q_per_particle);
 b2m_status b2m_moments_download(b2m_ctx* ctx, double* const* out, int n_arrays);
 /* Device view of the moment mesh: one contiguous block of n_doubles =
  * (4 or 10) * nx*ny*nz, arrays in the order above -- for reducing the

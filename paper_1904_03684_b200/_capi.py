@@ -90,6 +90,8 @@ SIGNATURES = {
     "b2m_field_phase_stub_host": (_st, [C.POINTER(b2m_grid), _dp, _dp, C.c_int]),
     "b2m_moments_zero": (_st, [C.c_void_p, C.c_int]),
     "b2m_deposit": (_st, [C.c_void_p, C.c_int, C.c_double]),
+    "b2m_move_deposit_all": (_st, [C.c_void_p, C.POINTER(b2m_mover_params),
+                                   C.POINTER(C.c_double)]),
     "b2m_moments_download": (_st, [C.c_void_p, C.POINTER(_dp), C.c_int]),
     "b2m_moments_device_ptr": (_st, [C.c_void_p, C.POINTER(_dp), C.POINTER(_u64)]),
     "b2m_deposit_moments_host": (_st, [C.POINTER(b2m_grid)] + [_dp] * 6 +

@@ -698,7 +698,8 @@ b2m_status b2m_move(b2m_ctx* ctx, int s, const b2m_mover_params* mp) {
   return b2m_move_range(ctx, s, mp, 0, ctx->sp[static_cast<size_t>(s)].count);
 }
 
-b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
+// b2m_move_all / b2m_move_deposit_all: qpp non-null = fused FAST deposit
+static b2m_status move_all_impl(b2m_ctx* ctx, const b2m_mover_params* mp, const double* qpp) {
   b2m_status st = check_ctx(ctx);
   if (st != B2M_OK) return st;
   if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
@@ -711,8 +712,12 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
     all[static_cast<size_t>(s)] = s;
   }
   ensure_tables(ctx, all.data(), mp, ns);
-  for (int s = 0; s < ns; ++s)
+  // kernels.cpp:148,162: qv = q_per_particle * (1 / cell_volume)
+  const double rvol = 1.0 / ((ctx->grid.dx * ctx->grid.dy) * ctx->grid.dz);
+  for (int s = 0; s < ns; ++s) {
     L.push_back(make_launch(ctx, s, mp[s], 0, ctx->sp[static_cast<size_t>(s)].count));
+    if (qpp) L.back().qv = qpp[s] * rvol;
+  }
   const double* nodes = ctx->mode == B2M_MODE_STRICT ? strict_nodes(ctx) : nullptr;
   // slots 11 / 12 (and the kernel-timing log) bracket the mover launch(es)
   // alone, after any table rebuild
@@ -724,11 +729,31 @@ b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
                                   ctx->fault, ctx->stream))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault, ctx->stream,
-                               nullptr, nullptr, nullptr, ctx->zvar))
+                               nullptr, nullptr, nullptr, ctx->zvar,
+                               qpp ? ctx->mom : nullptr))
     return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   B2M_CUDA(ctx, cudaEventRecord(ctx->ev[12], ctx->stream));
   if (kt >= 0) B2M_CUDA(ctx, cudaEventRecord(ctx->kt_ev[2 * kt + 1], ctx->stream));
   B2M_CUDA(ctx, cudaGetLastError());
+  return B2M_OK;
+}
+
+b2m_status b2m_move_all(b2m_ctx* ctx, const b2m_mover_params* mp) {
+  return move_all_impl(ctx, mp, nullptr);
+}
+
+b2m_status b2m_move_deposit_all(b2m_ctx* ctx, const b2m_mover_params* mp,
+                                const double* q_per_particle) {
+  b2m_status st = check_ctx(ctx);
+  if (st != B2M_OK) return st;
+  if (!q_per_particle) return fail(B2M_INVALID_ARGUMENT, "null q_per_particle");
+  if (!ctx->mom[0]) return fail(B2M_CONFIG_ERROR, "deposit: call b2m_moments_zero first");
+  if (ctx->mode == B2M_MODE_FAST && !ctx->mom_pressure)
+    return move_all_impl(ctx, mp, q_per_particle);
+  // STRICT terms or the pressure tensor: the mover, then the deposit kernels
+  if ((st = move_all_impl(ctx, mp, nullptr)) != B2M_OK) return st;
+  for (int s = 0; s < static_cast<int>(ctx->sp.size()); ++s)
+    if ((st = b2m_deposit(ctx, s, q_per_particle[s])) != B2M_OK) return st;
   return B2M_OK;
 }
 

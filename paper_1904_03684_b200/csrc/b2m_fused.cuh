@@ -1,0 +1,223 @@
+// b2m_fused.cuh — moment deposition fused into the FAST mover's tile loop
+// (deposit_moments, kernels.cpp:147-183, of the state the
+// mover just produced, without re-reading the particles from HBM).
+//
+// After a row of 32 particles (one per lane) has been moved in the tile's
+// shared-memory stage, the warp deposits rho and J of the NEW positions and
+// velocities.  The per-cell sums are a small matrix product: for the particles
+// of one cell,
+//     D[c][m] = sum_p W[c][p] * Mom[p][m],   c = corner 0..7, m = {1, u, v, w}
+// with W[c][p] = qv * wx * wy * wz the corner weight (kernels.cpp:168).  That
+// is an FP64 mma.sync m8n8k4 (DMMA, the tensor-core FP64 path of sm_100a)
+// over k = 4 particles at a time -- 8 per row of 32 -- with the 8x8 f64
+// accumulator held in TWO registers per lane.  That register economy is the
+// point: a per-lane register carry of the 32 sums (the separate deposit
+// kernel's design, 64 registers) does not fit beside the mover's column cache
+// at the mover's residency, and a shared-memory transpose of 32 terms per
+// particle costs 512 B of shared traffic per particle.
+//
+// The 8 accumulator columns hold two cells: columns 0-3 the warp's CARRIED
+// cell (the row's largest group; kept across rows and tiles while it stays
+// the largest), columns 4-7 the row's largest other group, flushed (one FP64
+// atomic per corner and moment) right after the pass.  Every row is ONE pass
+// of 8 DMMAs; particles in neither cell (strays drifted out of the sorted
+// order) add their 32 terms with direct atomics, all such lanes at once.  A
+// row whose particles all sit in the carried cell -- the common case after a
+// sort -- costs no atomics at all.
+//
+// Per lane, the A fragment (row c = lane/4, k = lane%4) is the corner-c weight
+// of particle 4k' + lane%4, built from 6 staged factors (qv*wx*wy for the 4
+// (dx, dy) corners, wz for the 2 dz) -- 1.5 KB of shared memory per warp; the
+// B fragment (k = lane%4, n = lane/4) is that particle's moment n%4 (1, or its
+// new u, v, w read from the tile stage), or 0 when it is not in the column
+// half's cell.  Locate and weights follow the FAST deposit (1/d scaling,
+// trunc, clamp, min(f, 1)); sums are in DMMA order, so the mesh matches the
+// separate deposit to rounding of the sums.
+#pragma once
+
+#include "b2m_tile.cuh"
+
+namespace b2m {
+
+#ifndef B2M_DEP_PASSES
+#define B2M_DEP_PASSES 0  // extra DMMA passes per row for groups of >= 2 beyond the first
+#endif
+constexpr int kDepStage = 6 * 32;  // staged weight factors per warp (doubles)
+
+struct DepCarry {
+  double d0, d1;   // DMMA accumulator: D[lane/4][2*(lane%4) + {0, 1}]
+  long long key;   // carried cell (warp-uniform), -1: none
+  int ci, cj, ck;  // its indices
+};
+
+__device__ __forceinline__ void dep_reset(DepCarry& C) {
+  C.d0 = C.d1 = 0.0;
+  C.key = -1;
+  C.ci = C.cj = C.ck = 0;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Add one half of the accumulator (columns 4h..4h+3: m = 0..3 of cell
+// (ci, cj, ck)) to the mesh and clear it.  Lane l holds D[c][n] for c = l/4,
+// n = 2(l%4) + e; the half's values sit on the lanes with (l%4)/2 == h.
+__device__ __forceinline__ void dep_flush_half(double& d0, double& d1, int h, int ci, int cj,
+                                               int ck, const FastGrid& g,
+                                               double* const* mom, int lane) {
+  const int q = lane & 3;
+  if ((q >> 1) != h) return;
+  const int c = lane >> 2;
+  const int ii = (c & 1) ? (ci + 1 == g.nx ? 0 : ci + 1) : ci;
+  const int jj = (c & 2) ? (cj + 1 == g.ny ? 0 : cj + 1) : cj;
+  const int kk = (c & 4) ? (ck + 1 == g.nz ? 0 : ck + 1) : ck;
+  const long long node = ii + static_cast<long long>(g.nx) * (jj + static_cast<long long>(g.ny) * kk);
+  const int m0 = (2 * q) & 3;  // moment of d0 (d1: m0 + 1)
+  atomicAdd(mom[m0] + node, d0);
+  atomicAdd(mom[m0 + 1] + node, d1);
+  d0 = 0.0;
+  d1 = 0.0;
+}
+
+// One pass: D[:, 0:4] += carried-cell members' terms, D[:, 4:8] += group
+// `g1` members' terms (masks over the row's 32 particles).
+template <int TILE>
+__device__ __forceinline__ void dep_pass(DepCarry& C, const double* sw, double (*buf)[TILE],
+                                         int row0, unsigned carry_mask, unsigned g1_mask,
+                                         int lane) {
+  const int q = lane & 3;     // A: k column / B: k row
+  const int n = lane >> 2;    // A: corner row / B: column
+  const int m = n & 3;        // moment of the B column
+  const unsigned mask = (n >> 2) ? g1_mask : carry_mask;
+  const int cxy = n & 3, cz = n >> 2;  // A: corner n = cxy + 4 cz
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int pl = 4 * k + q;  // particle of this fragment element, within the row
+    const double a = sw[cxy * 32 + pl] * sw[(4 + cz) * 32 + pl];
+    double b = 0.0;
+    if ((mask >> pl) & 1u) b = m == 0 ? 1.0 : buf[2 + m][row0 + pl];
+    dmma_8x8x4(C.d0, C.d1, a, b);
+  }
+}
+
+// Deposit the 32 particles of row `row0` (this lane's particle p = row0 +
+// lane) after the mover wrote them back to the tile stage; `ok` = the
+// particle exists and moved clean.  All 32 lanes must call it together.
+template <int TILE>
+__device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double qv,
+                                        double* const* mom, double* sw, double (*buf)[TILE],
+                                        int row0, bool ok, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int p = row0 + lane;
+  // FAST deposit locate (b2m_moments.cu, grid.hpp:64-82 with 1/d scaling)
+  const double sx = buf[0][p] * g.rdx, sy = buf[1][p] * g.rdy, sz = buf[2][p] * g.rdz;
+  int i = min(__double2int_rz(sx), g.nx - 1), j = min(__double2int_rz(sy), g.ny - 1),
+      k = min(__double2int_rz(sz), g.nz - 1);
+  i = max(i, 0);
+  j = max(j, 0);
+  k = max(k, 0);
+  const double fx = fmin(sx - static_cast<double>(i), 1.0);
+  const double fy = fmin(sy - static_cast<double>(j), 1.0);
+  const double fz = fmin(sz - static_cast<double>(k), 1.0);
+  // a particle that is not deposited stages zeros (B masks it, but 0 * NaN
+  // from a faulted particle's weights would still poison the accumulator)
+  const double qw = ok ? qv : 0.0, ow = ok ? 1.0 : 0.0;
+  const double wx0 = qw * (1.0 - fx), wx1 = qw * fx;
+  sw[0 * 32 + lane] = wx0 * (1.0 - fy);
+  sw[1 * 32 + lane] = wx1 * (1.0 - fy);
+  sw[2 * 32 + lane] = wx0 * fy;
+  sw[3 * 32 + lane] = wx1 * fy;
+  sw[4 * 32 + lane] = ow * (1.0 - fz);
+  sw[5 * 32 + lane] = ow * fz;
+  const long long key =
+      ok ? i + static_cast<long long>(g.nx) * (j + static_cast<long long>(g.ny) * k) : -1;
+  const unsigned okm = __ballot_sync(FULL, ok);
+  __syncwarp();
+  if (okm == 0) return;
+  const unsigned grp = __match_any_sync(FULL, key);
+  // the carried cell: kept while it still holds the row's largest group (or
+  // ties it), else the largest group's cell takes over (ties: the group of
+  // the row's last particle -- the sorted order continues there)
+  const unsigned score = ok ? (static_cast<unsigned>(__popc(grp)) << 6) |
+                                  (((grp >> 31) & 1u) << 5) | static_cast<unsigned>(lane)
+                            : 0u;
+  const unsigned best = __reduce_max_sync(FULL, score);
+  const int bl = best & 31;
+  const int ncar = __popc(__ballot_sync(FULL, ok && key == C.key));
+  if (ncar < static_cast<int>(best >> 6)) {
+    if (C.key >= 0) dep_flush_half(C.d0, C.d1, 0, C.ci, C.cj, C.ck, g, mom, lane);
+    C.key = __shfl_sync(FULL, key, bl);
+    C.ci = __shfl_sync(FULL, i, bl);
+    C.cj = __shfl_sync(FULL, j, bl);
+    C.ck = __shfl_sync(FULL, k, bl);
+  }
+  const unsigned carry = __ballot_sync(FULL, ok && key == C.key);
+  unsigned rest = okm & ~carry;
+  // the largest other group rides in columns 4-7 of the same pass
+  unsigned g1 = 0u;
+  int gi = 0, gj = 0, gk = 0;
+  if (rest) {
+    const unsigned s2 = ((rest >> lane) & 1u)
+                            ? (static_cast<unsigned>(__popc(grp)) << 6) | static_cast<unsigned>(lane)
+                            : 0u;
+    const int leader = __reduce_max_sync(FULL, s2) & 31;
+    g1 = __shfl_sync(FULL, grp, leader);
+    gi = __shfl_sync(FULL, i, leader);
+    gj = __shfl_sync(FULL, j, leader);
+    gk = __shfl_sync(FULL, k, leader);
+    rest &= ~g1;
+  }
+  dep_pass<TILE>(C, sw, buf, row0, carry, g1, lane);
+  if (g1) dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
+  // further passes for groups of >= 2 (B2M_DEP_PASSES of them, largest first)
+#pragma unroll 1
+  for (int x = 0; x < B2M_DEP_PASSES && rest; ++x) {
+    const unsigned s2 = ((rest >> lane) & 1u)
+                            ? (static_cast<unsigned>(__popc(grp & rest)) << 6) |
+                                  static_cast<unsigned>(lane)
+                            : 0u;
+    const unsigned b2 = __reduce_max_sync(FULL, s2);
+    if ((b2 >> 6) < 2) break;
+    const int leader = b2 & 31;
+    const unsigned gm = __shfl_sync(FULL, grp, leader);
+    gi = __shfl_sync(FULL, i, leader);
+    gj = __shfl_sync(FULL, j, leader);
+    gk = __shfl_sync(FULL, k, leader);
+    rest &= ~gm;
+    dep_pass<TILE>(C, sw, buf, row0, 0u, gm, lane);
+    dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
+  }
+  if (rest) {
+    // everything else (strays drifted out of the sorted order): each lane
+    // adds its own particle's 32 terms to the mesh, all lanes at once
+    if ((rest >> lane) & 1u) {
+      const double u = buf[3][p], v = buf[4][p], w = buf[5][p];
+      const int i1 = i + 1 == g.nx ? 0 : i + 1, j1 = j + 1 == g.ny ? 0 : j + 1,
+                k1 = k + 1 == g.nz ? 0 : k + 1;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double wq = sw[(c & 3) * 32 + lane] * sw[(4 + (c >> 2)) * 32 + lane];
+        const long long node =
+            ((c & 1) ? i1 : i) +
+            static_cast<long long>(g.nx) *
+                (((c & 2) ? j1 : j) + static_cast<long long>(g.ny) * ((c & 4) ? k1 : k));
+        atomicAdd(mom[0] + node, wq);
+        atomicAdd(mom[1] + node, wq * u);
+        atomicAdd(mom[2] + node, wq * v);
+        atomicAdd(mom[3] + node, wq * w);
+      }
+    }
+  }
+  __syncwarp();  // the stage is rewritten by the next row
+}
+
+__device__ __forceinline__ void dep_finish(DepCarry& C, const FastGrid& g, double* const* mom,
+                                           int lane) {
+  if (C.key >= 0) dep_flush_half(C.d0, C.d1, 0, C.ci, C.cj, C.ck, g, mom, lane);
+  C.key = -1;
+}
+
+}  // namespace b2m

@@ -35,7 +35,8 @@ struct SlabLaunch;
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp,
                       int n_spans, FaultWord* fault, cudaStream_t st,
                       const SlabLaunch* sl = nullptr, uint8_t* const* flags = nullptr,
-                      unsigned long long* const* tcnt = nullptr, const int* zvar = nullptr);
+                      unsigned long long* const* tcnt = nullptr, const int* zvar = nullptr,
+                      double* const* mom = nullptr);
 // STRICT mover on the same warp-tile pipeline (bit-identical to the reference)
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,

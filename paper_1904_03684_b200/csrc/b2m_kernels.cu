@@ -20,6 +20,7 @@
 
 #include "b2m_internal.hpp"
 #include "b2m_tile.cuh"
+#include "b2m_fused.cuh"
 
 namespace b2m {
 
@@ -61,13 +62,18 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
 #define B2M_J_UNROLL 1
 #endif
 constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
+#ifndef B2M_2D_PAIR
+#define B2M_2D_PAIR 0          // 1: two particles per lane at a time (measured slower: spills)
+#endif
 #ifndef B2M_2D_MINBLOCKS
-#define B2M_2D_MINBLOCKS 4     // z-invariant FAST kernel: 24-double column cache
+#define B2M_2D_MINBLOCKS (B2M_2D_PAIR ? 3 : 4)  // z-invariant FAST kernel: 24-double column cache
 #endif
 // DIM: 3 = general FAST (or STRICT), 2 = z-invariant FAST.  The two FAST
 // kernels are launched back to back; each reads the field's z-invariance
 // flag (zinv_check_kernel) and the one that does not apply exits at once.
-template <int P, bool STRICT, int DIM>
+// DEP: FAST only -- deposit rho and J of the moved particles in the tile loop
+// (b2m_fused.cuh) into F.mom.
+template <int P, bool STRICT, int DIM, bool DEP>
 __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2M_FAST_MINBLOCKS)
     warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
                      const __grid_constant__ SlabLaunch sl, unsigned long long total_tiles,
@@ -80,6 +86,10 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
   auto buf = reinterpret_cast<double(*)[6][WT]>(wt_smem) + warp * kWarpStages;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wt_smem + WARPS * kWarpStages * 6 * WT * 8) +
                   warp * kWarpStages;
+  double* const sw = reinterpret_cast<double*>(wt_smem + WARPS * kWarpStages * (6 * WT * 8 + 8)) +
+                     warp * kDepStage;  // DEP only
+  DepCarry dc;
+  if (DEP) dep_reset(dc);
   // tiles round-robin over all warps of the grid: at any moment the whole GPU
   // streams one contiguous window of the particle arrays (DRAM-friendly)
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * WARPS + warp;
@@ -157,13 +167,11 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       fast_col_reset(C);
       uint8_t* flags = S.flags[s];
       const double* cols = reinterpret_cast<const double*>(sp.cells);
-#pragma unroll 1
-      for (int j = 0; j < P; ++j) {
+      // per moved particle: fault record, fused deposit, migration flag
+      auto after = [&](int j, unsigned bad) {
         const int p = lane + 32 * j;
-        const unsigned bad =
-            F.U.rounds == 3 ? fast_particle_2d<WT, 3>(F.fg, F.U, cols, buf[st], p, cnt, C)
-                            : fast_particle_2d<WT, 0>(F.fg, F.U, cols, buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (DEP) dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, buf[st], 32 * j, p < cnt && !bad, lane);
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
@@ -176,6 +184,26 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           flags[off + p] = static_cast<uint8_t>(flag);
           n_prev += flag == 1;
           n_next += flag == 2;
+        }
+      };
+      if (B2M_2D_PAIR && (P % 2) == 0) {
+        // two particles per lane at a time (ILP 2, b2m_tile.cuh fast_pair_2d)
+#pragma unroll 1
+        for (int j = 0; j < P; j += 2) {
+          const int pa = lane + 32 * j, pb = pa + 32;
+          const unsigned bad2 =
+              F.U.rounds == 3
+                  ? fast_pair_2d<WT, 3>(F.fg, F.U, cols, buf[st], pa, pb, cnt, C)
+                  : fast_pair_2d<WT, 0>(F.fg, F.U, cols, buf[st], pa, pb, cnt, C);
+          after(j, bad2 & 1u);
+          after(j + 1, bad2 >> 1);
+        }
+      } else {
+#pragma unroll 1
+        for (int j = 0; j < P; ++j) {
+          const int p = lane + 32 * j;
+          after(j, F.U.rounds == 3 ? fast_particle_2d<WT, 3>(F.fg, F.U, cols, buf[st], p, cnt, C)
+                                   : fast_particle_2d<WT, 0>(F.fg, F.U, cols, buf[st], p, cnt, C));
         }
       }
     } else if (B2M_FAST_V == 2) {
@@ -191,6 +219,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
             F.U.rounds == 3 ? fast_particle_v2<WT, 3>(F.fg, F.U, cells, buf[st], p, cnt, C)
                             : fast_particle_v2<WT, 0>(F.fg, F.U, cells, buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
+        if (DEP) dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, buf[st], 32 * j, p < cnt && !bad, lane);
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
@@ -270,6 +299,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       phase ^= 1u;
     }
   }
+  if (DEP) dep_finish(dc, F.fg, F.mom, lane);
   if (lane == 0) tma_wait_all();
 }
 
@@ -384,7 +414,7 @@ __global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const doubl
     const int ci = min(__double2int_rz(cx), g.nx - 1);
     const int cj = min(__double2int_rz(cy), g.ny - 1);
     const int ck = min(__double2int_rz(cz), g.nz - 1);
-    key = static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
+    key = static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj));  // see cell_key
   }
   keys[i] = key;
   vals[i] = static_cast<uint32_t>(i);
@@ -398,6 +428,15 @@ __global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const doubl
 // over the lanes of a warp that share a cell (__match_any_sync), so a
 // cell-ordered species costs a few atomics per warp.  One read of the
 // positions, one read and one write of the six arrays: HBM-bound.
+//
+// Sort order: z fastest, then x, then y -- key k + nz*(i + nx*j).  Any cell
+// order keeps a cell's particles together (all the deposit and the 3-D cell
+// cache need); this one also keeps an x-y column's nz cells together, so the
+// z-invariant mover's column cache (b2m_tile.cuh) meets a new column once per
+// column (~7000 particles per species at C2) instead of once per cell (~216):
+// with cells in the reference's index order (x fastest) a lane's next
+// particle changed column ~15 % of the time and nearly every warp took the
+// reload path.  y slowest also groups a y-slab's particles.
 __device__ __forceinline__ uint32_t cell_key(const FastGrid& g, double x, double y, double z) {
   const double cx = x * g.rdx, cy = y * g.rdy, cz = z * g.rdz;
   uint32_t key = static_cast<uint32_t>(static_cast<long long>(g.nx) * g.ny * g.nz);
@@ -405,7 +444,7 @@ __device__ __forceinline__ uint32_t cell_key(const FastGrid& g, double x, double
     const int ci = min(__double2int_rz(cx), g.nx - 1);
     const int cj = min(__double2int_rz(cy), g.ny - 1);
     const int ck = min(__double2int_rz(cz), g.nz - 1);
-    key = static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
+    key = static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj));
   }
   return key;
 }
@@ -558,13 +597,14 @@ bool encode_species_map(CUtensorMap* map, const SpeciesLaunch& sp, int box_cols)
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool STRICT, int DIM>
+template <bool STRICT, int DIM, bool DEP = false>
 bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                        cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
                        unsigned long long* const* tcnt) {
   constexpr int P = B2M_FAST_PPT;
   constexpr int WT = 32 * P;
-  constexpr int smem = (kWarpThreads / 32) * kWarpStages * (6 * WT * 8 + 8);
+  constexpr int smem = (kWarpThreads / 32) * (kWarpStages * (6 * WT * 8 + 8) +
+                                              (DEP ? kDepStage * 8 : 0));
   static_assert(smem <= 227 * 1024, "warp tiles exceed shared memory");
   // resident grid, computed once (thread-safe static initialisation: engines
   // on several host threads may launch concurrently)
@@ -572,9 +612,9 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(warp_tile_kernel<P, STRICT, DIM>,
+    cudaFuncSetAttribute(warp_tile_kernel<P, STRICT, DIM, DEP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT, DIM>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_tile_kernel<P, STRICT, DIM, DEP>,
                                                   kWarpThreads, smem);
     int cap = sms * (per_sm > 0 ? per_sm : 1);
     // diagnostics: B2M_BLOCKS_PER_SM=k runs the persistent grid with k blocks per SM
@@ -618,7 +658,7 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
     constexpr unsigned long long WPB = kWarpThreads / 32;
     const unsigned long long blocks = (tiles + WPB - 1) / WPB;
     const int grid = static_cast<int>(blocks < static_cast<unsigned long long>(grid_cap) ? blocks : grid_cap);
-    warp_tile_kernel<P, STRICT, DIM><<<grid, kWarpThreads, smem, st>>>(FL, S, sl ? *sl : SlabLaunch{},
+    warp_tile_kernel<P, STRICT, DIM, DEP><<<grid, kWarpThreads, smem, st>>>(FL, S, sl ? *sl : SlabLaunch{},
                                                                    tiles, fault);
     note_launch();
   }
@@ -627,10 +667,16 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
 
 bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                       cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
-                      unsigned long long* const* tcnt, const int* zvar) {
+                      unsigned long long* const* tcnt, const int* zvar, double* const* mom) {
   TileField F{};
   F.fg = g;
   F.zvar = zvar;
+  if (mom) {
+    for (int m = 0; m < 4; ++m) F.mom[m] = mom[m];
+    if (zvar && !launch_warp_tiles<false, 2, true>(F, sp, n_spans, fault, st, sl, flags, tcnt))
+      return false;
+    return launch_warp_tiles<false, 3, true>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+  }
   // both FAST kernels; the one the field's z-invariance flag rules out exits
   // at its first instruction (no host round trip to decide)
   if (zvar && !launch_warp_tiles<false, 2>(F, sp, n_spans, fault, st, sl, flags, tcnt))

@@ -138,6 +138,7 @@ struct TileField {
   const double* nodes;   // STRICT: per-cell corner node values (strict_nodes_kernel)
   FastUniform U;
   const int* zvar;       // FAST: device flag, 0 = field z-invariant (null: general kernel only)
+  double* mom[4];        // fused deposit (b2m_fused.cuh): rho, jx, jy, jz mesh arrays
 };
 
 // FAST launch: per span a 2-D tensor map over the species' [6][stride]
@@ -705,6 +706,149 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
     return 0u;
   }
   return p < cnt ? 1u : 0u;
+}
+
+// ---- two particles per lane (ILP 2) on one column cache ------------------
+//
+// The lane's particles j and j+1 of a tile (32 apart in a cell-sorted
+// species, i.e. nearly always in the same column: a C2 column holds ~7000
+// particles per species) are advanced together, their dependency chains
+// interleaved.  Each particle keeps its own cell frame (corner, column,
+// fractions) exactly as fast_particle_2d does, so its arithmetic -- and
+// result -- is the same bit for bit; the shared cache is (re)loaded for a
+// particle's column before that particle's gather when it is not the cached
+// one (load-only branches, rare), so two particles in different columns
+// still move correctly, only with reloads.
+struct PairP {
+  double u0, v0, w0;
+  double fx0, fy0, fx, fy;  // fractions in the particle's own cell frame
+  double ci, cj;            // that cell's corner (cell units)
+  double nx, ny, nz, rc;
+  int col;
+  unsigned bad;
+};
+
+__device__ __forceinline__ void pair_locate2(const FastGrid& g, double tx, double ty, PairP& P) {
+  const int i = max(min(__double2int_rz(tx), g.nx - 1), 0);
+  const int j = max(min(__double2int_rz(ty), g.ny - 1), 0);
+  P.ci = static_cast<double>(i);
+  P.cj = static_cast<double>(j);
+  P.fx = tx - P.ci;
+  P.fy = ty - P.cj;
+  P.col = i + g.nx * j;
+}
+
+__device__ __forceinline__ void pair_cache(FastCol& C, const double* __restrict__ cols,
+                                           const PairP& P) {
+  if (P.col != C.col) {
+    const double* c = cols + static_cast<long long>(P.col) * 24;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) C.K[q] = load_coef4(c + 4 * q);
+    C.col = P.col;
+    C.ci = P.ci;
+    C.cj = P.cj;
+  }
+}
+
+template <int TILE>
+__device__ __forceinline__ void pair_start(const FastGrid& g, const FastCol& C,
+                                           double (*buf)[TILE], int p, int cnt, PairP& P) {
+  const double x0 = buf[0][p], y0 = buf[1][p], z0 = buf[2][p];
+  P.u0 = buf[3][p];
+  P.v0 = buf[4][p];
+  P.w0 = buf[5][p];
+  P.bad = 0u;
+  const double cx = x0 * g.rdx, cy = y0 * g.rdy;
+  P.fx = cx - C.ci;
+  P.fy = cy - C.cj;
+  P.ci = C.ci;
+  P.cj = C.cj;
+  P.col = C.col;
+  if (!((p < cnt) & below_bits(x0, dbits(g.lx)) & below_bits(y0, dbits(g.ly)) &
+        below_bits(z0, dbits(g.lz)) & in_unit(P.fx) & in_unit(P.fy))) {
+    const bool inside = (p < cnt) && in_range(x0, dbits(g.lx)) && in_range(y0, dbits(g.ly)) &&
+                        in_range(z0, dbits(g.lz));
+    P.bad = inside ? 0u : 1u;
+    pair_locate2(g, inside ? cx : 0.0, inside ? cy : 0.0, P);
+  }
+  P.fx0 = P.fx;
+  P.fy0 = P.fy;
+}
+
+template <int TILE>
+__device__ __forceinline__ void pair_predict(const FastGrid& g, const FastUniform& U,
+                                             double (*buf)[TILE], int p, PairP& P) {
+  // kernels.cpp:92: a non-finite predictor is a fault (z included)
+  if (!finite3(P.nz, P.rc, P.rc)) P.bad = 1u;
+  P.fx = fma(P.nx * U.dc[0], P.rc, P.fx0);
+  P.fy = fma(P.ny * U.dc[1], P.rc, P.fy0);
+  if (!(in_unit(P.fx) & in_unit(P.fy))) {
+    const double bx = P.nx * P.rc, by = P.ny * P.rc;
+    const double cx = lds_f64(&buf[0][p]) * g.rdx, cy = lds_f64(&buf[1][p]) * g.rdy;
+    double tx = fma(bx, U.dc[0], cx), ty = fma(by, U.dc[1], cy);
+    if ((dbits(tx) >= dbits(g.nxd)) | (dbits(ty) >= dbits(g.nyd))) {
+      tx = fold_fast(tx, g.nxd, dbits(g.nxd), g.rnx, P.bad);
+      ty = fold_fast(ty, g.nyd, dbits(g.nyd), g.rny, P.bad);
+    }
+    pair_locate2(g, tx, ty, P);
+    P.fx0 = fma(-bx, U.dc[0], P.fx);
+    P.fy0 = fma(-by, U.dc[1], P.fy);
+  }
+}
+
+template <int TILE>
+__device__ __forceinline__ unsigned pair_finish(const FastGrid& g, const FastUniform& U,
+                                                double (*buf)[TILE], int p, int cnt, PairP& P) {
+  const double bx = P.nx * P.rc, by = P.ny * P.rc, bz = P.nz * P.rc;
+  double x1 = fma(bx, U.dt, lds_f64(&buf[0][p]));
+  double y1 = fma(by, U.dt, lds_f64(&buf[1][p]));
+  double z1 = fma(bz, U.dt, lds_f64(&buf[2][p]));
+  const double u1 = fma(2.0, bx, -P.u0);
+  const double v1 = fma(2.0, by, -P.v0);
+  const double w1 = fma(2.0, bz, -P.w0);
+  const bool fin_v = finite3(u1, v1, w1);
+  if (!((dbits(x1) <= dbits(g.ax.hi0)) & (dbits(y1) <= dbits(g.ay.hi0)) &
+        (dbits(z1) <= dbits(g.az.hi0)))) {
+    x1 = wrap_exact_bits(x1, g.ax, dbits(g.ax.hi0), dbits(g.ax.hi1), dbits(g.ax.lom1) & kAbs);
+    y1 = wrap_exact_bits(y1, g.ay, dbits(g.ay.hi0), dbits(g.ay.hi1), dbits(g.ay.lom1) & kAbs);
+    z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
+    if (!finite3(x1, y1, z1)) P.bad = 1u;
+  }
+  if ((P.bad == 0u) & fin_v) {
+    buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
+    buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;
+    return 0u;
+  }
+  return p < cnt ? 1u : 0u;
+}
+
+// Particles pa and pb of the tile; returns the fault bits (1: pa, 2: pb).
+template <int TILE, int ROUNDS>
+__device__ __forceinline__ unsigned fast_pair_2d(const FastGrid& g, const FastUniform& U,
+                                                 const double* __restrict__ cols,
+                                                 double (*buf)[TILE], int pa, int pb, int cnt,
+                                                 FastCol& C) {
+  PairP A, B;
+  pair_start<TILE>(g, C, buf, pa, cnt, A);
+  pair_start<TILE>(g, C, buf, pb, cnt, B);
+  const int rounds = ROUNDS > 0 ? ROUNDS : U.rounds;
+#pragma unroll
+  for (int r = 0; r < rounds; ++r) {
+    double Fa[6], Fb[6];
+    pair_cache(C, cols, A);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Fa[q] = poly4(C.K[q], A.fx, A.fy);
+    pair_cache(C, cols, B);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Fb[q] = poly4(C.K[q], B.fx, B.fy);
+    implicit_num(A.u0, A.v0, A.w0, Fa, A.nx, A.ny, A.nz, A.rc);
+    implicit_num(B.u0, B.v0, B.w0, Fb, B.nx, B.ny, B.nz, B.rc);
+    if (r + 1 < rounds) {
+      pair_predict<TILE>(g, U, buf, pa, A);
+      pair_predict<TILE>(g, U, buf, pb, B);
+    }
+  }
+  return pair_finish<TILE>(g, U, buf, pa, cnt, A) | (pair_finish<TILE>(g, U, buf, pb, cnt, B) << 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -123,6 +123,15 @@ class DeviceStore:
         arr = (_capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
         _capi.check(_capi.lib().b2m_move_all(self.h, arr))
 
+    def move_deposit_all(self, mps, q_per_particle):
+        """One mover cycle of every species and the deposition of rho, J (and
+        the pressure tensor when the mesh has it) of the new state into the
+        moment mesh (b2m_moments_zero first).  FAST without pressure: one
+        fused launch (b2m_move_deposit_all)."""
+        arr = (_capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+        q = (C.c_double * len(mps))(*[float(x) for x in q_per_particle])
+        _capi.check(_capi.lib().b2m_move_deposit_all(self.h, arr, q))
+
     def run_mover_host(self, batches, mps, chunk: int = 1 << 21):
         """Chunked H2D -> kernel -> D2H over three streams (b2m_run_mover_host)."""
         ns = len(batches)

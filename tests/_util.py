@@ -75,6 +75,15 @@ def cells_of(p6, grid):
     return i + nx * (j + ny * k)
 
 
+def sort_keys_of(p6, grid):
+    """The device cell sort's order (b2m_kernels.cu cell_key): the reference
+    cell (grid_cell_of) ordered z fastest, then x, then y."""
+    nx, ny, nz = grid[:3]
+    c = cells_of(p6, grid)
+    i, j, k = c % nx, (c // nx) % ny, c // (nx * ny)
+    return k + nz * (i + nx * j)
+
+
 def random_particles(grid, n, seed, vscale=0.5):
     nx, ny, nz, lx, ly, lz = grid
     r = np.random.default_rng(seed)

@@ -257,3 +257,155 @@ def test_empty_species_and_batches(gpu):
     assert all(not np.any(a) for a in mine.arrays)
     assert st.count(0) == 0 and st.count(1) == 16
     st.close()
+
+
+# ---- the fused mover + deposit (b2m_move_deposit_all, b2m_fused.cuh) -------
+
+def _two_stores(g, batches, field, mode, sort=True, steps=0, mps=None):
+    """Two identical device stores of `batches` (optionally sorted, then
+    `steps` plain mover cycles of drift)."""
+    out = []
+    for _ in range(2):
+        st = DeviceStore(g, [b.count() for b in batches], mode)
+        st.upload_field(field)
+        for s, b in enumerate(batches):
+            st.upload(s, b.span())
+            if sort:
+                st.sort(s)
+        for _ in range(steps):
+            st.move_all(mps)
+        out.append(st)
+    return out
+
+
+def _fused_vs_separate(g, batches, field, mode="fast", sort=True, steps=0, pressure=False):
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    qs = [b.q_per_particle for b in batches]
+    a, b_ = _two_stores(g, batches, field, mode, sort, steps, mps)
+    a.moments_zero(pressure)
+    a.move_all(mps)
+    for s, q in enumerate(qs):
+        a.deposit(s, q)
+    b_.moments_zero(pressure)
+    b_.move_deposit_all(mps, qs)
+    ma, mb = MomentMesh.make(g, pressure), MomentMesh.make(g, pressure)
+    a.moments_download(ma)
+    b_.moments_download(mb)
+    # the mover arithmetic is the same code: particles bit-identical (as a
+    # multiset -- the counting sort's order within a cell is not deterministic)
+    for s, bt in enumerate(batches):
+        pa = [np.empty(bt.count()) for _ in range(6)]
+        pb = [np.empty(bt.count()) for _ in range(6)]
+        a.download(s, pa)
+        b_.download(s, pb)
+        a.sync()
+        b_.sync()
+        ra = np.stack([x.view(np.uint64) for x in pa], 1)
+        rb = np.stack([x.view(np.uint64) for x in pb], 1)
+        ra = ra[np.lexsort(ra.T[::-1])]
+        rb = rb[np.lexsort(rb.T[::-1])]
+        np.testing.assert_array_equal(ra, rb)
+    # and the moments of the moved state: the oracle's deposit of it
+    want = [np.zeros(g.cells()) for _ in range(10 if pressure else 4)]
+    for s, bt in enumerate(batches):
+        p = [np.empty(bt.count()) for _ in range(6)]
+        b_.download(s, p)
+        b_.sync()
+        for x, w in zip(oracle.port_deposit_moments(p, g.as_tuple(), bt.q_per_particle,
+                                                    pressure), want):
+            w += x
+    a.close()
+    b_.close()
+    return ma, mb, want
+
+
+@pytest.mark.parametrize("zvar", [False, True])
+@pytest.mark.parametrize("sort,steps", [(True, 0), (True, 6), (False, 0)])
+def test_fused_move_deposit_vs_separate_and_oracle(gpu, zvar, sort, steps):
+    """One fused launch (FAST, rho + J through FP64 DMMA in the mover's tile
+    loop) against b2m_move_all + b2m_deposit and against the oracle deposit of
+    the moved state: the column kernel (z-invariant field) and the general
+    3-D kernel (z-varying), right after a sort, after drift, and unsorted
+    (GEM init order: every row mixes cells)."""
+    g = Grid.make(16, 16, 8, 6.4, 6.4, 3.2)
+    batches = gem.init_gem_species(g, 24)
+    field = gem.gem_bench_field(g, z_varying=zvar)
+    ma, mb, want = _fused_vs_separate(g, batches, field, sort=sort, steps=steps)
+    assert_moments_close(mb.arrays, want, what="fused vs oracle")
+    assert_moments_close(mb.arrays, ma.arrays, what="fused vs separate")
+
+
+@pytest.mark.parametrize("mode,pressure", [("strict", False), ("fast", True)])
+def test_move_deposit_all_unfused_paths(gpu, mode, pressure):
+    """STRICT (bit-identical terms) and the pressure tensor take the
+    mover-then-deposit path of b2m_move_deposit_all: same results."""
+    g = Grid.make(8, 8, 8, 6.4, 6.4, 6.4)
+    batches = gem.init_gem_species(g, 16)
+    ma, mb, want = _fused_vs_separate(g, batches, gem.gem_bench_field(g), mode=mode,
+                                      pressure=pressure)
+    assert_moments_close(mb.arrays, ma.arrays, what=f"{mode} pressure={pressure} vs separate")
+    assert_moments_close(mb.arrays, want, what=f"{mode} pressure={pressure}")
+
+
+def test_fused_deposit_skips_faulted_particles(gpu):
+    """A particle that faults in the mover (NaN velocity) is not deposited
+    and does not poison the accumulator: the mesh equals the deposit of the
+    other particles; the fault is reported by sync."""
+    g = Grid.make(8, 8, 8, 6.4, 6.4, 6.4)
+    grid = g.as_tuple()
+    p = random_particles(grid, 4099, 77, vscale=0.05)
+    p[3][1000] = np.nan
+    st = DeviceStore(g, [4099], "fast")
+    st.upload_field(gem.gem_bench_field(g))
+    st.upload(0, p)
+    st.moments_zero(False)
+    ptr, n = st.moments_device()
+    st.move_deposit_all([MoverParams.make(0.1, -25.0, 3)], [0.5])
+    import torch
+    from paper_1904_03684_b200.partition import _CudaArray
+    torch.cuda.synchronize()
+    mesh = torch.as_tensor(_CudaArray(ptr, (n,)), device="cuda").cpu().numpy().copy()
+    from paper_1904_03684_b200.errors import NumericalFault as NF
+    with pytest.raises(NF):
+        st.sync()
+    st.close()
+    # the expected mesh: every particle but the faulted one, moved by the oracle
+    q = [np.delete(a, 1000) for a in p]
+    E, B = gem.gem_bench_field(g).E.ravel(), gem.gem_bench_field(g).B.ravel()
+    assert oracle.port_move_batch(q, E, B, grid, 0.1, -25.0, 3) == -1
+    want = oracle.port_deposit_moments(q, grid, 0.5, False)
+    assert np.all(np.isfinite(mesh))
+    assert_moments_close(list(mesh.reshape(4, -1)), want, what="faulted particle skipped")
+
+
+def test_fused_full_c2_vs_separate(gpu):
+    """All 61,046,784 C2 particles (gem+E, z-invariant: the column kernel),
+    cell-sorted: fused rho + J equal the separate deposit to rounding and the
+    moved particles are bit-identical (every array as a sorted multiset)."""
+    g = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
+    batches = gem.init_gem_species(g, 216, pinned=True)
+    mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
+    qs = [b.q_per_particle for b in batches]
+    a, b_ = _two_stores(g, batches, gem.gem_bench_field(g), "fast", True, 0, mps)
+    a.moments_zero(False)
+    a.move_all(mps)
+    for s, q in enumerate(qs):
+        a.deposit(s, q)
+    b_.moments_zero(False)
+    b_.move_deposit_all(mps, qs)
+    ma, mb = MomentMesh.make(g, False), MomentMesh.make(g, False)
+    a.moments_download(ma)
+    b_.moments_download(mb)
+    assert_moments_close(mb.arrays, ma.arrays, what="C2 fused vs separate")
+    import torch
+    from paper_1904_03684_b200.partition import _CudaArray
+    for s, bt in enumerate(batches):
+        # multiset equality of the moved particles (the sort's order within a
+        # cell is not deterministic): sorted columns of every array
+        for c, (pa, pb) in enumerate(zip(a.device_ptrs(s), b_.device_ptrs(s))):
+            ta = torch.as_tensor(_CudaArray(pa, (bt.count(),)), device="cuda")
+            tb = torch.as_tensor(_CudaArray(pb, (bt.count(),)), device="cuda")
+            assert bool((torch.sort(ta)[0].view(torch.int64) ==
+                         torch.sort(tb)[0].view(torch.int64)).all()), (s, c)
+    a.close()
+    b_.close()

@@ -12,7 +12,7 @@ from paper_1904_03684_b200.engine import B200Engine, DeviceStore
 from paper_1904_03684_b200.errors import EngineFault, NumericalFault
 from paper_1904_03684_b200.mover import FieldMesh, Grid, MoverParams, move_batch
 from tests._util import (assert_bitwise, assert_within_contract, cells_of, digest, from_hex,
-                         random_field, random_particles, uniform_field)
+                         random_field, random_particles, sort_keys_of, uniform_field)
 
 pytestmark = pytest.mark.gpu
 
@@ -212,7 +212,7 @@ def test_device_store_sort_preserves_multiset(gpu, mode, path, monkeypatch):
     assert st.download(0, srt) == len(p0[0])
     st.sync()
     np.testing.assert_array_equal(oracle.multiset(srt), oracle.multiset(p0))
-    keys = cells_of(srt, grid)
+    keys = sort_keys_of(srt, grid)
     assert np.all(np.diff(keys) >= 0)
     # moving the sorted batch == moving those particles with the oracle
     st.move(0, MoverParams.make(0.1, -25.0, 3))
@@ -546,4 +546,4 @@ def test_sort_at_full_capacity_allocates_nothing(gpu, path, monkeypatch):
         assert st.download(s, srt) == len(p[0])
         st.sync()
         np.testing.assert_array_equal(oracle.multiset(srt), oracle.multiset(p))
-        assert np.all(np.diff(cells_of(srt, grid)) >= 0)
+        assert np.all(np.diff(sort_keys_of(srt, grid)) >= 0)
