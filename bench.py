@@ -427,6 +427,32 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     alg_bytes = BYTES_PER_PARTICLE * n_total
 
+    # Moment deposition (deposit_moments, kernels.cpp:147-183; SURVEY 8(f)1)
+    moments = None
+    if args.moments:
+        def deposit_ms():
+            store.moments_zero(False)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for s, b in enumerate(batches):
+                store.deposit(s, b.q_per_particle)
+            b_.record()
+            torch.cuda.synchronize()
+            store.sync()
+            return a.elapsed_time(b_)
+        deposit_ms()  # warm-up
+        drifted = deposit_ms()   # the state the steps above left (drifted since the last sort)
+        for s in range(len(batches)):
+            store.sort(s)
+        fresh = deposit_ms()     # right after a cell sort
+        moments = {"value": n_total / (fresh * 1e-3) / 1e6, "unit": "MPA/s", "ms": fresh,
+                   "what": "deposit_moments rho+J, all species, device-resident C2 state right "
+                           "after a cell sort",
+                   "ms_drifted": drifted,
+                   "drifted_what": "the same on the state the timed steps left",
+                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / peak,
+                   "fused": fused_cycle(store, mps, [b.q_per_particle for b in batches],
+                                        len(batches)) if args.mode == "fast" else None}
     # ---- the general 3-D kernel on the same particles, z-varying field ----
     general = None
     if args.general_3d and args.mode == "fast":
@@ -462,32 +488,6 @@ def run_ours(args):
         store.sync()
         store.set_mode(args.mode)
 
-    # Moment deposition (deposit_moments, kernels.cpp:147-183; SURVEY 8(f)1)
-    moments = None
-    if args.moments:
-        def deposit_ms():
-            store.moments_zero(False)
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for s, b in enumerate(batches):
-                store.deposit(s, b.q_per_particle)
-            b_.record()
-            torch.cuda.synchronize()
-            store.sync()
-            return a.elapsed_time(b_)
-        deposit_ms()  # warm-up
-        drifted = deposit_ms()   # the state the steps above left (drifted since the last sort)
-        for s in range(len(batches)):
-            store.sort(s)
-        fresh = deposit_ms()     # right after a cell sort
-        moments = {"value": n_total / (fresh * 1e-3) / 1e6, "unit": "MPA/s", "ms": fresh,
-                   "what": "deposit_moments rho+J, all species, device-resident C2 state right "
-                           "after a cell sort",
-                   "ms_drifted": drifted,
-                   "drifted_what": "the same on the state the timed steps left",
-                   "hbm_frac": 48 * n_total / (fresh * 1e-3) / 1e9 / peak,
-                   "fused": fused_cycle(store, mps, [b.q_per_particle for b in batches],
-                                        len(batches)) if args.mode == "fast" else None}
     store.close()
 
     # ---- e2e through the reference-facing engine API, host batches ----

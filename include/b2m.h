@@ -312,11 +312,14 @@ b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
  * and B): runtime.cpp:143 gives every worker the whole mesh. */
 b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
 /* Sum every rank's moment mesh (b2m_moments_zero + b2m_deposit per rank) into
- * every rank's mesh, in place (ncclAllReduce): the reference adds the
- * per-worker meshes (runtime.cpp:251-262).  Not bitwise reproducible: the
- * per-rank deposit sums with FP64 atomics and NCCL picks the reduction order
- * (equal to rounding of the sums; the reference's fixed worker order is not
- * reproduced). */
+ * every rank's mesh, in place, in the reference's order: zero, then rank
+ * 0's mesh added, then rank 1's, ... (moments_.add per worker,
+ * runtime.cpp:256-262) -- an ncclAllGather of the meshes and one ordered,
+ * separately rounded sum per element on every rank, so the reduction itself
+ * is deterministic and identical on all ranks (unlike an ncclAllReduce,
+ * whose order depends on the NCCL algorithm).  Each rank's own mesh still
+ * sums its particles with FP64 atomics (equal to the reference to rounding).
+ * The gather buffer (world x mesh) is allocated on the first call. */
 b2m_status b2m_world_reduce_moments(b2m_ctx* ctx);
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count);

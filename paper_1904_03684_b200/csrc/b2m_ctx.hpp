@@ -62,6 +62,8 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -151,6 +153,8 @@ struct b2m_ctx {
     std::vector<uint64_t> stage_cap;         // records per species
     long long* red = nullptr;                // device [2]: count, faulted
     long long* red_h = nullptr;              // pinned [2]
+    double* mstage = nullptr;                // device [world][mesh]: gathered moment meshes
+    uint64_t mstage_n = 0;                   // doubles per rank in mstage
     uint64_t total = 0;
     bool total_set = false;
   } w;

@@ -62,6 +62,12 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
 #define B2M_J_UNROLL 1
 #endif
 constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
+#ifndef B2M_SORT_ZFAST
+#define B2M_SORT_ZFAST 1       // cell sort order: 1 = z fastest (column-contiguous), 0 = x fastest
+#endif
+#ifndef B2M_COL_PREFETCH
+#define B2M_COL_PREFETCH 0     // 1: L1 prefetch of the next particle's column (measured slower: 1.31 vs 1.16 ms)
+#endif
 #ifndef B2M_2D_PAIR
 #define B2M_2D_PAIR 0          // 1: two particles per lane at a time (measured slower: spills)
 #endif
@@ -202,6 +208,23 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
 #pragma unroll 1
         for (int j = 0; j < P; ++j) {
           const int p = lane + 32 * j;
+          if (B2M_COL_PREFETCH) {
+            // the column of this lane's next particle: the next row of this
+            // tile, or the first row of the next tile once its load landed
+            if (j + 1 < P) {
+              col_prefetch(F.fg, cols, C, buf[st][0][p + 32], buf[st][1][p + 32]);
+            } else {
+              const int nst = st + 1 == kWarpStages ? 0 : st + 1;
+              const uint32_t nph = nst == 0 ? phase ^ 1u : phase;
+              const unsigned long long nt = tile + GW;
+              if (nt < total_tiles && mbar_test(&bar[nst], nph)) {
+                int s2 = s;
+                advance_span(s2, nt);
+                col_prefetch(F.fg, reinterpret_cast<const double*>(S.sp[s2].cells), C,
+                             buf[nst][0][lane], buf[nst][1][lane]);
+              }
+            }
+          }
           after(j, F.U.rounds == 3 ? fast_particle_2d<WT, 3>(F.fg, F.U, cols, buf[st], p, cnt, C)
                                    : fast_particle_2d<WT, 0>(F.fg, F.U, cols, buf[st], p, cnt, C));
         }
@@ -414,7 +437,8 @@ __global__ void cell_keys_kernel(const __grid_constant__ FastGrid g, const doubl
     const int ci = min(__double2int_rz(cx), g.nx - 1);
     const int cj = min(__double2int_rz(cy), g.ny - 1);
     const int ck = min(__double2int_rz(cz), g.nz - 1);
-    key = static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj));  // see cell_key
+    key = B2M_SORT_ZFAST ? static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj))  // see cell_key
+                         : static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
   }
   keys[i] = key;
   vals[i] = static_cast<uint32_t>(i);
@@ -444,7 +468,8 @@ __device__ __forceinline__ uint32_t cell_key(const FastGrid& g, double x, double
     const int ci = min(__double2int_rz(cx), g.nx - 1);
     const int cj = min(__double2int_rz(cy), g.ny - 1);
     const int ck = min(__double2int_rz(cz), g.nz - 1);
-    key = static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj));
+    key = B2M_SORT_ZFAST ? static_cast<uint32_t>(ck + g.nz * (ci + g.nx * cj))
+                         : static_cast<uint32_t>(ci + g.nx * (cj + g.ny * ck));
   }
   return key;
 }

@@ -43,6 +43,9 @@ struct MomentPtrs {
 //    directly; a group writes its terms to shared-memory rows and lane j sums
 //    column j over them before one atomic per column.
 constexpr int kGroupThreads = 128;
+#ifndef B2M_DEP_DIRECT_MAX
+#define B2M_DEP_DIRECT_MAX 1  // groups up to this size add their terms with direct atomics
+#endif
 
 template <int SET>
 constexpr int group_row() { return (SET == 0 ? 32 : 48) + 1; }  // +1: conflict-free rows
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
     }
     const bool mine = (rest >> lane) & 1;
     // alone in its cell: straight to the mesh
-    const bool single = mine && __popc(grp) == 1;
+    const bool single = mine && __popc(grp) <= B2M_DEP_DIRECT_MAX;
     if (single) terms([&](int v, double t) { red(v, i, j, k, t); });
     unsigned multi = rest & ~__ballot_sync(FULL, single);
     if (multi == 0) continue;

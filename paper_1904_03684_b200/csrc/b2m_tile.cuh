@@ -72,6 +72,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe of an mbarrier phase (true: the phase completed).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // L2 eviction priorities: the particle stream (2.9 GB per cycle at C2) is
 // evict-first so it does not sweep the 50 MB coefficient table, which is
 // evict-last (createpolicy, PTX ISA 7.4+).
@@ -634,6 +653,21 @@ __device__ __forceinline__ void fast_enter2(const FastGrid& g, const double* __r
   }
   C.ci = di;
   C.cj = dj;
+}
+
+// Prefetch into L1 the column table of the particle at (x, y) when it is not
+// the lane's cached column: a lane whose next particle sits in another column
+// then reloads from L1 instead of waiting an L2 round trip with its whole warp.
+__device__ __forceinline__ void col_prefetch(const FastGrid& g, const double* __restrict__ cols,
+                                             const FastCol& C, double x, double y) {
+  const int i = max(min(__double2int_rz(x * g.rdx), g.nx - 1), 0);
+  const int j = max(min(__double2int_rz(y * g.rdy), g.ny - 1), 0);
+  const int col = i + g.nx * j;
+  if (col != C.col) {
+    const double* c = cols + static_cast<long long>(col) * 24;
+    prefetch_l1(c);
+    prefetch_l1(c + 23);
+  }
 }
 
 template <int TILE, int ROUNDS>

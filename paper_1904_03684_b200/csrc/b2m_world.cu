@@ -34,7 +34,7 @@ const NcclApi& nccl() {
     a.ok = sym(a.GetUniqueId, "ncclGetUniqueId") && sym(a.CommInitRank, "ncclCommInitRank") &&
            sym(a.CommDestroy, "ncclCommDestroy") && sym(a.AllReduce, "ncclAllReduce") &&
            sym(a.Send, "ncclSend") && sym(a.Recv, "ncclRecv") &&
-           sym(a.Broadcast, "ncclBroadcast") &&
+           sym(a.Broadcast, "ncclBroadcast") && sym(a.AllGather, "ncclAllGather") &&
            sym(a.GroupStart, "ncclGroupStart") && sym(a.GroupEnd, "ncclGroupEnd") &&
            sym(a.GetErrorString, "ncclGetErrorString");
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
@@ -45,6 +45,26 @@ const NcclApi& nccl() {
 
 
 
+}  // namespace b2m
+
+namespace b2m {
+namespace {
+
+// The reference's moment reduction (runtime.cpp:256-262): moments_.zero(),
+// then moments_.add(worker w) for w = 0..N-1 -- element by element, in rank
+// order, separately rounded -- from the gathered [world][n] meshes.
+__global__ void ordered_sum_kernel(const double* __restrict__ stage, unsigned long long n,
+                                   int world, double* __restrict__ out) {
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                              threadIdx.x;
+       i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < world; ++r) a = __dadd_rn(a, stage[static_cast<unsigned long long>(r) * n + i]);
+    out[i] = a;
+  }
+}
+
+}  // namespace
 }  // namespace b2m
 
 using namespace b2m;
@@ -271,9 +291,25 @@ b2m_status b2m_world_reduce_moments(b2m_ctx* ctx) {
   double* mesh = nullptr;
   uint64_t n = 0;
   if ((st = b2m_moments_device_ptr(ctx, &mesh, &n)) != B2M_OK) return st;
-  if (ctx->w.comm)
-    B2M_NCCL(ctx, nccl().AllReduce(mesh, mesh, n, ncclFloat64, ncclSum, ctx->w.comm,
+  if (ctx->w.comm) {
+    // deterministic and bitwise the reference's order (not an NCCL sum, whose
+    // order depends on the algorithm and protocol): every rank gathers all
+    // meshes and adds them in rank order
+    const int world = ctx->sl.world;
+    if (ctx->w.mstage_n < n) {  // sized for the mesh in use (4 or 10 arrays)
+      if ((st = dalloc(ctx, &ctx->w.mstage, static_cast<size_t>(world) * n,
+                       "moment gather buffer")) != B2M_OK)
+        return st;
+      ctx->w.mstage_n = n;
+    }
+    B2M_NCCL(ctx, nccl().AllGather(mesh, ctx->w.mstage, n, ncclFloat64, ctx->w.comm,
                                    ctx->stream));
+    const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, 4096);
+    ordered_sum_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+        ctx->w.mstage, n, world, mesh);
+    note_launch();
+    B2M_CUDA(ctx, cudaGetLastError());
+  }
   return B2M_OK;
 }
 

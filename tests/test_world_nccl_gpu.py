@@ -1,0 +1,105 @@
+"""The native slab world over real NCCL with one process per GPU (ADVICE r1:
+the multi-rank exchange had never run).  Skipped unless the box has at least
+`world` GPUs -- the round's gpurun boxes have one; the driver's multi-GPU
+boxes run it.  STRICT mode: the union of the ranks' particles after the cycles
+equals the reference's multi-worker Simulation as a bitwise multiset (the
+reference's own worker-count test, test_runtime.cpp:214-226); the reduced
+moment mesh is bitwise identical on every rank (rank-ordered sum) and equals
+the oracle deposit of all particles to rounding; a NaN on one rank ends the
+cycle on every rank with typed errors instead of a hang."""
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1904_03684_b200.mover import Grid
+from paper_1904_03684_b200.partition import owner_of
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GRID = (8, 12, 8, 6.4, 9.6, 6.4)
+
+
+def _gpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world, cycles, mode):
+    d = tempfile.mkdtemp(prefix="b2m_nccl_")
+    port = str(_free_port())
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "nccl_world_worker.py"),
+                               str(r), str(world), port, d, str(cycles), mode],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+             for r in range(world)]
+    for p in procs:
+        try:
+            p.wait(timeout=300)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise AssertionError("NCCL world ranks hung")
+    return d, [p.stdout.read().decode(errors="replace") for p in procs]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_world_matches_reference_simulation(gpu, world):
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs (one rank per GPU), found {_gpus()}")
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    d, logs = _run(world, 3, "ok")
+    for r in range(world):
+        err = os.path.join(d, f"rank{r}.err")
+        assert os.path.exists(os.path.join(d, f"rank{r}.npz")), \
+            "\n".join(logs) + (open(err).read() if os.path.exists(err) else "")
+    per = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+    sim = oracle.RefSimulation(GRID, 8, workers=world, engine="cpu", field_passes=0)
+    sim.run(3)
+    g = Grid.make(*GRID)
+    allp = []
+    for s in range(4):
+        mine = [np.concatenate([z[f"s{s}a{a}"] for z in per]) for a in range(6)]
+        ref = sim.gather(s)
+        assert len(mine[0]) == len(ref[0])
+        np.testing.assert_array_equal(oracle.multiset(mine), oracle.multiset(ref))
+        for r, z in enumerate(per):
+            assert np.all(owner_of(z[f"s{s}a1"], g, world) == r)
+        allp.append(mine)
+    # the rank-ordered reduction: identical on every rank, = oracle to rounding
+    for z in per[1:]:
+        np.testing.assert_array_equal(z["mesh"], per[0]["mesh"])
+    from paper_1904_03684_b200 import gem
+    want = [np.zeros(g.cells()) for _ in range(10)]
+    qpp = [b.q_per_particle for b in gem.init_gem_species(g, 8)]
+    for s, p in enumerate(allp):
+        for x, w in zip(oracle.port_deposit_moments(p, GRID, qpp[s], True), want):
+            w += x
+    got = per[0]["mesh"].reshape(10, -1)
+    for a in range(10):
+        scale = float(np.max(np.abs(want[a])))
+        assert float(np.max(np.abs(got[a] - want[a]))) <= 1e-12 * max(scale, 1e-300)
+
+
+def test_nccl_world_fault_on_one_rank_aborts_all(gpu):
+    if _gpus() < 2:
+        pytest.skip(f"needs 2 GPUs (one rank per GPU), found {_gpus()}")
+    d, logs = _run(2, 1, "nan")
+    errs = [open(os.path.join(d, f"rank{r}.err")).read() if os.path.exists(
+        os.path.join(d, f"rank{r}.err")) else "" for r in range(2)]
+    assert errs[1].startswith("NumericalFault"), (errs, logs)
+    assert errs[0].startswith("EngineFault"), (errs, logs)
