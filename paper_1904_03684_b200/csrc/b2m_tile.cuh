@@ -608,6 +608,10 @@ __device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const Fa
 // the z predictor feeds nothing but the gather, so it is not formed (a
 // non-finite vbar_z is still flagged, and z1 is checked at the end).
 
+#ifndef B2M_2D_LOCATE_ALWAYS
+#define B2M_2D_LOCATE_ALWAYS 1  // locate every particle's start (no frame test): 1.16 -> 1.13 ms
+#endif
+
 struct Coef4 {
   double p0, p1, p2, p3;
 };
@@ -679,7 +683,14 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
   const double u0 = buf[3][p], v0 = buf[4][p], w0 = buf[5][p];
   double fx0, fy0;
   unsigned bad = 0u;
-  {
+  if (B2M_2D_LOCATE_ALWAYS) {
+    // every start located (no frame test, no divergent slow path): only the
+    // column reload is a branch, and it holds loads only
+    const bool inside = (p < cnt) & in_range(x0, dbits(g.lx)) & in_range(y0, dbits(g.ly)) &
+                        in_range(z0, dbits(g.lz));
+    bad = inside ? 0u : 1u;
+    fast_enter2(g, cols, C, inside ? x0 * g.rdx : 0.0, inside ? y0 * g.rdy : 0.0, fx0, fy0);
+  } else {
     const double cx = x0 * g.rdx, cy = y0 * g.rdy;
     fx0 = cx - C.ci;
     fy0 = cy - C.cj;
