@@ -418,7 +418,7 @@ __device__ __forceinline__ unsigned fast_tile_thread_p1(const FastGrid& g,
 // boundary position is evaluated in only changes rounding.
 
 #ifndef B2M_V2_R1_LOCATE
-#define B2M_V2_R1_LOCATE 0  // 1: every particle's start is located (no frame test)
+#define B2M_V2_R1_LOCATE 1  // every particle's start is located (no frame test): 2.15 -> 2.12 ms
 #endif
 
 // f in [+0, 1): the high word of +0..1-ulp is below that of 1.0; negatives
