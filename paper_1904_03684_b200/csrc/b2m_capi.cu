@@ -153,6 +153,10 @@ double* strict_nodes(b2m_ctx* ctx) {
   if (ctx->strict_gen != ctx->field_gen) {  // allocated at context creation
     launch_strict_nodes(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB,
                         ctx->strict_nodes, ctx->stream);
+    // the z-invariance flag of this field (the STRICT column kernel's test)
+    if (ctx->zvar)
+      launch_zinv_check(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB, ctx->zvar,
+                        ctx->stream);
     ctx->strict_gen = ctx->field_gen;
   }
   return ctx->strict_nodes;
@@ -681,7 +685,7 @@ b2m_status b2m_move_range(b2m_ctx* ctx, int s, const b2m_mover_params* mp, uint6
   const SpeciesLaunch L = make_launch(ctx, s, *mp, offset, n);
   if (ctx->mode == B2M_MODE_STRICT) {
     if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
-                                  ctx->stream))
+                                  ctx->stream, nullptr, nullptr, nullptr, ctx->zvar))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, nullptr,
                                       nullptr, nullptr, ctx->zvar)) {
@@ -726,7 +730,7 @@ static b2m_status move_all_impl(b2m_ctx* ctx, const b2m_mover_params* mp, const 
   if (kt >= 0) B2M_CUDA(ctx, cudaEventRecord(ctx->kt_ev[2 * kt], ctx->stream));
   if (ctx->mode == B2M_MODE_STRICT) {
     if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), nodes, L.data(), ns,
-                                  ctx->fault, ctx->stream))
+                                  ctx->fault, ctx->stream, nullptr, nullptr, nullptr, ctx->zvar))
       return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
   } else if (!launch_move_fast(to_fast(ctx->grid), L.data(), ns, ctx->fault, ctx->stream,
                                nullptr, nullptr, nullptr, ctx->zvar,
@@ -834,7 +838,7 @@ b2m_status b2m_run_mover_host(b2m_ctx* ctx, int n_species, double* const* host6_
       const SpeciesLaunch L = make_launch(ctx, s, mp[s], off, n);
       if (ctx->mode == B2M_MODE_STRICT) {
         if (!launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx), &L, 1, ctx->fault,
-                                      ctx->stream))
+                                      ctx->stream, nullptr, nullptr, nullptr, ctx->zvar))
           return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");
       } else if (!launch_move_fast(to_fast(ctx->grid), &L, 1, ctx->fault, ctx->stream, nullptr,
                                       nullptr, nullptr, ctx->zvar))
@@ -1298,7 +1302,7 @@ b2m_status b2m::move_migrate_species(b2m_ctx* ctx, const int* species,
       ctx->mode == B2M_MODE_STRICT
           ? launch_move_strict_tiles(to_dev(ctx->grid), to_fast(ctx->grid), strict_nodes(ctx),
                                      L.data(), nl, ctx->fault, ctx->stream, &ctx->sl, fl.data(),
-                                     tc.data())
+                                     tc.data(), ctx->zvar)
           : launch_move_fast(to_fast(ctx->grid), L.data(), nl, ctx->fault, ctx->stream, &ctx->sl,
                              fl.data(), tc.data(), ctx->zvar);
   if (!ok) return fail(B2M_CUDA_ERROR, "TMA tensor map setup failed (cuTensorMapEncodeTiled)");

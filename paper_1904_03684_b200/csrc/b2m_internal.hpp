@@ -42,7 +42,12 @@ bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                               cudaStream_t st, const SlabLaunch* sl = nullptr,
                               uint8_t* const* flags = nullptr,
-                              unsigned long long* const* tcnt = nullptr);
+                              unsigned long long* const* tcnt = nullptr,
+                              const int* zvar = nullptr);
+// The field's z-invariance flag alone (0 = every node plane equals plane 0
+// bit for bit); launch_field_to_cells runs it too.
+void launch_zinv_check(int nx, int ny, int nz, const double* E, const double* B, int* zvar,
+                       cudaStream_t st);
 // STRICT cell table: per cell the 8 corner nodes' E, B (48 doubles).
 void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* B, double* out,
                          cudaStream_t st);

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
     warp_tile_kernel(const __grid_constant__ TileField F, const __grid_constant__ TensorSpans S,
                      const __grid_constant__ SlabLaunch sl, unsigned long long total_tiles,
                      FaultWord* fault) {
-  if (!STRICT && F.zvar && ((*F.zvar == 0) != (DIM == 2))) return;
+  if (F.zvar && ((*F.zvar == 0) != (DIM == 2))) return;
   constexpr int WT = 32 * P;
   constexpr int WARPS = kWarpThreads / 32;
   extern __shared__ __align__(128) unsigned char wt_smem[];
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
         // pc_iterations = 3 (the reference default) gets a fully unrolled body
         const unsigned bad =
             sp.rounds == 3
-                ? strict_tile_thread_p1<WT, 3>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc)
-                : strict_tile_thread_p1<WT, 0>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc);
+                ? strict_tile_thread_p1<WT, 3, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc)
+                : strict_tile_thread_p1<WT, 0, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (flags && p < cnt) {
           int flag = 0;
@@ -712,12 +712,25 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, F
 bool launch_move_strict_tiles(const DevGrid& g, const FastGrid& fg, const double* nodes,
                               const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                               cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
-                              unsigned long long* const* tcnt) {
+                              unsigned long long* const* tcnt, const int* zvar) {
   TileField F{};
   F.dg = g;
   F.fg = fg;  // wrap thresholds (WrapAxis)
   F.nodes = nodes;
+  F.zvar = zvar;
+  // as FAST: the column kernel for a z-invariant field, the general one else
+  if (zvar && !launch_warp_tiles<true, 2>(F, sp, n_spans, fault, st, sl, flags, tcnt))
+    return false;
   return launch_warp_tiles<true, 3>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+}
+
+void launch_zinv_check(int nx, int ny, int nz, const double* E, const double* B, int* zvar,
+                       cudaStream_t st) {
+  const long long plane = static_cast<long long>(nx + 1) * (ny + 1);
+  const long long nodes = plane * (nz + 1);
+  cudaMemsetAsync(zvar, 0, sizeof(int), st);
+  zinv_check_kernel<<<grid_for(3 * (nodes - plane), 256), 256, 0, st>>>(plane, nodes, E, B, zvar);
+  note_launch();
 }
 
 void launch_strict_nodes(int nx, int ny, int nz, const double* E, const double* B, double* out,
@@ -731,13 +744,7 @@ void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double
                            const double* scale, double2* const* tables, int n_tables,
                            cudaStream_t st, int* zvar) {
   const long long ncell = static_cast<long long>(nx) * ny * nz;
-  if (zvar) {
-    const long long plane = static_cast<long long>(nx + 1) * (ny + 1);
-    const long long nodes = plane * (nz + 1);
-    cudaMemsetAsync(zvar, 0, sizeof(int), st);
-    zinv_check_kernel<<<grid_for(3 * (nodes - plane), 256), 256, 0, st>>>(plane, nodes, E, B, zvar);
-    note_launch();
-  }
+  if (zvar) launch_zinv_check(nx, ny, nz, E, B, zvar, st);
   for (int base = 0; base < n_tables; base += kMaxTables) {
     CellTables T{};
     for (T.n = 0; T.n < kMaxTables && base + T.n < n_tables; ++T.n) {

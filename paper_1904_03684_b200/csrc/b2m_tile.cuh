@@ -919,11 +919,14 @@ struct CellCache {
 // strict_nodes_kernel in exactly the cache's order (corner c: Ex Ey Ez Bx By
 // Bz), so the reload is twelve 256-bit loads -- the same values the
 // reference reads from the node mesh, bit for bit.
+// DIM 2 (z-invariant field: corners 4-7 equal corners 0-3 bit for bit): the
+// first 24 doubles of the column's k = 0 cell, corners 0-3.
+template <int DIM = 3>
 __device__ __forceinline__ void cache_load_strict(CellCache& cc, const double* __restrict__ nodes,
                                                   int cell) {
   const double* c = nodes + static_cast<long long>(cell) * 48;
 #pragma unroll
-  for (int q = 0; q < 12; ++q) {
+  for (int q = 0; q < (DIM == 2 ? 6 : 12); ++q) {
     double a, b, d, e;
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(a), "=d"(b), "=d"(d), "=d"(e)
@@ -942,7 +945,8 @@ __device__ __forceinline__ void begin(PState& P, const double* p) {
   P.ok = true;
 }
 
-__device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, double* wt) {
+__device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, double* wt,
+                                             int* column = nullptr) {
   if (!(P.tx >= 0.0 && P.tx < g.lx && P.ty >= 0.0 && P.ty < g.ly && P.tz >= 0.0 && P.tz < g.lz)) {
     P.ok = false;
     return -1;
@@ -965,21 +969,24 @@ __device__ __forceinline__ int strict_locate(PState& P, const DevGrid& g, double
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     wt[c] = __dmul_rn(__dmul_rn(wx[c & 1], wy[(c >> 1) & 1]), wz[(c >> 2) & 1]);
+  if (column) *column = i + g.nx * j;
   return i + g.nx * (j + g.ny * k);
 }
 
+template <int DIM = 3>
 __device__ __forceinline__ void strict_round(PState& P, const CellCache& cc, const double* wt,
                                              double beta) {
   double ex = 0.0, ey = 0.0, ez = 0.0, fbx = 0.0, fby = 0.0, fbz = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const double w = wt[c];
-    ex = __dadd_rn(ex, __dmul_rn(w, cc.c[3 * c + 0].x));
-    ey = __dadd_rn(ey, __dmul_rn(w, cc.c[3 * c + 0].y));
-    ez = __dadd_rn(ez, __dmul_rn(w, cc.c[3 * c + 1].x));
-    fbx = __dadd_rn(fbx, __dmul_rn(w, cc.c[3 * c + 1].y));
-    fby = __dadd_rn(fby, __dmul_rn(w, cc.c[3 * c + 2].x));
-    fbz = __dadd_rn(fbz, __dmul_rn(w, cc.c[3 * c + 2].y));
+    const int n = DIM == 2 ? (c & 3) : c;  // z-invariant: corner c + 4 holds corner c's values
+    ex = __dadd_rn(ex, __dmul_rn(w, cc.c[3 * n + 0].x));
+    ey = __dadd_rn(ey, __dmul_rn(w, cc.c[3 * n + 0].y));
+    ez = __dadd_rn(ez, __dmul_rn(w, cc.c[3 * n + 1].x));
+    fbx = __dadd_rn(fbx, __dmul_rn(w, cc.c[3 * n + 1].y));
+    fby = __dadd_rn(fby, __dmul_rn(w, cc.c[3 * n + 2].x));
+    fbz = __dadd_rn(fbz, __dmul_rn(w, cc.c[3 * n + 2].y));
   }
   const double vtx = __dadd_rn(P.u0, __dmul_rn(beta, ex));
   const double vty = __dadd_rn(P.v0, __dmul_rn(beta, ey));
@@ -1036,7 +1043,11 @@ __device__ __forceinline__ bool strict_finish(PState& P, const FastGrid& w, doub
 // stay in registers while the particle -- and the lane's next particles --
 // remain in the same cell: a bitwise-identical reuse of values the reference
 // would re-read.
-template <int TILE, int ROUNDS = 0>
+// DIM 2: the field is z-invariant (zinv_check_kernel, bitwise), so the cache
+// holds the column's 4 corner nodes -- the reference's 8 products and sums are
+// all still formed, in its order, from the same values -- and z crossings do
+// not reload.
+template <int TILE, int ROUNDS = 0, int DIM = 3>
 __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, const FastGrid& wg,
                                                           const double* __restrict__ nodes,
                                                           const SpeciesLaunch& sp,
@@ -1050,10 +1061,12 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, cons
 #pragma unroll
   for (int r = 0; r < rounds; ++r) {
     double wt[8];
-    const int cell = strict_locate(P, g, wt);
+    int column;
+    const int cell = strict_locate(P, g, wt, DIM == 2 ? &column : nullptr);
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
-    if (cell != cc.cell) cache_load_strict(cc, nodes, cell);
-    strict_round(P, cc, wt, sp.beta);
+    const int key = DIM == 2 ? column : cell;
+    if (key != cc.cell) cache_load_strict<DIM>(cc, nodes, key);
+    strict_round<DIM>(P, cc, wt, sp.beta);
     if (r + 1 < rounds) strict_predict(P, wg, sp.dto2);
   }
   double out[6];

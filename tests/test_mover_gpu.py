@@ -547,3 +547,29 @@ def test_sort_at_full_capacity_allocates_nothing(gpu, path, monkeypatch):
         st.sync()
         np.testing.assert_array_equal(oracle.multiset(srt), oracle.multiset(p))
         assert np.all(np.diff(sort_keys_of(srt, grid)) >= 0)
+
+
+@pytest.mark.parametrize("seed,qom,pc", [(41, -25.0, 3), (42, 1.0, 5), (43, -25.0, 1)])
+def test_strict_column_kernel_bitwise(gpu, monkeypatch, seed, qom, pc):
+    """STRICT on a z-invariant field runs the column kernel (4 cached corner
+    nodes stand in for 8, the reference's 8 products and sums still formed in
+    its order): bit-identical to the oracle and to the general STRICT kernel
+    (B2M_FAST_3D=1 disables the z-invariance test), edge positions included;
+    one node off the z-invariance takes the general kernel, still bitwise."""
+    grid = (6, 5, 4, 2.4, 2.0, 1.6)
+    E, B = zinvariant_field(grid, seed)
+    p0 = random_particles(grid, 50000, seed)
+    L = np.array(grid[3:])
+    p0[0][:7] = [0.0, -0.0, np.nextafter(L[0], 0.0), 0.4, np.nextafter(0.4, 0.0), 2.0, 5e-324]
+    p0[2][7:14] = [0.0, np.nextafter(L[2], 0.0), 0.4, np.nextafter(0.8, 1.0), 1.2, 0.0, 1.6 / 2]
+    want = port_move(p0, E, B, grid, 0.1, qom, pc)
+    got = gpu_move(p0, E, B, grid, 0.1, qom, pc, "strict")
+    assert_bitwise(got, want, "strict column kernel")
+    monkeypatch.setenv("B2M_FAST_3D", "1")
+    assert_bitwise(gpu_move(p0, E, B, grid, 0.1, qom, pc, "strict"), want, "strict general")
+    monkeypatch.delenv("B2M_FAST_3D")
+    nx, ny = grid[:2]
+    E2 = E.copy()
+    E2[3 * (1 + (nx + 1) * (2 + (ny + 1) * 3)) + 2] += 0.125  # Ez at node (1, 2, 3)
+    assert_bitwise(gpu_move(p0, E2, B, grid, 0.1, qom, pc, "strict"),
+                   port_move(p0, E2, B, grid, 0.1, qom, pc), "strict nearly z-invariant")
