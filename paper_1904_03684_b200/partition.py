@@ -343,7 +343,7 @@ class NativeSlabWorld:
     ``dist`` (torch.distributed, initialised) only carries the NCCL unique
     id from rank 0 to the others; ``store`` is this rank's DeviceStore."""
 
-    def __init__(self, grid, store, rank: int, world: int, dist=None):
+    def __init__(self, grid, store, rank: int, world: int, dist=None, comm: bool | None = None):
         from . import _capi
         self._capi = _capi
         self.grid, self.store, self.rank, self.world = grid, store, rank, world
@@ -351,10 +351,13 @@ class NativeSlabWorld:
         self.last_exchange = {}
         self.total = None
         uid = (C.c_ubyte * 128)()
-        if world > 1 and dist is None:
+        # comm: create an NCCL communicator (default: world > 1; a one-rank
+        # communicator runs the same collectives with no peers)
+        comm = world > 1 if comm is None else comm
+        if comm and dist is None and world > 1:
             raise ConfigError("NativeSlabWorld: world > 1 needs torch.distributed (dist) to "
                               "share the NCCL unique id")
-        if world > 1:
+        if comm:
             if rank == 0:
                 _capi.check(_capi.lib().b2m_world_id(uid))
             if dist is not None:
