@@ -674,11 +674,13 @@ __device__ __forceinline__ void col_prefetch(const FastGrid& g, const double* __
   }
 }
 
+// y_out: the new y of a particle that moved clean (the migration scan reads
+// it from a register instead of the tile)
 template <int TILE, int ROUNDS>
 __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const FastUniform& U,
                                                      const double* __restrict__ cols,
                                                      double (*buf)[TILE], int p, int cnt,
-                                                     FastCol& C) {
+                                                     FastCol& C, double* y_out = nullptr) {
   const double x0 = buf[0][p], y0 = buf[1][p], z0 = buf[2][p];
   const double u0 = buf[3][p], v0 = buf[4][p], w0 = buf[5][p];
   double fx0, fy0;
@@ -745,6 +747,7 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
     z1 = wrap_exact_bits(z1, g.az, dbits(g.az.hi0), dbits(g.az.hi1), dbits(g.az.lom1) & kAbs);
     if (!finite3(x1, y1, z1)) bad = 1u;
   }
+  if (y_out) *y_out = y1;
   if ((bad == 0u) & fin_v) {
     buf[0][p] = x1; buf[1][p] = y1; buf[2][p] = z1;
     buf[3][p] = u1; buf[4][p] = v1; buf[5][p] = w1;

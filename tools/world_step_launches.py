@@ -29,3 +29,19 @@ st.record(2)
 for _ in range(10): st.move_all(mps)
 st.record(3); st.sync()
 print(f"world step {a:.3f} ms, plain move_all {st.elapsed_ms(2, 3) / 10:.3f} ms")
+# the mover with the owner scan + compaction alone (b2m_move_migrate_all)
+from paper_1904_03684_b200 import _capi
+arr = (_capi.b2m_mover_params * len(mps))(*[m.to_c() for m in mps])
+for _ in range(3): _capi.check(_capi.lib().b2m_move_migrate_all(st.h, arr))
+st.sync()
+st.record(2)
+for _ in range(10): _capi.check(_capi.lib().b2m_move_migrate_all(st.h, arr))
+st.record(3); st.sync()
+print(f"move_migrate_all (mover + owner scan + compaction) {st.elapsed_ms(2, 3) / 10:.3f} ms")
+# interleaved: plain mover vs mover + owner scan + compaction, same drift
+ta = tb = 0.0
+for _ in range(10):
+    st.record(2); st.move_all(mps); st.record(3); st.sync(); ta += st.elapsed_ms(2, 3)
+    st.record(2); _capi.check(_capi.lib().b2m_move_migrate_all(st.h, arr)); st.record(3); st.sync()
+    tb += st.elapsed_ms(2, 3)
+print(f"interleaved: move_all {ta / 10:.3f} ms, move_migrate_all {tb / 10:.3f} ms")
