@@ -48,6 +48,8 @@ PPC = 216
 NX, NY, NZ = 64, 64, 32
 LX, LY, LZ = 25.6, 12.8, 6.4
 C4_PPC = 905           # 64x64x32 cells, 255,774,720 particles
+C3_GRID = (128, 128, 64, 51.2, 25.6, 12.8)   # SURVEY §8d C3 (BASELINE configs[2])
+C3_PPC = 235                                 # -> 512,081,920 particles
 BYTES_PER_PARTICLE = 96  # 48 B read + 48 B write of x,y,z,u,v,w
 REP_CYCLES = 10          # cycles per repetition (bench.cpp:13-45)
 CPU_SAMPLE_PER_THREAD = 2_000_000
@@ -335,6 +337,73 @@ def fused_cycle(store, mps, qs, ns, reps=3, drift=32):
                     "DMMA); fresh = right after a cell sort"}
 
 
+def load_gem_chunked(store, grid, ppc, chunk=1 << 24):
+    """The reference GEM state straight into a device store without holding it
+    on the host: background species generated in index ranges by the
+    counter-RNG jump-ahead and uploaded chunk by chunk, the (domain-size
+    independent) sheet species whole."""
+    import ctypes as C
+    import numpy as np
+    from paper_1904_03684_b200 import _capi, gem
+    counts = gem.gem_counts(grid, ppc)
+    g = grid.to_c()
+    for s in range(4):
+        if s >= 2:
+            b = gem.init_gem_species(grid, ppc, species=(s,))[0]
+            store.upload(s, b.span())
+            continue
+        for m0 in range(0, counts[s], chunk):
+            m1 = min(counts[s], m0 + chunk)
+            arrs = [np.empty(m1 - m0) for _ in range(6)]
+            _capi.check(_capi.lib().b2m_gem_fill_species_range(
+                C.byref(g), ppc, gem.DEFAULT_SEED, s, m0, m1, _capi.ptr6(arrs), 0))
+            _capi.check(_capi.lib().b2m_species_upload_range(store.h, s, _capi.ptr6(arrs), m0,
+                                                             m1 - m0))
+        _capi.check(_capi.lib().b2m_species_set_count(store.h, s, counts[s]))
+    store.sync()
+    return counts
+
+
+def c3_single_gpu(args, local, field_kind):
+    """SURVEY C3 (BASELINE configs[2]: 128x128x64 cells, 235 ppc, 512,081,920
+    particles, 24.6 GB of SoA) on this one GPU: field refresh + mover, the
+    same step as the headline."""
+    import torch
+    from paper_1904_03684_b200 import gem
+    from paper_1904_03684_b200.engine import DeviceStore
+    from paper_1904_03684_b200.mover import Grid, MoverParams
+    grid = Grid.make(*C3_GRID)
+    t0 = time.perf_counter()
+    counts = gem.gem_counts(grid, C3_PPC)
+    qom, _ = gem.gem_species_params(grid, C3_PPC)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    store = DeviceStore(grid, counts, args.mode, device=local)
+    store.set_stream(stream.cuda_stream)
+    store.upload_field(gem.gem_bench_field(grid) if field_kind == "gem+E" else gem.gem_field(grid))
+    load_gem_chunked(store, grid, C3_PPC)
+    t_init = time.perf_counter() - t0
+    for s in range(4):
+        store.sort(s)
+    mps = [MoverParams.make(DT, float(qom[s]), PC) for s in range(4)]
+    time_steps(store, mps, args.warmup, True, False)
+    torch.cuda.synchronize()
+    ev = time_steps(store, mps, args.steps, True, True)
+    torch.cuda.synchronize()
+    store.sync()
+    store.close()
+    n = sum(counts)
+    ms = sum(t for t, k in ev) / len(ev)
+    kms = sum(k for t, k in ev) / len(ev)
+    peak, _ = load_peaks()
+    return {"particles": n, "n_gpus": 1, "ms_per_step": ms, "value": n / (ms * 1e-3) / 1e6,
+            "unit": "MPA/s", "kernel_ms": kms,
+            "roofline_frac": BYTES_PER_PARTICLE * n / (kms * 1e-3) / 1e9 / peak,
+            "init_s": t_init,
+            "workload": "GEM 128x128x64, L = (51.2, 25.6, 12.8), 235 ppc (SURVEY C3, BASELINE "
+                        "configs[2]) on one GPU: field refresh + mover"}
+
+
 def c4_single_gpu(args, local, field_kind):
     """SURVEY C4 (255.8M particles) on this one GPU: the strong-scaling
     baseline T1 (plain mover + field refresh, no exchange)."""
@@ -515,6 +584,7 @@ def run_ours(args):
 
     # ---- strong-scaling baseline (C4 on this GPU) ----
     strong = c4_single_gpu(args, local, args.field) if args.strong else None
+    c3 = c3_single_gpu(args, local, args.field) if args.c3 else None
 
     # ---- CPU baseline: the reference arm's own measurement ----
     cpu = cpu_reference_measure(args.field, 2, 1) if args.cpu_baseline else None
@@ -557,6 +627,7 @@ def run_ours(args):
                        "(z-invariant: warp_tile_kernel<4,1,2,0>), 3 cycles",
         "moments": moments,
         "strong_scaling": strong,
+        "c3": c3,
         "init_s": t_init,
     }
     print(json.dumps(line), flush=True)
@@ -671,9 +742,9 @@ def run_world(args):
     field_of = (lambda g: gem.gem_bench_field(g)) if args.field == "gem+E" \
         else (lambda g: gem.gem_field(g))
 
-    def setup(grid, ppc):
+    def setup(grid, ppc, pinned=True):
         """This rank's slab of the GEM state in a device store + its slab world."""
-        batches = gem.init_gem_slab(grid, ppc, rank, world)
+        batches = gem.init_gem_slab(grid, ppc, rank, world, pinned=pinned)
         field = field_of(grid)
         mps = [MoverParams.make(DT, b.qom, PC) for b in batches]
         caps = [int(b.count() * 1.05) + 65536 for b in batches]
@@ -819,6 +890,25 @@ def run_world(args):
                       "efficiency_def": "S/N with S = T1/TN (bench.cpp:53-59)", "ranks": per4}
         dist.barrier()
 
+    # ---- C3 (BASELINE configs[2]): 512M particles in N y-slabs of 128/N cells ----
+    c3 = None
+    if args.c3:
+        g3 = Grid.make(*C3_GRID)
+        b3, f3, mps3, st3, sw3, step3 = setup(g3, C3_PPC, pinned=False)
+        n3 = int(reduce(sum(st3.count(s) for s in range(len(b3))), dist.ReduceOp.SUM))
+        del b3
+        ms3, _, mv3, ex3, _ = timed(st3, step3, args.steps)
+        per3 = gather({"rank": rank, "ms_per_step": ms3, "mover_ms": mv3, "exchange_ms": ex3,
+                       "particles": sum(st3.count(s) for s in range(st3.n_species))})
+        ms3 = reduce(ms3, dist.ReduceOp.MAX)
+        st3.close()
+        if rank == 0:
+            c3 = {"workload": "GEM 128x128x64, L = (51.2, 25.6, 12.8), 235 ppc (SURVEY C3, "
+                              f"BASELINE configs[2]); y-slabs of {C3_GRID[1] // world} cells",
+                  "particles": n3, "n_gpus": world, "ms_per_step": ms3,
+                  "value": n3 / (ms3 * 1e-3) / 1e6, "unit": "MPA/s", "ranks": per3}
+        dist.barrier()
+
     cpu = cpu_reference_measure(args.field, 2, 1) if args.cpu_baseline and rank == 0 else None
     if rank == 0:
         mv = [r["mover_ms"] for r in ranks if r["mover_ms"] is not None]
@@ -855,7 +945,7 @@ def run_world(args):
                              if mv else None),
                 "verify": verify, "counts_conserved": counts_ok,
                 "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-                "strong_scaling": strong}
+                "strong_scaling": strong, "c3": c3}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
@@ -905,6 +995,8 @@ def parse(argv=None):
     ap.add_argument("--moments", type=int, default=1)
     ap.add_argument("--general-3d", type=int, default=1,
                     help="also time the general 3-D kernel on a z-varying field")
+    ap.add_argument("--c3", type=int, default=1,
+                    help="the C3 leg (BASELINE configs[2]: 512M particles, 128x128x64)")
     ap.add_argument("--strong", type=int, default=1,
                     help="the C4 strong-scaling leg (255.8M particles)")
     ap.add_argument("--verify", type=int, default=1,
