@@ -40,9 +40,14 @@
 namespace b2m {
 
 #ifndef B2M_DEP_PASSES
-#define B2M_DEP_PASSES 0  // extra DMMA passes per row for groups of >= 2 beyond the first
+#define B2M_DEP_PASSES 3  // extra DMMA passes per row for groups of >= 2 beyond the first
 #endif
-constexpr int kDepStage = 6 * 32;  // staged weight factors per warp (doubles)
+// Staging rows are kDepRow doubles apart: with 36, the 16 (row, lane%4)
+// pairs a DMMA fragment load touches fall in 16 distinct 64-bit bank pairs
+// (2 * (36 r + q) mod 32 = 8 r + 2 q) -- rows of 32 would put every row on
+// the same banks (4-way conflicts).
+constexpr int kDepRow = 36;
+constexpr int kDepStage = 6 * kDepRow;  // fused mover: six staged weight factors per warp
 
 struct DepCarry {
   double d0, d1;   // DMMA accumulator: D[lane/4][2*(lane%4) + {0, 1}]
@@ -65,9 +70,10 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // Add one half of the accumulator (columns 4h..4h+3: m = 0..3 of cell
 // (ci, cj, ck)) to the mesh and clear it.  Lane l holds D[c][n] for c = l/4,
 // n = 2(l%4) + e; the half's values sit on the lanes with (l%4)/2 == h.
+template <class G>
 __device__ __forceinline__ void dep_flush_half(double& d0, double& d1, int h, int ci, int cj,
-                                               int ck, const FastGrid& g,
-                                               double* const* mom, int lane) {
+                                               int ck, const G& g, double* const* mom,
+                                               int lane) {
   const int q = lane & 3;
   if ((q >> 1) != h) return;
   const int c = lane >> 2;
@@ -83,37 +89,40 @@ __device__ __forceinline__ void dep_flush_half(double& d0, double& d1, int h, in
 }
 
 // One pass: D[:, 0:4] += carried-cell members' terms, D[:, 4:8] += group
-// `g1` members' terms (masks over the row's 32 particles).
-template <int TILE>
-__device__ __forceinline__ void dep_pass(DepCarry& C, const double* sw, double (*buf)[TILE],
-                                         int row0, unsigned carry_mask, unsigned g1_mask,
-                                         int lane) {
+// `g1` members' terms (masks over the row's 32 particles).  mrow[(m - 1) *
+// MS + l] is moment m (u, v, w) of the row's particle l.  W8: sw holds the 8
+// corner weights (row c = corner c); else the 6 factors (rows 0-3: qv wx wy
+// per (dx, dy) corner, rows 4-5: wz), multiplied here.
+template <int MS, bool W8>
+__device__ __forceinline__ void dep_pass(DepCarry& C, const double* sw, const double* mrow,
+                                         unsigned carry_mask, unsigned g1_mask, int lane) {
   const int q = lane & 3;     // A: k column / B: k row
   const int n = lane >> 2;    // A: corner row / B: column
   const int m = n & 3;        // moment of the B column
   const unsigned mask = (n >> 2) ? g1_mask : carry_mask;
   const int cxy = n & 3, cz = n >> 2;  // A: corner n = cxy + 4 cz
+  const double* mr = mrow + (m == 0 ? 0 : (m - 1) * MS);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int pl = 4 * k + q;  // particle of this fragment element, within the row
-    const double a = sw[cxy * 32 + pl] * sw[(4 + cz) * 32 + pl];
+    const double a = W8 ? sw[n * kDepRow + pl]
+                        : sw[cxy * kDepRow + pl] * sw[(4 + cz) * kDepRow + pl];
     double b = 0.0;
-    if ((mask >> pl) & 1u) b = m == 0 ? 1.0 : buf[2 + m][row0 + pl];
+    if ((mask >> pl) & 1u) b = m == 0 ? 1.0 : mr[pl];
     dmma_8x8x4(C.d0, C.d1, a, b);
   }
 }
 
-// Deposit the 32 particles of row `row0` (this lane's particle p = row0 +
-// lane) after the mover wrote them back to the tile stage; `ok` = the
-// particle exists and moved clean.  All 32 lanes must call it together.
-template <int TILE>
-__device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double qv,
-                                        double* const* mom, double* sw, double (*buf)[TILE],
-                                        int row0, bool ok, int lane) {
+// (px, py, pz): this lane's particle's position; mrow as in dep_pass.
+// Used by the fused mover (the row in the tile stage, MS = tile width) and by
+// the standalone FAST deposit (u, v, w staged per lane, MS = 32).
+template <int MS, bool W8 = false, class G>
+__device__ __forceinline__ void dep_row(DepCarry& C, const G& g, double qv, double* const* mom,
+                                        double* sw, const double* mrow, double px, double py,
+                                        double pz, bool ok, int lane) {
   constexpr unsigned FULL = 0xffffffffu;
-  const int p = row0 + lane;
   // FAST deposit locate (b2m_moments.cu, grid.hpp:64-82 with 1/d scaling)
-  const double sx = buf[0][p] * g.rdx, sy = buf[1][p] * g.rdy, sz = buf[2][p] * g.rdz;
+  const double sx = px * g.rdx, sy = py * g.rdy, sz = pz * g.rdz;
   int i = min(__double2int_rz(sx), g.nx - 1), j = min(__double2int_rz(sy), g.ny - 1),
       k = min(__double2int_rz(sz), g.nz - 1);
   i = max(i, 0);
@@ -126,12 +135,17 @@ __device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double q
   // from a faulted particle's weights would still poison the accumulator)
   const double qw = ok ? qv : 0.0, ow = ok ? 1.0 : 0.0;
   const double wx0 = qw * (1.0 - fx), wx1 = qw * fx;
-  sw[0 * 32 + lane] = wx0 * (1.0 - fy);
-  sw[1 * 32 + lane] = wx1 * (1.0 - fy);
-  sw[2 * 32 + lane] = wx0 * fy;
-  sw[3 * 32 + lane] = wx1 * fy;
-  sw[4 * 32 + lane] = ow * (1.0 - fz);
-  sw[5 * 32 + lane] = ow * fz;
+  const double wxy[4] = {wx0 * (1.0 - fy), wx1 * (1.0 - fy), wx0 * fy, wx1 * fy};
+  const double wz[2] = {ow * (1.0 - fz), ow * fz};
+  if (W8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sw[c * kDepRow + lane] = wxy[c & 3] * wz[c >> 2];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sw[c * kDepRow + lane] = wxy[c];
+    sw[4 * kDepRow + lane] = wz[0];
+    sw[5 * kDepRow + lane] = wz[1];
+  }
   const long long key =
       ok ? i + static_cast<long long>(g.nx) * (j + static_cast<long long>(g.ny) * k) : -1;
   const unsigned okm = __ballot_sync(FULL, ok);
@@ -170,7 +184,7 @@ __device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double q
     gk = __shfl_sync(FULL, k, leader);
     rest &= ~g1;
   }
-  dep_pass<TILE>(C, sw, buf, row0, carry, g1, lane);
+  dep_pass<MS, W8>(C, sw, mrow, carry, g1, lane);
   if (g1) dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
   // further passes for groups of >= 2 (B2M_DEP_PASSES of them, largest first)
 #pragma unroll 1
@@ -187,19 +201,19 @@ __device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double q
     gj = __shfl_sync(FULL, j, leader);
     gk = __shfl_sync(FULL, k, leader);
     rest &= ~gm;
-    dep_pass<TILE>(C, sw, buf, row0, 0u, gm, lane);
+    dep_pass<MS, W8>(C, sw, mrow, 0u, gm, lane);
     dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
   }
   if (rest) {
     // everything else (strays drifted out of the sorted order): each lane
     // adds its own particle's 32 terms to the mesh, all lanes at once
     if ((rest >> lane) & 1u) {
-      const double u = buf[3][p], v = buf[4][p], w = buf[5][p];
+      const double u = mrow[lane], v = mrow[MS + lane], w = mrow[2 * MS + lane];
       const int i1 = i + 1 == g.nx ? 0 : i + 1, j1 = j + 1 == g.ny ? 0 : j + 1,
                 k1 = k + 1 == g.nz ? 0 : k + 1;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const double wq = sw[(c & 3) * 32 + lane] * sw[(4 + (c >> 2)) * 32 + lane];
+        const double wq = wxy[c & 3] * wz[c >> 2];
         const long long node =
             ((c & 1) ? i1 : i) +
             static_cast<long long>(g.nx) *
@@ -214,7 +228,8 @@ __device__ __forceinline__ void dep_row(DepCarry& C, const FastGrid& g, double q
   __syncwarp();  // the stage is rewritten by the next row
 }
 
-__device__ __forceinline__ void dep_finish(DepCarry& C, const FastGrid& g, double* const* mom,
+template <class G>
+__device__ __forceinline__ void dep_finish(DepCarry& C, const G& g, double* const* mom,
                                            int lane) {
   if (C.key >= 0) dep_flush_half(C.d0, C.d1, 0, C.ci, C.cj, C.ck, g, mom, lane);
   C.key = -1;

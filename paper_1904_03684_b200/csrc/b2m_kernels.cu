@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       auto after = [&](int j, unsigned bad, double y1) {
         const int p = lane + 32 * j;
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (DEP) dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, buf[st], 32 * j, p < cnt && !bad, lane);
+        if (DEP)
+          dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
+                      buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
@@ -252,7 +254,9 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
             F.U.rounds == 3 ? fast_particle_v2<WT, 3>(F.fg, F.U, cells, buf[st], p, cnt, C)
                             : fast_particle_v2<WT, 0>(F.fg, F.U, cells, buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (DEP) dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, buf[st], 32 * j, p < cnt && !bad, lane);
+        if (DEP)
+          dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
+                      buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {

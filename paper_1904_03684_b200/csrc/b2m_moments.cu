@@ -17,6 +17,7 @@
 // 262 adds per-worker meshes).  A first kernel that gave every lane its own
 // contiguous range and flushed a run at every change of cell degraded 4.5x
 // with drift since the last sort; profiles/README.md has both.
+#include "b2m_fused.cuh"
 #include "b2m_internal.hpp"
 
 namespace b2m {
@@ -43,6 +44,12 @@ struct MomentPtrs {
 //    directly; a group writes its terms to shared-memory rows and lane j sums
 //    column j over them before one atomic per column.
 constexpr int kGroupThreads = 128;
+#ifndef B2M_DMMA_MINB
+#define B2M_DMMA_MINB 6  // blocks per SM of the DMMA deposit (<= 85 registers)
+#endif
+#ifndef B2M_DEP_DMMA
+#define B2M_DEP_DMMA 1  // FAST rho + J: the DMMA kernel (0: the register-carry kernel)
+#endif
 #ifndef B2M_DEP_DIRECT_MAX
 #define B2M_DEP_DIRECT_MAX 1  // groups up to this size add their terms with direct atomics
 #endif
@@ -252,6 +259,56 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
   if (ckey >= 0) flush_carry();
 }
 
+// FAST rho + J (set 0) with the fused mover's deposit machinery
+// (b2m_fused.cuh): a warp streams its contiguous span 32 particles at a time
+// (the next row prefetched into registers), stages the 8 corner weights and
+// u, v, w per lane (3.2 KB per warp), and runs one FP64 DMMA pass per row --
+// the carried cell's sums live in the 8x8 accumulator (2 registers per lane),
+// the row's largest other cell rides in the other half and is flushed, strays
+// add their terms with direct atomics.  ~70 registers instead of 166, so 8
+// blocks (32 warps) per SM hide the loads that bound the register-carry
+// kernel.
+constexpr int kDmmaThreads = 128;
+__global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
+    deposit_dmma_kernel(const __grid_constant__ DevGrid g, const __grid_constant__ SpeciesLaunch sp,
+                        double qv, const __grid_constant__ MomentPtrs M,
+                        unsigned long long span, FaultWord* fault) {
+  __shared__ __align__(16) double sbuf[kDmmaThreads / 32][11 * kDepRow];
+  const int lane = threadIdx.x & 31;
+  double* const sw = sbuf[threadIdx.x >> 5];
+  const unsigned long long wid =
+      (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long lb = wid * span;
+  if (lb >= sp.n) return;
+  const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
+  DepCarry C;
+  dep_reset(C);
+  auto load = [&](unsigned long long p, double (&q)[6]) {
+    if (p < le) {
+      q[0] = sp.x[p]; q[1] = sp.y[p]; q[2] = sp.z[p];
+      q[3] = sp.u[p]; q[4] = sp.v[p]; q[5] = sp.w[p];
+    }
+  };
+  double nxt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  load(lb + lane, nxt);
+  for (unsigned long long base = lb; base < le; base += 32) {
+    const unsigned long long p = base + lane;
+    bool ok = p < le;
+    const double px = nxt[0], py = nxt[1], pz = nxt[2];
+    sw[8 * kDepRow + lane] = nxt[3];
+    sw[9 * kDepRow + lane] = nxt[4];
+    sw[10 * kDepRow + lane] = nxt[5];
+    load(p + 32, nxt);
+    // grid.hpp:65-67: the reference throws DomainError
+    if (ok && !(px >= 0.0 && px < g.lx && py >= 0.0 && py < g.ly && pz >= 0.0 && pz < g.lz)) {
+      atomicMin(&fault->domain, fault_key(sp.species, sp.base + p));
+      ok = false;
+    }
+    dep_row<kDepRow, true>(C, g, qv, M.m, sw, sw + 8 * kDepRow, px, py, pz, ok, lane);
+  }
+  dep_finish(C, g, M.m, lane);
+}
+
 template <int SET, bool EXACT>
 void launch_group(const DevGrid& g, const SpeciesLaunch& sp, double qv, const MomentPtrs& M,
                   FaultWord* fault, cudaStream_t st) {
@@ -281,8 +338,25 @@ void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double
   if (sp.n == 0) return;
   MomentPtrs M{};
   for (int m = 0; m < (pressure ? 10 : 4); ++m) M.m[m] = mesh[m];
-  if (exact) launch_group<0, true>(g, sp, qv, M, fault, st);
-  else launch_group<0, false>(g, sp, qv, M, fault, st);
+  if (exact) {
+    launch_group<0, true>(g, sp, qv, M, fault, st);
+  } else if (B2M_DEP_DMMA) {
+    static const int per_sm = [] {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_dmma_kernel, kDmmaThreads, 0);
+      return b > 0 ? b : 1;
+    }();
+    const unsigned long long warps =
+        static_cast<unsigned long long>(device_sms()) * per_sm * (kDmmaThreads / 32);
+    unsigned long long span = (sp.n + warps - 1) / warps;
+    span = (span + 31) / 32 * 32;
+    const unsigned long long used = (sp.n + span - 1) / span;
+    const int blocks = static_cast<int>((used + kDmmaThreads / 32 - 1) / (kDmmaThreads / 32));
+    deposit_dmma_kernel<<<blocks, kDmmaThreads, 0, st>>>(g, sp, qv, M, span, fault);
+    note_launch();
+  } else {
+    launch_group<0, false>(g, sp, qv, M, fault, st);
+  }
   if (pressure) {
     if (exact) launch_group<1, true>(g, sp, qv, M, fault, st);
     else launch_group<1, false>(g, sp, qv, M, fault, st);
