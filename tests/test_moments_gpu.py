@@ -409,3 +409,60 @@ def test_fused_full_c2_vs_separate(gpu):
                          torch.sort(tb)[0].view(torch.int64)).all()), (s, c)
     a.close()
     b_.close()
+
+
+def _fast_store_deposit(p, grid, q):
+    g = Grid.make(*grid)
+    st = DeviceStore(g, [len(p[0])], "fast")
+    st.upload_field(gem.gem_field(g))
+    st.upload(0, p)
+    st.moments_zero(False)
+    st.deposit(0, q)
+    m = MomentMesh.make(g, False)
+    st.moments_download(m)
+    st.close()
+    return m
+
+
+@pytest.mark.parametrize("order", ["random", "sorted", "sorted_jittered", "one_cell"])
+def test_fast_dmma_deposit_paths_vs_oracle(gpu, order):
+    """The FAST rho + J kernel (deposit_dmma_kernel) on every path: rows in
+    one cell (the carried cell across rows), runs across rows, groups taken
+    by the extra DMMA passes, strays by direct atomics (random order), one
+    cell holding everything; a ragged tail."""
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    n = 100_003
+    p = random_particles(grid, n, 43, vscale=1.0)
+    if order == "one_cell":
+        p[0] = 1.0 + 0.999 * (p[0] / 4.0)
+        p[1] = 2.0 + 0.999 * (p[1] / 4.0)
+        p[2] = 3.0 + 0.999 * (p[2] / 4.0)
+    cell = (np.floor(p[0]).astype(np.int64) + 4 * (np.floor(p[1]).astype(np.int64)
+            + 4 * np.floor(p[2]).astype(np.int64)))
+    if order in ("sorted", "sorted_jittered"):
+        perm = np.argsort(cell, kind="stable")
+        if order == "sorted_jittered":
+            rng = np.random.default_rng(9)
+            for a, b in rng.integers(0, n, size=(n // 10, 2)):
+                perm[a], perm[b] = perm[b], perm[a]
+        p = [np.ascontiguousarray(a[perm]) for a in p]
+    m = _fast_store_deposit(p, grid, 0.003)
+    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.003, False),
+                         what=f"fast {order}")
+
+
+def test_fast_dmma_deposit_domain_error(gpu):
+    """A particle outside the domain: DomainError from the FAST kernel too
+    (grid.hpp:65-67)."""
+    grid = (4, 4, 4, 4.0, 4.0, 4.0)
+    p = random_particles(grid, 1000, 5)
+    p[0][777] = 4.0
+    g = Grid.make(*grid)
+    st = DeviceStore(g, [1000], "fast")
+    st.upload_field(gem.gem_field(g))
+    st.upload(0, p)
+    st.moments_zero(False)
+    st.deposit(0, 1.0)
+    with pytest.raises(DomainError, match="outside domain"):
+        st.sync()
+    st.close()
