@@ -319,7 +319,9 @@ b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
  * is deterministic and identical on all ranks (unlike an ncclAllReduce,
  * whose order depends on the NCCL algorithm).  Each rank's own mesh still
  * sums its particles with FP64 atomics (equal to the reference to rounding).
- * The gather buffer (world x mesh) is allocated on the first call. */
+ * The gather buffer (world x mesh) is reserved with the mesh
+ * (b2m_moments_zero, or b2m_world_init when the mesh exists): the reduction
+ * allocates nothing. */
 b2m_status b2m_world_reduce_moments(b2m_ctx* ctx);
 b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* sent,
                           uint64_t* global_count);

@@ -1048,6 +1048,7 @@ b2m_status b2m_moments_zero(b2m_ctx* ctx, int with_pressure) {
     if ((st = dalloc(ctx, &blk, na * nodes, "moment mesh")) != B2M_OK) return st;
     for (int a = 0; a < 10; ++a) ctx->mom[a] = a < na ? blk + a * nodes : nullptr;
     ctx->mom_arrays = na;
+    if ((st = world_reserve_moments(ctx, na * nodes)) != B2M_OK) return st;
   }
   for (int a = 0; a < na; ++a)
     B2M_CUDA(ctx, cudaMemsetAsync(ctx->mom[a], 0, nodes * sizeof(double), ctx->stream));

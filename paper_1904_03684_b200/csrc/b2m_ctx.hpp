@@ -168,6 +168,8 @@ struct b2m_ctx {
 namespace b2m {
 
 b2m_status cuda_fail(b2m_ctx* ctx, cudaError_t e, const char* what);
+// b2m_world.cu: reserve the moment all-gather buffer for an n-double mesh
+b2m_status world_reserve_moments(b2m_ctx* ctx, uint64_t n);
 b2m_status check_ctx(b2m_ctx* ctx);
 b2m_status check_species(b2m_ctx* ctx, int s);
 b2m_status check_params(const b2m_mover_params* mp);

@@ -65,6 +65,19 @@ __global__ void ordered_sum_kernel(const double* __restrict__ stage, unsigned lo
 }
 
 }  // namespace
+
+// The all-gather buffer of b2m_world_reduce_moments (world x mesh doubles),
+// reserved with the moment mesh (b2m_moments_zero) or at b2m_world_init when
+// the mesh exists already, so the reduction itself allocates nothing.
+b2m_status world_reserve_moments(b2m_ctx* ctx, uint64_t n) {
+  if (!ctx->w.on || !ctx->w.comm || ctx->w.mstage_n >= n) return B2M_OK;
+  b2m_status st = dalloc(ctx, &ctx->w.mstage, static_cast<size_t>(ctx->sl.world) * n,
+                         "moment gather buffer");
+  if (st != B2M_OK) return st;
+  ctx->w.mstage_n = n;
+  return B2M_OK;
+}
+
 }  // namespace b2m
 
 using namespace b2m;
@@ -258,7 +271,12 @@ b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world) {
     B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
   for (auto& c : cap) c *= 2;  // from prev + from next
-  return world_alloc(ctx, cap);
+  if ((st = world_alloc(ctx, cap)) != B2M_OK) return st;
+  if (ctx->mom[0]) {  // a moment mesh exists: its gather buffer now
+    const uint64_t nodes = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
+    return world_reserve_moments(ctx, static_cast<uint64_t>(ctx->mom_arrays) * nodes);
+  }
+  return B2M_OK;
 }
 
 b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
@@ -296,12 +314,7 @@ b2m_status b2m_world_reduce_moments(b2m_ctx* ctx) {
     // order depends on the algorithm and protocol): every rank gathers all
     // meshes and adds them in rank order
     const int world = ctx->sl.world;
-    if (ctx->w.mstage_n < n) {  // sized for the mesh in use (4 or 10 arrays)
-      if ((st = dalloc(ctx, &ctx->w.mstage, static_cast<size_t>(world) * n,
-                       "moment gather buffer")) != B2M_OK)
-        return st;
-      ctx->w.mstage_n = n;
-    }
+    if ((st = world_reserve_moments(ctx, n)) != B2M_OK) return st;  // normally a no-op
     B2M_NCCL(ctx, nccl().AllGather(mesh, ctx->w.mstage, n, ncclFloat64, ctx->w.comm,
                                    ctx->stream));
     const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, 4096);
