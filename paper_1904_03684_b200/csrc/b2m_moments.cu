@@ -47,6 +47,9 @@ constexpr int kGroupThreads = 128;
 #ifndef B2M_DMMA_MINB
 #define B2M_DMMA_MINB 6  // blocks per SM of the DMMA deposit (<= 85 registers)
 #endif
+#ifndef B2M_DEP_WSORT
+#define B2M_DEP_WSORT 0  // 1: sort windows of 128 particles by cell in the warp (measured slower)
+#endif
 #ifndef B2M_DEP_DMMA
 #define B2M_DEP_DMMA 1  // FAST rho + J: the DMMA kernel (0: the register-carry kernel)
 #endif
@@ -274,6 +277,7 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
                         double qv, const __grid_constant__ MomentPtrs M,
                         unsigned long long span, FaultWord* fault) {
   __shared__ __align__(16) double sbuf[kDmmaThreads / 32][11 * kDepRow];
+  __shared__ __align__(16) double wbuf[kDmmaThreads / 32][B2M_DEP_WSORT ? 6 : 1][4 * 32];
   const int lane = threadIdx.x & 31;
   double* const sw = sbuf[threadIdx.x >> 5];
   const unsigned long long wid =
@@ -283,6 +287,98 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
   const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
   DepCarry C;
   dep_reset(C);
+  if (B2M_DEP_WSORT) {
+    // Windows of 4 rows (128 particles): loaded together, sorted by cell in
+    // the warp (bitonic network over (key << 8 | slot), 4 per lane), then
+    // deposited row by row in cell order -- so particles that drifted out of
+    // the sorted order meet their cell-mates of the window in one DMMA group
+    // instead of taking a stray's 32 atomics.  An already sorted window (a
+    // freshly sorted species) skips the network.
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int WR = 4;
+    constexpr unsigned long long kInvalid = 0xffffffffull;
+    double (*const win)[WR * 32] = wbuf[threadIdx.x >> 5];
+    for (unsigned long long base = lb; base < le; base += WR * 32) {
+      unsigned long long pk[WR];
+#pragma unroll
+      for (int r = 0; r < WR; ++r) {
+        const unsigned long long p = base + 32 * r + lane;
+        const int slot = 32 * r + lane;
+        unsigned long long key = kInvalid;
+        if (p < le) {
+          const double px = sp.x[p], py = sp.y[p], pz = sp.z[p];
+          win[0][slot] = px; win[1][slot] = py; win[2][slot] = pz;
+          win[3][slot] = sp.u[p]; win[4][slot] = sp.v[p]; win[5][slot] = sp.w[p];
+          if (px >= 0.0 && px < g.lx && py >= 0.0 && py < g.ly && pz >= 0.0 && pz < g.lz) {
+            const int i = min(__double2int_rz(px * g.rdx), g.nx - 1);
+            const int j = min(__double2int_rz(py * g.rdy), g.ny - 1);
+            const int k = min(__double2int_rz(pz * g.rdz), g.nz - 1);
+            // the cell sort's order (z fastest, b2m_kernels.cu cell_key), so a
+            // freshly sorted window passes the check below
+            key = static_cast<unsigned long long>(k) +
+                  static_cast<unsigned long long>(g.nz) *
+                      (static_cast<unsigned long long>(i) +
+                       static_cast<unsigned long long>(g.nx) * static_cast<unsigned long long>(j));
+          } else {
+            atomicMin(&fault->domain, fault_key(sp.species, sp.base + p));
+          }
+        }
+        pk[r] = (key << 8) | static_cast<unsigned long long>(slot);
+      }
+      // sorted already?  (position 32r + lane <= its successor)
+      bool sorted = true;
+#pragma unroll
+      for (int r = 0; r < WR; ++r) {
+        unsigned long long nx = __shfl_down_sync(FULL, pk[r], 1);
+        const unsigned long long wrap = __shfl_sync(FULL, pk[r + 1 < WR ? r + 1 : r], 0);
+        if (lane == 31) nx = r + 1 < WR ? wrap : ~0ull;
+        sorted = sorted && (pk[r] >> 8) <= (nx >> 8);
+      }
+      if (!__all_sync(FULL, sorted)) {
+#pragma unroll
+        for (int k = 2; k <= WR * 32; k <<= 1) {
+#pragma unroll
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+              const int rj = j >> 5;
+#pragma unroll
+              for (int r = 0; r < WR; ++r) {
+                if (r & rj) continue;
+                const bool asc = ((32 * r + lane) & k) == 0;
+                const unsigned long long a = pk[r], b = pk[r | rj];
+                if ((a > b) == asc) {
+                  pk[r] = b;
+                  pk[r | rj] = a;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < WR; ++r) {
+                const unsigned long long o = __shfl_xor_sync(FULL, pk[r], j);
+                const bool asc = ((32 * r + lane) & k) == 0;
+                const bool lower = (lane & j) == 0;
+                pk[r] = (lower == asc) ? (pk[r] < o ? pk[r] : o) : (pk[r] < o ? o : pk[r]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll 1
+      for (int r = 0; r < WR; ++r) {
+        if (base + 32 * r >= le) break;
+        const int slot = static_cast<int>(pk[r] & 0xff);
+        const bool ok = (pk[r] >> 8) != kInvalid;
+        sw[8 * kDepRow + lane] = win[3][slot];
+        sw[9 * kDepRow + lane] = win[4][slot];
+        sw[10 * kDepRow + lane] = win[5][slot];
+        dep_row<kDepRow, true>(C, g, qv, M.m, sw, sw + 8 * kDepRow, win[0][slot], win[1][slot],
+                               win[2][slot], ok, lane);
+      }
+      __syncwarp();  // the window is rewritten by the next one
+    }
+    dep_finish(C, g, M.m, lane);
+    return;
+  }
   auto load = [&](unsigned long long p, double (&q)[6]) {
     if (p < le) {
       q[0] = sp.x[p]; q[1] = sp.y[p]; q[2] = sp.z[p];
