@@ -738,7 +738,10 @@ def run_world(args):
         dist.all_gather_object(out, obj)
         return out
 
-    native = backend == "nccl" and os.environ.get("B2M_NATIVE_WORLD", "1") != "0"
+    # the native world over NCCL; B2M_NATIVE_WORLD=force also with a gloo
+    # process group (ranks sharing a GPU with B2M_NCCL_LIB = tests/fake_nccl)
+    nw_env = os.environ.get("B2M_NATIVE_WORLD", "1")
+    native = nw_env == "force" or (backend == "nccl" and nw_env != "0")
     field_of = (lambda g: gem.gem_bench_field(g)) if args.field == "gem+E" \
         else (lambda g: gem.gem_field(g))
 

@@ -1205,7 +1205,8 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
   if ((st = dalloc(ctx, &ctx->mig_tcnt, tiles, "tile counts")) != B2M_OK) return st;
   if ((st = dalloc(ctx, &ctx->mig_toff, tiles, "tile offsets")) != B2M_OK) return st;
   if ((st = dalloc(ctx, &ctx->mig_totals, 3 * ns, "migration totals")) != B2M_OK) return st;
-  B2M_CUDA(ctx, cudaMemset(ctx->mig_tcnt, 0, tiles * sizeof(unsigned long long)));
+  B2M_CUDA(ctx, cudaMemsetAsync(ctx->mig_tcnt, 0, tiles * sizeof(unsigned long long),
+                                ctx->stream));  // ordered with the movers on ctx->stream
   if (cudaMallocHost(&ctx->mig_totals_h, 3 * ns * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return fail(B2M_ALLOC_ERROR, "pinned migration totals");

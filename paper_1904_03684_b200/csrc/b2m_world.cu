@@ -5,6 +5,7 @@
 // check -- and the same phases over several in-process ranks with device
 // copies in place of NCCL (b2m_world_loopback_step, for tests).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -20,7 +21,17 @@ namespace b2m {
 const NcclApi& nccl() {
   static const NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's own, if any
+    // B2M_NCCL_LIB: an explicit library (tests: tests/fake_nccl, several
+    // ranks on one GPU); else the process's own libnccl, if any
+    void* h = nullptr;
+    if (const char* lib = std::getenv("B2M_NCCL_LIB")) {
+      h = dlopen(lib, RTLD_NOW | RTLD_LOCAL);
+      if (!h) {
+        a.why = std::string("B2M_NCCL_LIB: ") + dlerror();
+        return a;
+      }
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW);
     if (!h) {
@@ -229,10 +240,17 @@ b2m_status world_alloc(b2m_ctx* ctx, const std::vector<uint64_t>& stage_cap) {
                      "exchange buffer")) != B2M_OK)
       return st;
   }
-  B2M_CUDA(ctx, cudaMemcpy(w.totals, tp.data(), ns * sizeof(void*), cudaMemcpyHostToDevice));
-  B2M_CUDA(ctx, cudaMemcpy(w.cap, cap.data(), ns * sizeof(unsigned long long),
-                           cudaMemcpyHostToDevice));
-  B2M_CUDA(ctx, cudaMemset(w.cnt_recv, 0, 2 * ns * sizeof(unsigned long long)));
+  // on the context's (non-blocking) stream, complete before the host buffers
+  // go away: a legacy-stream cudaMemcpy / cudaMemset is not ordered with the
+  // work later enqueued on ctx->stream (a pageable H2D may still be in flight
+  // when cudaMemcpy returns) -- found by tests/fake_nccl, whose collectives
+  // read the buffers through ctx->stream
+  B2M_CUDA(ctx, cudaMemcpyAsync(w.totals, tp.data(), ns * sizeof(void*), cudaMemcpyHostToDevice,
+                                ctx->stream));
+  B2M_CUDA(ctx, cudaMemcpyAsync(w.cap, cap.data(), ns * sizeof(unsigned long long),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  B2M_CUDA(ctx, cudaMemsetAsync(w.cnt_recv, 0, 2 * ns * sizeof(unsigned long long), ctx->stream));
+  B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   w.on = true;
   return B2M_OK;
 }
@@ -264,7 +282,8 @@ b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world) {
     // exchange buffers hold the largest outbox any rank can send
     unsigned long long* d = nullptr;
     if ((st = dalloc(ctx, &d, std::max<size_t>(1, ns), "world caps")) != B2M_OK) return st;
-    B2M_CUDA(ctx, cudaMemcpy(d, cap.data(), ns * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    B2M_CUDA(ctx, cudaMemcpyAsync(d, cap.data(), ns * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                  ctx->stream));  // ordered before the all-reduce on ctx->stream
     B2M_NCCL(ctx, nccl().AllReduce(d, d, ns, ncclUint64, ncclMax, ctx->w.comm, ctx->stream));
     B2M_CUDA(ctx, cudaMemcpyAsync(cap.data(), d, ns * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                   ctx->stream));

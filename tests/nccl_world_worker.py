@@ -3,7 +3,8 @@ test_world_nccl_gpu.py, one process per GPU):
 
     python tests/nccl_world_worker.py RANK WORLD PORT OUTDIR CYCLES MODE
 
-The rank holds its y-slab of the GEM state on GPU RANK in a STRICT device
+The rank holds its y-slab of the GEM state on GPU RANK (GPU 0 for every rank
+with B2M_NCCL_LIB = the fake NCCL of tests/fake_nccl) in a STRICT device
 store and runs CYCLES of b2m_world_step (mover + owner scan + compaction +
 grouped ncclSend/ncclRecv with prev/next + merge + count all-reduce) through
 NativeSlabWorld, then deposits rho/J/pressure and reduces them across ranks
@@ -35,14 +36,21 @@ def main():
                                                sys.argv[4], int(sys.argv[5]), sys.argv[6])
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=port, RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+    # B2M_NCCL_LIB (tests/fake_nccl): every rank on GPU 0, torch.distributed
+    # over gloo (it only carries the unique id); else one GPU per rank
+    fake = bool(os.environ.get("B2M_NCCL_LIB"))
+    dev = 0 if fake else rank
+    torch.cuda.set_device(dev)
+    if fake:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     grid = Grid.make(*GRID)
     batches = gem.init_gem_slab(grid, PPC, rank, world, pinned=False)
     p6s = [b.span() for b in batches]
     if mode == "nan" and rank == 1:
         p6s[0][3][5] = np.nan
-    st = DeviceStore(grid, [int(b.count() * 1.5) + 4096 for b in batches], "strict", device=rank)
+    st = DeviceStore(grid, [int(b.count() * 1.5) + 4096 for b in batches], "strict", device=dev)
     st.upload_field(gem.gem_field(grid))
     for s, p in enumerate(p6s):
         st.upload(s, p)

@@ -39,12 +39,13 @@ def _free_port():
     return p
 
 
-def _run(world, cycles, mode):
+def _run(world, cycles, mode, env=None):
     d = tempfile.mkdtemp(prefix="b2m_nccl_")
     port = str(_free_port())
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "nccl_world_worker.py"),
                                str(r), str(world), port, d, str(cycles), mode],
-                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                              env=dict(os.environ, **(env or {})))
              for r in range(world)]
     for p in procs:
         try:
@@ -56,13 +57,18 @@ def _run(world, cycles, mode):
     return d, [p.stdout.read().decode(errors="replace") for p in procs]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_nccl_world_matches_reference_simulation(gpu, world):
-    if _gpus() < world:
-        pytest.skip(f"needs {world} GPUs (one rank per GPU), found {_gpus()}")
-    if not oracle.ref_available():
-        pytest.skip("reference library not built")
-    d, logs = _run(world, 3, "ok")
+def fake_nccl_lib():
+    """tests/fake_nccl built into a temporary directory (test infrastructure:
+    several native-world ranks on one GPU through host shared memory)."""
+    out = os.path.join(tempfile.mkdtemp(prefix="b2m_fake_nccl_"), "libfakenccl.so")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", out,
+                    os.path.join(HERE, "fake_nccl", "fake_nccl.cpp"), f"-I{cuda}/include",
+                    f"-L{cuda}/lib64", "-lcudart", "-lrt"], check=True)
+    return out
+
+
+def _check_world_vs_reference(world, d, logs):
     for r in range(world):
         err = os.path.join(d, f"rank{r}.err")
         assert os.path.exists(os.path.join(d, f"rank{r}.npz")), \
@@ -93,6 +99,38 @@ def test_nccl_world_matches_reference_simulation(gpu, world):
     for a in range(10):
         scale = float(np.max(np.abs(want[a])))
         assert float(np.max(np.abs(got[a] - want[a]))) <= 1e-12 * max(scale, 1e-300)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_native_world_over_fake_nccl_one_gpu(gpu, world):
+    """The native slab world's multi-rank protocol (b2m_world_step with real
+    peers: counts and records over grouped send/recv, merge, count check;
+    the field broadcast; the ordered moments reduction) in separate
+    processes on ONE GPU, through tests/fake_nccl (host shared memory, NCCL's
+    posting-order matching) -- runnable on this round's one-GPU boxes;
+    against the reference's multi-worker Simulation as a bitwise multiset."""
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    d, logs = _run(world, 3, "ok", env={"B2M_NCCL_LIB": fake_nccl_lib()})
+    _check_world_vs_reference(world, d, logs)
+
+
+def test_native_world_over_fake_nccl_fault_on_one_rank(gpu):
+    d, logs = _run(2, 1, "nan", env={"B2M_NCCL_LIB": fake_nccl_lib()})
+    errs = [open(os.path.join(d, f"rank{r}.err")).read() if os.path.exists(
+        os.path.join(d, f"rank{r}.err")) else "" for r in range(2)]
+    assert errs[1].startswith("NumericalFault"), (errs, logs)
+    assert errs[0].startswith("EngineFault"), (errs, logs)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_world_matches_reference_simulation(gpu, world):
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs (one rank per GPU), found {_gpus()}")
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    d, logs = _run(world, 3, "ok")
+    _check_world_vs_reference(world, d, logs)
 
 
 def test_nccl_world_fault_on_one_rank_aborts_all(gpu):
