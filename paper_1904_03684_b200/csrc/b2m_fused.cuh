@@ -228,6 +228,124 @@ __device__ __forceinline__ void dep_row(DepCarry& C, const G& g, double qv, doub
   __syncwarp();  // the stage is rewritten by the next row
 }
 
+// ---- the pressure tensor (set 1: p_ab = sum w u_a u_b) ------------------
+// Same fragments, 6 of the 8 accumulator columns: {uu, uv, uw, vv, vw, ww} of
+// the members of one cell; the carried cell keeps D across rows, every other
+// group of >= 2 takes a pass into the temporary E, strays add their 48 terms
+// with direct atomics.
+__device__ __forceinline__ void dep_pass_p(double& d0, double& d1, const double* sw,
+                                           const double* mrow, int ms, unsigned mask, int lane) {
+  const int q = lane & 3, n = lane >> 2;
+  const int a = n < 3 ? 0 : (n < 5 ? 1 : 2);               // u_a of column n
+  const int b = n < 3 ? n : (n < 5 ? n - 2 : 2);           // u_b of column n
+  const double* ma = mrow + a * ms;
+  const double* mb = mrow + b * ms;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int pl = 4 * k + q;
+    const double av = sw[n * kDepRow + pl];
+    double bv = 0.0;
+    if (n < 6 && ((mask >> pl) & 1u)) bv = ma[pl] * mb[pl];
+    dmma_8x8x4(d0, d1, av, bv);
+  }
+}
+
+// flush columns 0-5 of a pressure accumulator to mom[4..9] at cell (ci, cj, ck)
+template <class G>
+__device__ __forceinline__ void dep_flush_p(double& d0, double& d1, int ci, int cj, int ck,
+                                            const G& g, double* const* mom, int lane) {
+  const int q = lane & 3;
+  if (q < 3) {
+    const int c = lane >> 2;
+    const int ii = (c & 1) ? (ci + 1 == g.nx ? 0 : ci + 1) : ci;
+    const int jj = (c & 2) ? (cj + 1 == g.ny ? 0 : cj + 1) : cj;
+    const int kk = (c & 4) ? (ck + 1 == g.nz ? 0 : ck + 1) : ck;
+    const long long node =
+        ii + static_cast<long long>(g.nx) * (jj + static_cast<long long>(g.ny) * kk);
+    atomicAdd(mom[4 + 2 * q] + node, d0);
+    atomicAdd(mom[4 + 2 * q + 1] + node, d1);
+  }
+  d0 = 0.0;
+  d1 = 0.0;
+}
+
+// One row of the pressure deposit; the 8 corner weights staged in sw rows
+// 0-7 (W8 layout) and u, v, w in mrow (stride ms).
+template <class G>
+__device__ __forceinline__ void dep_row_p(DepCarry& C, const G& g, double qv, double* const* mom,
+                                          double* sw, const double* mrow, int ms, double px,
+                                          double py, double pz, bool ok, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const double sx = px * g.rdx, sy = py * g.rdy, sz = pz * g.rdz;
+  int i = max(min(__double2int_rz(sx), g.nx - 1), 0), j = max(min(__double2int_rz(sy), g.ny - 1), 0),
+      k = max(min(__double2int_rz(sz), g.nz - 1), 0);
+  const double fx = fmin(sx - static_cast<double>(i), 1.0);
+  const double fy = fmin(sy - static_cast<double>(j), 1.0);
+  const double fz = fmin(sz - static_cast<double>(k), 1.0);
+  const double qw = ok ? qv : 0.0, ow = ok ? 1.0 : 0.0;
+  const double wx0 = qw * (1.0 - fx), wx1 = qw * fx;
+  const double wxy[4] = {wx0 * (1.0 - fy), wx1 * (1.0 - fy), wx0 * fy, wx1 * fy};
+  const double wz[2] = {ow * (1.0 - fz), ow * fz};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) sw[c * kDepRow + lane] = wxy[c & 3] * wz[c >> 2];
+  const long long key =
+      ok ? i + static_cast<long long>(g.nx) * (j + static_cast<long long>(g.ny) * k) : -1;
+  const unsigned okm = __ballot_sync(FULL, ok);
+  __syncwarp();
+  if (okm == 0) return;
+  const unsigned grp = __match_any_sync(FULL, key);
+  const unsigned score = ok ? (static_cast<unsigned>(__popc(grp)) << 6) |
+                                  (((grp >> 31) & 1u) << 5) | static_cast<unsigned>(lane)
+                            : 0u;
+  const unsigned best = __reduce_max_sync(FULL, score);
+  const int bl = best & 31;
+  const int ncar = __popc(__ballot_sync(FULL, ok && key == C.key));
+  if (ncar < static_cast<int>(best >> 6)) {
+    if (C.key >= 0) dep_flush_p(C.d0, C.d1, C.ci, C.cj, C.ck, g, mom, lane);
+    C.key = __shfl_sync(FULL, key, bl);
+    C.ci = __shfl_sync(FULL, i, bl);
+    C.cj = __shfl_sync(FULL, j, bl);
+    C.ck = __shfl_sync(FULL, k, bl);
+  }
+  const unsigned carry = __ballot_sync(FULL, ok && key == C.key);
+  unsigned rest = okm & ~carry;
+  if (carry) dep_pass_p(C.d0, C.d1, sw, mrow, ms, carry, lane);
+#pragma unroll 1
+  for (int x = 0; x < 1 + B2M_DEP_PASSES && rest; ++x) {
+    const unsigned s2 = ((rest >> lane) & 1u)
+                            ? (static_cast<unsigned>(__popc(grp & rest)) << 6) |
+                                  static_cast<unsigned>(lane)
+                            : 0u;
+    const unsigned b2 = __reduce_max_sync(FULL, s2);
+    if ((b2 >> 6) < 2) break;
+    const int leader = b2 & 31;
+    const unsigned gm = __shfl_sync(FULL, grp, leader);
+    const int gi = __shfl_sync(FULL, i, leader), gj = __shfl_sync(FULL, j, leader),
+              gk = __shfl_sync(FULL, k, leader);
+    rest &= ~gm;
+    double e0 = 0.0, e1 = 0.0;
+    dep_pass_p(e0, e1, sw, mrow, ms, gm, lane);
+    dep_flush_p(e0, e1, gi, gj, gk, g, mom, lane);
+  }
+  if ((rest >> lane) & 1u) {
+    const double u = mrow[lane], v = mrow[ms + lane], w = mrow[2 * ms + lane];
+    const double m6[6] = {u * u, u * v, u * w, v * v, v * w, w * w};
+    const int i1 = i + 1 == g.nx ? 0 : i + 1, j1 = j + 1 == g.ny ? 0 : j + 1,
+              k1 = k + 1 == g.nz ? 0 : k + 1;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double wq = wxy[c & 3] * wz[c >> 2];
+      const long long node =
+          ((c & 1) ? i1 : i) +
+          static_cast<long long>(g.nx) *
+              (((c & 2) ? j1 : j) + static_cast<long long>(g.ny) * ((c & 4) ? k1 : k));
+#pragma unroll
+      for (int m = 0; m < 6; ++m) atomicAdd(mom[4 + m] + node, wq * m6[m]);
+    }
+  }
+  __syncwarp();
+}
+
 template <class G>
 __device__ __forceinline__ void dep_finish(DepCarry& C, const G& g, double* const* mom,
                                            int lane) {

@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
 // blocks (32 warps) per SM hide the loads that bound the register-carry
 // kernel.
 constexpr int kDmmaThreads = 128;
+template <int SET>
 __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
     deposit_dmma_kernel(const __grid_constant__ DevGrid g, const __grid_constant__ SpeciesLaunch sp,
                         double qv, const __grid_constant__ MomentPtrs M,
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
   const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
   DepCarry C;
   dep_reset(C);
-  if (B2M_DEP_WSORT) {
+  if (B2M_DEP_WSORT && SET == 0) {
     // Windows of 4 rows (128 particles): loaded together, sorted by cell in
     // the warp (bitonic network over (key << 8 | slot), 4 per lane), then
     // deposited row by row in cell order -- so particles that drifted out of
@@ -400,9 +401,31 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
       atomicMin(&fault->domain, fault_key(sp.species, sp.base + p));
       ok = false;
     }
-    dep_row<kDepRow, true>(C, g, qv, M.m, sw, sw + 8 * kDepRow, px, py, pz, ok, lane);
+    if (SET == 0)
+      dep_row<kDepRow, true>(C, g, qv, M.m, sw, sw + 8 * kDepRow, px, py, pz, ok, lane);
+    else
+      dep_row_p(C, g, qv, M.m, sw, sw + 8 * kDepRow, kDepRow, px, py, pz, ok, lane);
   }
-  dep_finish(C, g, M.m, lane);
+  if (SET == 0) dep_finish(C, g, M.m, lane);
+  else if (C.key >= 0) dep_flush_p(C.d0, C.d1, C.ci, C.cj, C.ck, g, M.m, lane);
+}
+
+template <int SET>
+void launch_dmma(const DevGrid& g, const SpeciesLaunch& sp, double qv, const MomentPtrs& M,
+                 FaultWord* fault, cudaStream_t st) {
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_dmma_kernel<SET>, kDmmaThreads, 0);
+    return b > 0 ? b : 1;
+  }();
+  const unsigned long long warps =
+      static_cast<unsigned long long>(device_sms()) * per_sm * (kDmmaThreads / 32);
+  unsigned long long span = (sp.n + warps - 1) / warps;
+  span = (span + 31) / 32 * 32;
+  const unsigned long long used = (sp.n + span - 1) / span;
+  const int blocks = static_cast<int>((used + kDmmaThreads / 32 - 1) / (kDmmaThreads / 32));
+  deposit_dmma_kernel<SET><<<blocks, kDmmaThreads, 0, st>>>(g, sp, qv, M, span, fault);
+  note_launch();
 }
 
 template <int SET, bool EXACT>
@@ -437,24 +460,13 @@ void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double
   if (exact) {
     launch_group<0, true>(g, sp, qv, M, fault, st);
   } else if (B2M_DEP_DMMA) {
-    static const int per_sm = [] {
-      int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_dmma_kernel, kDmmaThreads, 0);
-      return b > 0 ? b : 1;
-    }();
-    const unsigned long long warps =
-        static_cast<unsigned long long>(device_sms()) * per_sm * (kDmmaThreads / 32);
-    unsigned long long span = (sp.n + warps - 1) / warps;
-    span = (span + 31) / 32 * 32;
-    const unsigned long long used = (sp.n + span - 1) / span;
-    const int blocks = static_cast<int>((used + kDmmaThreads / 32 - 1) / (kDmmaThreads / 32));
-    deposit_dmma_kernel<<<blocks, kDmmaThreads, 0, st>>>(g, sp, qv, M, span, fault);
-    note_launch();
+    launch_dmma<0>(g, sp, qv, M, fault, st);
   } else {
     launch_group<0, false>(g, sp, qv, M, fault, st);
   }
   if (pressure) {
     if (exact) launch_group<1, true>(g, sp, qv, M, fault, st);
+    else if (B2M_DEP_DMMA) launch_dmma<1>(g, sp, qv, M, fault, st);
     else launch_group<1, false>(g, sp, qv, M, fault, st);
   }
 }

@@ -411,21 +411,22 @@ def test_fused_full_c2_vs_separate(gpu):
     b_.close()
 
 
-def _fast_store_deposit(p, grid, q):
+def _fast_store_deposit(p, grid, q, pressure=False):
     g = Grid.make(*grid)
     st = DeviceStore(g, [len(p[0])], "fast")
     st.upload_field(gem.gem_field(g))
     st.upload(0, p)
-    st.moments_zero(False)
+    st.moments_zero(pressure)
     st.deposit(0, q)
-    m = MomentMesh.make(g, False)
+    m = MomentMesh.make(g, pressure)
     st.moments_download(m)
     st.close()
     return m
 
 
+@pytest.mark.parametrize("pressure", [False, True])
 @pytest.mark.parametrize("order", ["random", "sorted", "sorted_jittered", "one_cell"])
-def test_fast_dmma_deposit_paths_vs_oracle(gpu, order):
+def test_fast_dmma_deposit_paths_vs_oracle(gpu, order, pressure):
     """The FAST rho + J kernel (deposit_dmma_kernel) on every path: rows in
     one cell (the carried cell across rows), runs across rows, groups taken
     by the extra DMMA passes, strays by direct atomics (random order), one
@@ -446,9 +447,9 @@ def test_fast_dmma_deposit_paths_vs_oracle(gpu, order):
             for a, b in rng.integers(0, n, size=(n // 10, 2)):
                 perm[a], perm[b] = perm[b], perm[a]
         p = [np.ascontiguousarray(a[perm]) for a in p]
-    m = _fast_store_deposit(p, grid, 0.003)
-    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.003, False),
-                         what=f"fast {order}")
+    m = _fast_store_deposit(p, grid, 0.003, pressure)
+    assert_moments_close(m.arrays, oracle.port_deposit_moments(p, grid, 0.003, pressure),
+                         what=f"fast {order} pressure={pressure}")
 
 
 def test_fast_dmma_deposit_domain_error(gpu):

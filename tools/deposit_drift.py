@@ -2,7 +2,8 @@
 context), the separate deposit and the fused mover+deposit, with the state's
 disorder: the fraction of particles whose cell differs from the cell of the
 particle before them in memory order, and of rows of 32 in one cell.
-FIELD=gem: E = 0 (the reference's init_gem field); default gem+E (bench)."""
+FIELD=gem: E = 0 (the reference's init_gem field); default gem+E (bench).
+PRESSURE=1: rho, J and the pressure tensor."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -37,7 +38,8 @@ def disorder():
     return ch / n, rows / nrows
 
 
-st.moments_zero(False)   # warm-up: the first deposit call sets the kernel up
+PRESSURE = os.environ.get("PRESSURE") == "1"
+st.moments_zero(PRESSURE)   # warm-up: the first deposit call sets the kernel up
 for s, b in enumerate(batches): st.deposit(s, b.q_per_particle)
 st.sync()
 done = 0
@@ -46,7 +48,7 @@ for target in (0, 1, 4, 8, 16, 32):
         st.move_all(mps); done += 1
     st.sync()
     chg, pure = disorder()
-    st.moments_zero(False)
+    st.moments_zero(PRESSURE)
     st.record(2)
     for s, b in enumerate(batches): st.deposit(s, b.q_per_particle)
     st.record(3)
