@@ -1,6 +1,6 @@
 """A device-resident PIC cycle at C2 on one B200, the reference's cycle order
 (runtime.cpp:218-262): field phase stand-in (field_phase_stub, 100 passes =
-the reference default cfg.field_passes) -> mover (FAST) -> moments (rho+J),
+the reference default cfg.field_passes) -> mover (FAST) -> moments (rho+J, + the pressure tensor by default),
 with a cell sort every --resort cycles.  Prints per-phase device times."""
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,6 +12,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cycles", type=int, default=16)
 ap.add_argument("--passes", type=int, default=100)
 ap.add_argument("--resort", type=int, default=8)
+ap.add_argument("--pressure", type=int, default=1,
+                help="deposit the pressure tensor too (the reference Simulation default, sim_config.hpp:46)")
 a = ap.parse_args()
 grid = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
 batches = gem.init_gem_species(grid, 216, pinned=True)
@@ -22,7 +24,7 @@ for s, b in enumerate(batches):
     st.upload(s, b.span())
 n = sum(b.count() for b in batches)
 phases = {"sort": 0.0, "field_stub": 0.0, "mover": 0.0, "moments": 0.0}
-st.moments_zero(False)
+st.moments_zero(bool(a.pressure))
 for c in range(a.cycles + 1):
     times = {}
     st.record(0)
@@ -34,7 +36,7 @@ for c in range(a.cycles + 1):
     st.record(2)
     st.move_all(mps)
     st.record(3)
-    st.moments_zero(False)
+    st.moments_zero(bool(a.pressure))
     for s, b in enumerate(batches):
         st.deposit(s, b.q_per_particle)
     st.record(4)
@@ -44,6 +46,6 @@ for c in range(a.cycles + 1):
     for k, (i, j) in zip(phases, [(0, 1), (1, 2), (2, 3), (3, 4)]):
         phases[k] += st.elapsed_ms(i, j) / a.cycles
 total = sum(phases.values())
-print(json.dumps({"config": "C2 61M particles, FAST, field_passes=%d, sort every %d cycles"
-                  % (a.passes, a.resort), "ms_per_cycle": total,
+print(json.dumps({"config": "C2 61M particles, FAST, field_passes=%d, sort every %d cycles, "
+                  "pressure %d" % (a.passes, a.resort, a.pressure), "ms_per_cycle": total,
                   "phases_ms": phases, "mover_mpa_s": n / (phases["mover"] * 1e-3) / 1e6}))
