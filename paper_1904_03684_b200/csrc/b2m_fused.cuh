@@ -346,6 +346,114 @@ __device__ __forceinline__ void dep_row_p(DepCarry& C, const G& g, double qv, do
   __syncwarp();
 }
 
+// ---- rho, J and the pressure tensor in one pass over the particles -------
+// dep_row's set-0 machinery and dep_row_p's set-1 passes on ONE staging of
+// the row (locate, weights, groups computed once): the carried cell keeps both
+// accumulators (C.d0/d1 for rho and J, P.d0/d1 for the pressure), every other
+// group of >= 2 takes a set-0 pass (columns 4-7) and a set-1 pass into a
+// temporary, strays add their 32 + 48 terms with direct atomics.
+template <class G>
+__device__ __forceinline__ void dep_row_all(DepCarry& C, DepCarry& P, const G& g, double qv,
+                                            double* const* mom, double* sw, const double* mrow,
+                                            double px, double py, double pz, bool ok, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int MS = kDepRow;
+  const double sx = px * g.rdx, sy = py * g.rdy, sz = pz * g.rdz;
+  int i = max(min(__double2int_rz(sx), g.nx - 1), 0), j = max(min(__double2int_rz(sy), g.ny - 1), 0),
+      k = max(min(__double2int_rz(sz), g.nz - 1), 0);
+  const double fx = fmin(sx - static_cast<double>(i), 1.0);
+  const double fy = fmin(sy - static_cast<double>(j), 1.0);
+  const double fz = fmin(sz - static_cast<double>(k), 1.0);
+  const double qw = ok ? qv : 0.0, ow = ok ? 1.0 : 0.0;
+  const double wx0 = qw * (1.0 - fx), wx1 = qw * fx;
+  const double wxy[4] = {wx0 * (1.0 - fy), wx1 * (1.0 - fy), wx0 * fy, wx1 * fy};
+  const double wz[2] = {ow * (1.0 - fz), ow * fz};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) sw[c * kDepRow + lane] = wxy[c & 3] * wz[c >> 2];
+  const long long key =
+      ok ? i + static_cast<long long>(g.nx) * (j + static_cast<long long>(g.ny) * k) : -1;
+  const unsigned okm = __ballot_sync(FULL, ok);
+  __syncwarp();
+  if (okm == 0) return;
+  const unsigned grp = __match_any_sync(FULL, key);
+  const unsigned score = ok ? (static_cast<unsigned>(__popc(grp)) << 6) |
+                                  (((grp >> 31) & 1u) << 5) | static_cast<unsigned>(lane)
+                            : 0u;
+  const unsigned best = __reduce_max_sync(FULL, score);
+  const int bl = best & 31;
+  const int ncar = __popc(__ballot_sync(FULL, ok && key == C.key));
+  if (ncar < static_cast<int>(best >> 6)) {
+    if (C.key >= 0) {
+      dep_flush_half(C.d0, C.d1, 0, C.ci, C.cj, C.ck, g, mom, lane);
+      dep_flush_p(P.d0, P.d1, C.ci, C.cj, C.ck, g, mom, lane);
+    }
+    C.key = __shfl_sync(FULL, key, bl);
+    C.ci = __shfl_sync(FULL, i, bl);
+    C.cj = __shfl_sync(FULL, j, bl);
+    C.ck = __shfl_sync(FULL, k, bl);
+  }
+  const unsigned carry = __ballot_sync(FULL, ok && key == C.key);
+  unsigned rest = okm & ~carry;
+  unsigned g1 = 0u;
+  int gi = 0, gj = 0, gk = 0;
+  if (rest) {
+    const unsigned s2 = ((rest >> lane) & 1u)
+                            ? (static_cast<unsigned>(__popc(grp)) << 6) | static_cast<unsigned>(lane)
+                            : 0u;
+    const int leader = __reduce_max_sync(FULL, s2) & 31;
+    g1 = __shfl_sync(FULL, grp, leader);
+    gi = __shfl_sync(FULL, i, leader);
+    gj = __shfl_sync(FULL, j, leader);
+    gk = __shfl_sync(FULL, k, leader);
+    rest &= ~g1;
+  }
+  dep_pass<MS, true>(C, sw, mrow, carry, g1, lane);
+  dep_pass_p(P.d0, P.d1, sw, mrow, MS, carry, lane);
+  if (g1) {
+    dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
+    double e0 = 0.0, e1 = 0.0;
+    dep_pass_p(e0, e1, sw, mrow, MS, g1, lane);
+    dep_flush_p(e0, e1, gi, gj, gk, g, mom, lane);
+  }
+#pragma unroll 1
+  for (int x = 0; x < B2M_DEP_PASSES && rest; ++x) {
+    const unsigned s2 = ((rest >> lane) & 1u)
+                            ? (static_cast<unsigned>(__popc(grp & rest)) << 6) |
+                                  static_cast<unsigned>(lane)
+                            : 0u;
+    const unsigned b2 = __reduce_max_sync(FULL, s2);
+    if ((b2 >> 6) < 2) break;
+    const int leader = b2 & 31;
+    const unsigned gm = __shfl_sync(FULL, grp, leader);
+    gi = __shfl_sync(FULL, i, leader);
+    gj = __shfl_sync(FULL, j, leader);
+    gk = __shfl_sync(FULL, k, leader);
+    rest &= ~gm;
+    dep_pass<MS, true>(C, sw, mrow, 0u, gm, lane);
+    dep_flush_half(C.d0, C.d1, 1, gi, gj, gk, g, mom, lane);
+    double e0 = 0.0, e1 = 0.0;
+    dep_pass_p(e0, e1, sw, mrow, MS, gm, lane);
+    dep_flush_p(e0, e1, gi, gj, gk, g, mom, lane);
+  }
+  if ((rest >> lane) & 1u) {
+    const double u = mrow[lane], v = mrow[MS + lane], w = mrow[2 * MS + lane];
+    const double m10[10] = {1.0, u, v, w, u * u, u * v, u * w, v * v, v * w, w * w};
+    const int i1 = i + 1 == g.nx ? 0 : i + 1, j1 = j + 1 == g.ny ? 0 : j + 1,
+              k1 = k + 1 == g.nz ? 0 : k + 1;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double wq = wxy[c & 3] * wz[c >> 2];
+      const long long node =
+          ((c & 1) ? i1 : i) +
+          static_cast<long long>(g.nx) *
+              (((c & 2) ? j1 : j) + static_cast<long long>(g.ny) * ((c & 4) ? k1 : k));
+#pragma unroll
+      for (int m = 0; m < 10; ++m) atomicAdd(mom[m] + node, wq * m10[m]);
+    }
+  }
+  __syncwarp();
+}
+
 template <class G>
 __device__ __forceinline__ void dep_finish(DepCarry& C, const G& g, double* const* mom,
                                            int lane) {

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kGroupThreads, 3)
 // kernel.
 constexpr int kDmmaThreads = 128;
 template <int SET>
-__global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
+__global__ void __launch_bounds__(kDmmaThreads, SET == 2 ? B2M_DMMA_MINB - 1 : B2M_DMMA_MINB)
     deposit_dmma_kernel(const __grid_constant__ DevGrid g, const __grid_constant__ SpeciesLaunch sp,
                         double qv, const __grid_constant__ MomentPtrs M,
                         unsigned long long span, FaultWord* fault) {
@@ -286,8 +286,9 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
   const unsigned long long lb = wid * span;
   if (lb >= sp.n) return;
   const unsigned long long le = lb + span < sp.n ? lb + span : sp.n;
-  DepCarry C;
+  DepCarry C, Pc;  // Pc: the pressure accumulator of the carried cell (SET 2)
   dep_reset(C);
+  dep_reset(Pc);
   if (B2M_DEP_WSORT && SET == 0) {
     // Windows of 4 rows (128 particles): loaded together, sorted by cell in
     // the warp (bitonic network over (key << 8 | slot), 4 per lane), then
@@ -403,11 +404,17 @@ __global__ void __launch_bounds__(kDmmaThreads, B2M_DMMA_MINB)
     }
     if (SET == 0)
       dep_row<kDepRow, true>(C, g, qv, M.m, sw, sw + 8 * kDepRow, px, py, pz, ok, lane);
-    else
+    else if (SET == 1)
       dep_row_p(C, g, qv, M.m, sw, sw + 8 * kDepRow, kDepRow, px, py, pz, ok, lane);
+    else
+      dep_row_all(C, Pc, g, qv, M.m, sw, sw + 8 * kDepRow, px, py, pz, ok, lane);
   }
-  if (SET == 0) dep_finish(C, g, M.m, lane);
-  else if (C.key >= 0) dep_flush_p(C.d0, C.d1, C.ci, C.cj, C.ck, g, M.m, lane);
+  if (SET == 0) {
+    dep_finish(C, g, M.m, lane);
+  } else if (C.key >= 0) {
+    if (SET == 2) dep_flush_half(C.d0, C.d1, 0, C.ci, C.cj, C.ck, g, M.m, lane);
+    dep_flush_p(SET == 2 ? Pc.d0 : C.d0, SET == 2 ? Pc.d1 : C.d1, C.ci, C.cj, C.ck, g, M.m, lane);
+  }
 }
 
 template <int SET>
@@ -457,16 +464,17 @@ void launch_deposit(const DevGrid& g, const SpeciesLaunch& sp, double qv, double
   if (sp.n == 0) return;
   MomentPtrs M{};
   for (int m = 0; m < (pressure ? 10 : 4); ++m) M.m[m] = mesh[m];
-  if (exact) {
-    launch_group<0, true>(g, sp, qv, M, fault, st);
-  } else if (B2M_DEP_DMMA) {
-    launch_dmma<0>(g, sp, qv, M, fault, st);
-  } else {
-    launch_group<0, false>(g, sp, qv, M, fault, st);
+  if (!exact && B2M_DEP_DMMA) {
+    // FAST: one pass for rho + J, or rho + J + pressure (SET 2: the particles
+    // read once, locate / weights / groups shared)
+    if (pressure) launch_dmma<2>(g, sp, qv, M, fault, st);
+    else launch_dmma<0>(g, sp, qv, M, fault, st);
+    return;
   }
+  if (exact) launch_group<0, true>(g, sp, qv, M, fault, st);
+  else launch_group<0, false>(g, sp, qv, M, fault, st);
   if (pressure) {
     if (exact) launch_group<1, true>(g, sp, qv, M, fault, st);
-    else if (B2M_DEP_DMMA) launch_dmma<1>(g, sp, qv, M, fault, st);
     else launch_group<1, false>(g, sp, qv, M, fault, st);
   }
 }
