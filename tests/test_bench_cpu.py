@@ -78,3 +78,17 @@ def test_reference_arm_line(monkeypatch, capsys):
     assert line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"] == {"value": 80.0, "unit": "MPA/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def test_one_rank_world_path_on_request(monkeypatch):
+    """B2M_BENCH_WORLD=1 under a one-rank torchrun runs the N > 1 code path
+    (the slab world over a one-rank NCCL communicator); without it, N = 1 is
+    the plain single-GPU path."""
+    called = {}
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setattr(bench, "run_world", lambda a: (called.__setitem__("path", "world"), 0)[1])
+    monkeypatch.setattr(bench, "run_ours", lambda a: (called.__setitem__("path", "ours"), 0)[1])
+    monkeypatch.delenv("B2M_BENCH_WORLD", raising=False)
+    assert bench.main([]) == 0 and called["path"] == "ours"
+    monkeypatch.setenv("B2M_BENCH_WORLD", "1")
+    assert bench.main([]) == 0 and called["path"] == "world"
