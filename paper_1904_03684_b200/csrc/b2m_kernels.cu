@@ -14,6 +14,7 @@
 //                         runtime.cpp:64-76)
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 #include <cudaTypedefs.h>
@@ -72,6 +73,13 @@ constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
 #ifndef B2M_SORT_ZFAST
 #define B2M_SORT_ZFAST 1       // cell sort order: 1 = z fastest (column-contiguous), 0 = x fastest
 #endif
+#ifndef B2M_2D_RDISPATCH
+#define B2M_2D_RDISPATCH 1     // pc_iterations dispatched once per tile (not per particle)
+#endif
+#ifndef B2M_2D_UNROLL
+#define B2M_2D_UNROLL 2        // unroll of the column kernel's particle loop (2: 1.15 -> 1.12 ms; 4: 1.19)
+#endif
+constexpr int kUnroll2D = B2M_2D_UNROLL;
 #ifndef B2M_COL_PREFETCH
 #define B2M_COL_PREFETCH 0     // 1: L1 prefetch of the next particle's column (measured slower: 1.31 vs 1.16 ms)
 #endif
@@ -213,6 +221,20 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           after(j, bad2 & 1u, buf[st][1][pa]);
           after(j + 1, bad2 >> 1, buf[st][1][pb]);
         }
+      } else if (B2M_2D_RDISPATCH && !B2M_COL_PREFETCH) {
+        // pc_iterations dispatched once per tile, the particle loop inside
+        auto run = [&](auto rounds_tag) {
+          constexpr int R = decltype(rounds_tag)::value;
+#pragma unroll (kUnroll2D)
+          for (int j = 0; j < P; ++j) {
+            const int p = lane + 32 * j;
+            double y1 = 0.0;
+            const unsigned bad = fast_particle_2d<WT, R>(F.fg, F.U, cols, buf[st], p, cnt, C, &y1);
+            after(j, bad, y1);
+          }
+        };
+        if (F.U.rounds == 3) run(std::integral_constant<int, 3>{});
+        else run(std::integral_constant<int, 0>{});
       } else {
 #pragma unroll 1
         for (int j = 0; j < P; ++j) {

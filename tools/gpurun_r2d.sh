@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests/test_moments_gpu.py -x -q 2>&1 | tail -2
-PRESSURE=1 python tools/deposit_drift.py | cut -c1-40
-python tools/cycle_c2.py --resort 4
+for lib in libb2m.so libb2m_4x3_rd1u1.so libb2m_4x3_rd1u2.so libb2m_4x3_rd1u4.so libb2m.so; do
+  echo "== $lib"; B2M_LIB=paper_1904_03684_b200/$lib python tools/one_launch.py 8 | tail -3
+done
