@@ -80,6 +80,10 @@ constexpr int kJUnroll = B2M_J_UNROLL;  // unroll of the per-lane particle loop
 #define B2M_2D_UNROLL 2        // unroll of the column kernel's particle loop (2: 1.15 -> 1.12 ms; 4: 1.19)
 #endif
 constexpr int kUnroll2D = B2M_2D_UNROLL;
+#ifndef B2M_3D_UNROLL
+#define B2M_3D_UNROLL 1        // unroll of the general FAST kernel's particle loop
+#endif
+constexpr int kUnroll3D = B2M_3D_UNROLL;
 #ifndef B2M_COL_PREFETCH
 #define B2M_COL_PREFETCH 0     // 1: L1 prefetch of the next particle's column (measured slower: 1.31 vs 1.16 ms)
 #endif
@@ -269,12 +273,12 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       fast_cell_reset(C);
       uint8_t* flags = S.flags[s];
       const double2* cells = sp.cells;
-#pragma unroll 1
+      auto run3 = [&](auto rounds_tag) {
+      constexpr int R = decltype(rounds_tag)::value;
+#pragma unroll (kUnroll3D)
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        const unsigned bad =
-            F.U.rounds == 3 ? fast_particle_v2<WT, 3>(F.fg, F.U, cells, buf[st], p, cnt, C)
-                            : fast_particle_v2<WT, 0>(F.fg, F.U, cells, buf[st], p, cnt, C);
+        const unsigned bad = fast_particle_v2<WT, R>(F.fg, F.U, cells, buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (DEP)
           dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
@@ -293,6 +297,10 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           n_next += flag == 2;
         }
       }
+      };
+      // pc_iterations dispatched once per tile
+      if (F.U.rounds == 3) run3(std::integral_constant<int, 3>{});
+      else run3(std::integral_constant<int, 0>{});
     } else {
       const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
