@@ -47,7 +47,14 @@ namespace b2m {
 // (2 * (36 r + q) mod 32 = 8 r + 2 q) -- rows of 32 would put every row on
 // the same banks (4-way conflicts).
 constexpr int kDepRow = 36;
-constexpr int kDepStage = 6 * kDepRow;  // fused mover: six staged weight factors per warp
+#ifndef B2M_DEP_STAGE_UVW
+#define B2M_DEP_STAGE_UVW 1  // fused mover: stage u, v, w too (conflict-free B rows), 96-particle tiles
+#endif
+// fused mover: six staged weight factors (+ u, v, w) per warp
+constexpr int kDepStage = (B2M_DEP_STAGE_UVW ? 9 : 6) * kDepRow;
+// fused mover tile width in rows of 32 (the staging has to fit beside the TMA
+// ring at 4 blocks per SM)
+constexpr int kDepPPT = B2M_DEP_STAGE_UVW ? 3 : 4;
 
 struct DepCarry {
   double d0, d1;   // DMMA accumulator: D[lane/4][2*(lane%4) + {0, 1}]

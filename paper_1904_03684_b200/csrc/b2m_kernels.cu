@@ -196,9 +196,20 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       auto after = [&](int j, unsigned bad, double y1) {
         const int p = lane + 32 * j;
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (DEP)
-          dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
-                      buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+        if (DEP) {
+          if (B2M_DEP_STAGE_UVW) {
+            // u, v, w into padded rows: the DMMA B fragments read them without
+            // the tile rows' 3-way bank conflicts
+            sw[6 * kDepRow + lane] = buf[st][3][p];
+            sw[7 * kDepRow + lane] = buf[st][4][p];
+            sw[8 * kDepRow + lane] = buf[st][5][p];
+            dep_row<kDepRow>(dc, F.fg, sp.qv, F.mom, sw, sw + 6 * kDepRow, buf[st][0][p],
+                             buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+          } else {
+            dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
+                        buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+          }
+        }
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
@@ -229,7 +240,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
         // pc_iterations dispatched once per tile, the particle loop inside
         auto run = [&](auto rounds_tag) {
           constexpr int R = decltype(rounds_tag)::value;
-#pragma unroll (kUnroll2D)
+#pragma unroll (DEP ? 1 : kUnroll2D)
           for (int j = 0; j < P; ++j) {
             const int p = lane + 32 * j;
             double y1 = 0.0;
@@ -280,9 +291,20 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
         const int p = lane + 32 * j;
         const unsigned bad = fast_particle_v2<WT, R>(F.fg, F.U, cells, buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (DEP)
-          dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
-                      buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+        if (DEP) {
+          if (B2M_DEP_STAGE_UVW) {
+            // u, v, w into padded rows: the DMMA B fragments read them without
+            // the tile rows' 3-way bank conflicts
+            sw[6 * kDepRow + lane] = buf[st][3][p];
+            sw[7 * kDepRow + lane] = buf[st][4][p];
+            sw[8 * kDepRow + lane] = buf[st][5][p];
+            dep_row<kDepRow>(dc, F.fg, sp.qv, F.mom, sw, sw + 6 * kDepRow, buf[st][0][p],
+                             buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+          } else {
+            dep_row<WT>(dc, F.fg, sp.qv, F.mom, sw, &buf[st][3][32 * j], buf[st][0][p],
+                        buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
+          }
+        }
         if (flags && p < cnt) {
           int flag = 0;
           if (!bad) {
@@ -670,7 +692,7 @@ template <bool STRICT, int DIM, bool DEP = false>
 bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans, FaultWord* fault,
                        cudaStream_t st, const SlabLaunch* sl, uint8_t* const* flags,
                        unsigned long long* const* tcnt) {
-  constexpr int P = B2M_FAST_PPT;
+  constexpr int P = DEP ? kDepPPT : B2M_FAST_PPT;
   constexpr int WT = 32 * P;
   constexpr int smem = (kWarpThreads / 32) * (kWarpStages * (6 * WT * 8 + 8) +
                                               (DEP ? kDepStage * 8 : 0));
