@@ -22,7 +22,7 @@ B2M_MODE=strict $NCU -k "regex:warp_tile_kernel<(.int.)?4, (.bool.)?(1|true), (.
     --launch-skip 2 --launch-count 1 -f -o gpurun_out/prof_strict python tools/one_launch.py 3 \
     > gpurun_out/ncu_strict.log 2>&1
 echo "strict rc=$?"
-$NCU -k "regex:warp_tile_kernel<(.int.)?4, (.bool.)?(0|false), (.int.)?2, (.bool.)?(1|true)>" \
+$NCU -k "regex:warp_tile_kernel<(.int.)?[0-9], (.bool.)?(0|false), (.int.)?2, (.bool.)?(1|true)>" \
     --launch-skip 1 --launch-count 1 -f -o gpurun_out/prof_fused python tools/fused_time.py 2 \
     > gpurun_out/ncu_fused.log 2>&1
 echo "fused rc=$?"
