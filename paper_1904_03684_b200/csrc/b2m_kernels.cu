@@ -84,6 +84,9 @@ constexpr int kUnroll2D = B2M_2D_UNROLL;
 #define B2M_3D_UNROLL 1        // unroll of the general FAST kernel's particle loop
 #endif
 constexpr int kUnroll3D = B2M_3D_UNROLL;
+#ifndef B2M_TILE_PREFETCH
+#define B2M_TILE_PREFETCH 0    // 1: L1 prefetch of the next tile's first-row columns
+#endif
 #ifndef B2M_COL_PREFETCH
 #define B2M_COL_PREFETCH 0     // 1: L1 prefetch of the next particle's column (measured slower: 1.31 vs 1.16 ms)
 #endif
@@ -243,6 +246,18 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
 #pragma unroll (DEP ? 1 : kUnroll2D)
           for (int j = 0; j < P; ++j) {
             const int p = lane + 32 * j;
+            if (B2M_TILE_PREFETCH && j == P - 2) {
+              // the next tile's first-row columns into L1 once its load landed
+              const int nst = st + 1 == kWarpStages ? 0 : st + 1;
+              const uint32_t nph = nst == 0 ? phase ^ 1u : phase;
+              const unsigned long long nt = tile + GW;
+              if (nt < total_tiles && mbar_test(&bar[nst], nph)) {
+                int s2 = s;
+                advance_span(s2, nt);
+                col_prefetch(F.fg, reinterpret_cast<const double*>(S.sp[s2].cells), C,
+                             buf[nst][0][lane], buf[nst][1][lane]);
+              }
+            }
             double y1 = 0.0;
             const unsigned bad = fast_particle_2d<WT, R>(F.fg, F.U, cols, buf[st], p, cnt, C, &y1);
             after(j, bad, y1);
