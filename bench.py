@@ -137,6 +137,25 @@ def measured_traffic(kernel_tag: str):
     return None
 
 
+def measured_ncu(kernel_tag: str):
+    """FP64-pipe / issue / occupancy figures of the same ncu capture
+    (profiles/r02_c2_bench.json) for the kernel whose name contains
+    `kernel_tag` -- the regime the roofline fraction sits in."""
+    if not os.path.exists(PROFILE):
+        return None
+    with open(PROFILE) as f:
+        d = json.load(f)
+    keys = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "registers": "launch__registers_per_thread",
+            "ncu_ms": "gpu__time_duration.sum"}
+    for k in d.get("kernels", []):
+        if kernel_tag in k["kernel"]:
+            return {name: float(k[m][0]) for name, m in keys.items() if m in k}
+    return None
+
+
 def host_info():
     model = "unknown"
     try:
@@ -613,6 +632,7 @@ def run_ours(args):
                      "peak": peak, "unit": "GB/s",
                      "frac": alg_bytes / (kernel_ms * 1e-3) / 1e9 / peak,
                      "traffic": measured_traffic("<4, 0, 2, 0>") if args.mode == "fast" else None,
+                     "ncu": measured_ncu("<4, 0, 2, 0>") if args.mode == "fast" else None,
                      "traffic_source": "ncu --set full, profiles/r02_c2_bench.json",
                      "kernel": kname, "kernel_ms": kernel_ms,
                      "bytes_per_launch": alg_bytes, "bytes_per_particle": BYTES_PER_PARTICLE,
