@@ -309,7 +309,11 @@ b2m_status b2m_world_id(void* id);
 b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world);
 b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
 /* Replicate the root rank's device field on every rank (ncclBroadcast of E
- * and B): runtime.cpp:143 gives every worker the whole mesh. */
+ * and B): runtime.cpp:143 gives every worker the whole mesh.  A header with
+ * the root's z-invariance flag and node plane 0 go first; a z-invariant field
+ * is rebuilt from plane 0 on the other ranks (bitwise the root's field), any
+ * other field is sent whole (B2M_BCAST_ZINV=0: always whole).  One host read
+ * of the header per call. */
 b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root);
 /* Sum every rank's moment mesh (b2m_moments_zero + b2m_deposit per rank) into
  * every rank's mesh, in place, in the reference's order: zero, then rank

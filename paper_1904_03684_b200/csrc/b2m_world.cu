@@ -61,6 +61,23 @@ const NcclApi& nccl() {
 namespace b2m {
 namespace {
 
+// Field broadcast of a z-invariant field: header = the root's z-invariance
+// flag (0: every node plane equals plane 0 bit for bit), then plane 0 of E
+// and of B; a non-root rank that receives flag 0 rebuilds every plane from
+// plane 0 -- bitwise the root's field, for 1/(nz+1) of the broadcast bytes.
+__global__ void bcast_header_kernel(const int* zvar, double* stage) {
+  stage[0] = static_cast<double>(*zvar);
+}
+
+__global__ void expand_planes_kernel(long long plane3, long long total3, double* __restrict__ E,
+                                     double* __restrict__ B) {
+  for (long long t = plane3 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+       t < total3; t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    E[t] = E[t % plane3];
+    B[t] = B[t % plane3];
+  }
+}
+
 // The reference's moment reduction (runtime.cpp:256-262): moments_.zero(),
 // then moments_.add(worker w) for w = 0..N-1 -- element by element, in rank
 // order, separately rounded -- from the gathered [world][n] meshes.
@@ -291,6 +308,15 @@ b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world) {
   }
   for (auto& c : cap) c *= 2;  // from prev + from next
   if ((st = world_alloc(ctx, cap)) != B2M_OK) return st;
+  {  // the compressed field broadcast's staging (b2m_world_broadcast_field)
+    const uint64_t plane = static_cast<uint64_t>(ctx->grid.nx + 1) * (ctx->grid.ny + 1);
+    if ((st = dalloc(ctx, &ctx->w.bstage, 1 + 6 * plane, "field broadcast staging")) != B2M_OK)
+      return st;
+    if (cudaMallocHost(&ctx->w.bflag_h, sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(B2M_ALLOC_ERROR, "pinned broadcast header");
+    }
+  }
   if (ctx->mom[0]) {  // a moment mesh exists: its gather buffer now
     const uint64_t nodes = static_cast<uint64_t>(ctx->grid.nx) * ctx->grid.ny * ctx->grid.nz;
     return world_reserve_moments(ctx, static_cast<uint64_t>(ctx->mom_arrays) * nodes);
@@ -309,12 +335,49 @@ b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
     return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no field uploaded on the root");
   if (ctx->w.comm) {
     const size_t n = 3 * ctx->n_nodes;
-    B2M_NCCL(ctx, nccl().GroupStart());
-    B2M_NCCL(ctx, nccl().Broadcast(ctx->dE, ctx->dE, n, ncclFloat64, root, ctx->w.comm,
-                                   ctx->stream));
-    B2M_NCCL(ctx, nccl().Broadcast(ctx->dB, ctx->dB, n, ncclFloat64, root, ctx->w.comm,
-                                   ctx->stream));
-    B2M_NCCL(ctx, nccl().GroupEnd());
+    const size_t plane3 = 3 * static_cast<size_t>(ctx->grid.nx + 1) * (ctx->grid.ny + 1);
+    bool full = true;
+    const char* zb = std::getenv("B2M_BCAST_ZINV");
+    if (ctx->zvar && ctx->w.bstage && !(zb && zb[0] == '0')) {
+      // header + plane 0, then the whole field only if it is not z-invariant
+      // (one host read of the header on every rank)
+      double* stg = ctx->w.bstage;
+      if (ctx->sl.rank == root) {
+        launch_zinv_check(ctx->grid.nx, ctx->grid.ny, ctx->grid.nz, ctx->dE, ctx->dB, ctx->zvar,
+                          ctx->stream);
+        bcast_header_kernel<<<1, 1, 0, ctx->stream>>>(ctx->zvar, stg);
+        note_launch();
+        B2M_CUDA(ctx, cudaMemcpyAsync(stg + 1, ctx->dE, plane3 * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        B2M_CUDA(ctx, cudaMemcpyAsync(stg + 1 + plane3, ctx->dB, plane3 * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+      B2M_NCCL(ctx, nccl().Broadcast(stg, stg, 1 + 2 * plane3, ncclFloat64, root, ctx->w.comm,
+                                     ctx->stream));
+      B2M_CUDA(ctx, cudaMemcpyAsync(ctx->w.bflag_h, stg, sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+      B2M_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      full = *ctx->w.bflag_h != 0.0;
+      if (!full && ctx->sl.rank != root) {
+        B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dE, stg + 1, plane3 * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        B2M_CUDA(ctx, cudaMemcpyAsync(ctx->dB, stg + 1 + plane3, plane3 * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        const long long blocks = std::min<long long>((static_cast<long long>(n) + 255) / 256, 4096);
+        expand_planes_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+            static_cast<long long>(plane3), static_cast<long long>(n), ctx->dE, ctx->dB);
+        note_launch();
+        B2M_CUDA(ctx, cudaGetLastError());
+      }
+    }
+    if (full) {
+      B2M_NCCL(ctx, nccl().GroupStart());
+      B2M_NCCL(ctx, nccl().Broadcast(ctx->dE, ctx->dE, n, ncclFloat64, root, ctx->w.comm,
+                                     ctx->stream));
+      B2M_NCCL(ctx, nccl().Broadcast(ctx->dB, ctx->dB, n, ncclFloat64, root, ctx->w.comm,
+                                     ctx->stream));
+      B2M_NCCL(ctx, nccl().GroupEnd());
+    }
   }
   ++ctx->field_gen;  // a new field: FAST tables and the STRICT node table rebuild
   ctx->field_ready = true;

@@ -54,6 +54,23 @@ def main():
     st.upload_field(gem.gem_field(grid))
     for s, p in enumerate(p6s):
         st.upload(s, p)
+    if mode in ("bcast_zinv", "bcast_zvar"):
+        # rank 0's field (z-invariant, or varying in z) broadcast over fields
+        # the other ranks scrambled: every rank must end with rank 0's bits
+        f = gem.gem_bench_field(grid, z_varying=(mode == "bcast_zvar"))
+        if rank != 0:
+            f.E[:] = -7.0
+            f.B[:] = 3.0
+        st.upload_field(f)
+        sw = NativeSlabWorld(grid, st, rank, world, dist)
+        sw.broadcast_field(0)
+        from paper_1904_03684_b200.mover import FieldMesh
+        out = FieldMesh(grid, np.zeros_like(f.E.ravel()), np.zeros_like(f.B.ravel()))
+        st.download_field(out)
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), E=out.E.ravel(), B=out.B.ravel())
+        st.close()
+        dist.destroy_process_group()
+        return
     sw = NativeSlabWorld(grid, st, rank, world, dist)
     sw.set_total()
     mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]

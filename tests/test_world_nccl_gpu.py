@@ -115,6 +115,27 @@ def test_native_world_over_fake_nccl_one_gpu(gpu, world):
     _check_world_vs_reference(world, d, logs)
 
 
+@pytest.mark.parametrize("mode", ["bcast_zinv", "bcast_zvar"])
+@pytest.mark.parametrize("compress", ["1", "0"])
+def test_field_broadcast_over_fake_nccl(gpu, mode, compress):
+    """b2m_world_broadcast_field at 3 ranks: a z-invariant root field goes
+    as plane 0 + a header and is rebuilt on the other ranks, a z-varying one
+    (or B2M_BCAST_ZINV=0) as the whole field -- either way every rank ends
+    with the root's field bit for bit."""
+    lib = fake_nccl_lib()
+    d, logs = _run(3, 0, mode, env={"B2M_NCCL_LIB": lib, "B2M_BCAST_ZINV": compress})
+    got = []
+    for r in range(3):
+        f = os.path.join(d, f"rank{r}.npz")
+        assert os.path.exists(f), "\n".join(logs)
+        got.append(np.load(f))
+    from paper_1904_03684_b200 import gem
+    want = gem.gem_bench_field(Grid.make(*GRID), z_varying=(mode == "bcast_zvar"))
+    for z in got:
+        np.testing.assert_array_equal(z["E"].view(np.uint64), want.E.ravel().view(np.uint64))
+        np.testing.assert_array_equal(z["B"].view(np.uint64), want.B.ravel().view(np.uint64))
+
+
 def test_native_world_over_fake_nccl_fault_on_one_rank(gpu):
     d, logs = _run(2, 1, "nan", env={"B2M_NCCL_LIB": fake_nccl_lib()})
     errs = [open(os.path.join(d, f"rank{r}.err")).read() if os.path.exists(
