@@ -1261,6 +1261,7 @@ static b2m_status migrate_compact(b2m_ctx* ctx, const int* species, const Specie
     c.tile0 = ctx->mig_tile0[static_cast<size_t>(s)];
     c.n_tiles = migrate_tiles(S.count);  // 0 for an empty species: zero totals
   }
+  C.sl = ctx->sl;
   launch_compact(C, ctx->scan_temp, ctx->scan_temp_bytes, ctx->mig_tcnt, ctx->mig_toff,
                  ctx->stream);
   B2M_CUDA(ctx, cudaMemcpyAsync(ctx->mig_totals_h, ctx->mig_totals,
@@ -1378,10 +1379,10 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
   L.n = old_n;
   L.species = s;
   if (S.migrate_pending) {
-    launch_fill(L, S.holes, holes, d_recs, n, S.flags, ctx->stream);
+    launch_fill(L, S.holes, holes, d_recs, n, ctx->sl, ctx->stream);
   } else if (n > 0) {
     // plain append: no holes
-    launch_fill(L, S.holes, 0, d_recs, n, S.flags, ctx->stream);
+    launch_fill(L, S.holes, 0, d_recs, n, ctx->sl, ctx->stream);
   }
   B2M_CUDA(ctx, cudaGetLastError());
   S.count = new_n;

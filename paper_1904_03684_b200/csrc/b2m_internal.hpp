@@ -127,6 +127,7 @@ struct CompactSpecies {
 };
 struct CompactSet {
   CompactSpecies s[kMaxCompactSpecies];
+  SlabLaunch sl;  // the owner scan's thresholds: leavers re-derived from the new y
   int n;
 };
 // scan of the shared tile counts, every species' totals, outbox + hole scatter
@@ -137,6 +138,6 @@ size_t scan_temp_bytes(uint64_t n_tiles);
 
 // Fill holes with incoming records, then append / compact the tail.
 void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
-                 const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st);
+                 const double* in_recs, uint64_t n_in, const SlabLaunch& sl, cudaStream_t st);
 
 }  // namespace b2m

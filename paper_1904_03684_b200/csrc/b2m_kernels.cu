@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
     const unsigned long long left = sp.n - off;
     const int cnt = left < static_cast<unsigned long long>(WT) ? static_cast<int>(left) : WT;
     mbar_wait(&bar[st], phase);
-    unsigned n_prev = 0, n_next = 0;  // this lane's leavers in the tile
+    unsigned n_prev = 0, n_next = 0;  // the warp's leavers in the tile (ballot totals)
     if (STRICT) {
       CellCache cc;
       cc.cell = -1;
@@ -172,18 +172,19 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                 ? strict_tile_thread_p1<WT, 3, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc)
                 : strict_tile_thread_p1<WT, 0, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (flags && p < cnt) {
+        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
+        // warp ballot; the compaction re-derives each leaver from its y
+        if (flags) {
           int flag = 0;
-          if (!bad) {
+          if (p < cnt && !bad) {
             flag = slab_flag(buf[st][1][p], sl);
             if (flag == 3) {
               atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
               flag = 0;
             }
           }
-          flags[off + p] = static_cast<uint8_t>(flag);
-          n_prev += flag == 1;
-          n_next += flag == 2;
+          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       }
     } else if (B2M_ABL_STREAM_ONLY) {
@@ -213,18 +214,19 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                         buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
           }
         }
-        if (flags && p < cnt) {
+        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
+        // warp ballot; the compaction re-derives each leaver from its y
+        if (flags) {
           int flag = 0;
-          if (!bad) {
+          if (p < cnt && !bad) {
             flag = slab_flag(y1, sl);
             if (flag == 3) {
               atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
               flag = 0;
             }
           }
-          flags[off + p] = static_cast<uint8_t>(flag);
-          n_prev += flag == 1;
-          n_next += flag == 2;
+          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       };
       if (B2M_2D_PAIR && (P % 2) == 0) {
@@ -320,18 +322,19 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                         buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
           }
         }
-        if (flags && p < cnt) {
+        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
+        // warp ballot; the compaction re-derives each leaver from its y
+        if (flags) {
           int flag = 0;
-          if (!bad) {
+          if (p < cnt && !bad) {
             flag = slab_flag(buf[st][1][p], sl);
             if (flag == 3) {
               atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
               flag = 0;
             }
           }
-          flags[off + p] = static_cast<uint8_t>(flag);
-          n_prev += flag == 1;
-          n_next += flag == 2;
+          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       }
       };
@@ -356,29 +359,27 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                 ? fast_tile_thread_p1<WT, 3>(F.fg, sp.cells, kc, buf[st], p, cnt, K, kcell)
                 : fast_tile_thread_p1<WT, 0>(F.fg, sp.cells, kc, buf[st], p, cnt, K, kcell);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        if (flags && p < cnt) {
+        if (flags) {
           // migration scan fused into the mover (partition_outgoing,
           // runtime.cpp:46-62): 0 stay, 1 prev, 2 next; a non-neighbour
           // destination records a CflViolation
           int flag = 0;
-          if (!bad) {
+          if (p < cnt && !bad) {
             flag = slab_flag(buf[st][1][p], sl);
             if (flag == 3) {
               atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
               flag = 0;
             }
           }
-          flags[off + p] = static_cast<uint8_t>(flag);
-          n_prev += flag == 1;
-          n_next += flag == 2;
+          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       }
     }
-    if (S.tcnt[s]) {  // per-tile leaver counts: the scan input of the compaction
-      const unsigned cp = __reduce_add_sync(0xffffffffu, n_prev);
-      const unsigned cn = __reduce_add_sync(0xffffffffu, n_next);
+    if (S.tcnt[s]) {  // per-tile leaver counts (warp totals): the compaction's scan input
       if (lane == 0)
-        S.tcnt[s][tile - S.tile_start[s]] = (static_cast<unsigned long long>(cn) << 32) | cp;
+        S.tcnt[s][tile - S.tile_start[s]] =
+            (static_cast<unsigned long long>(n_next) << 32) | n_prev;
     }
     fence_proxy_async();
     __syncwarp();
@@ -625,7 +626,7 @@ __global__ void fill_in_kernel(const __grid_constant__ SpeciesLaunch sp,
 __global__ void __launch_bounds__(1024)
     fill_tail_kernel(const __grid_constant__ SpeciesLaunch sp,
                      const unsigned long long* __restrict__ holes, unsigned long long n_in,
-                     const uint8_t* __restrict__ flags, unsigned long long new_n) {
+                     const __grid_constant__ SlabLaunch sl, unsigned long long new_n) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
@@ -633,7 +634,11 @@ __global__ void __launch_bounds__(1024)
   __syncthreads();
   for (unsigned long long base = new_n; base < sp.n; base += 1024) {
     const unsigned long long i = base + threadIdx.x;
-    const int keep = (i < sp.n && flags[i] == 0) ? 1 : 0;
+    // tail positions still hold their own moved particles (arrivals only
+    // fill holes below new_n): a leaver by the owner scan of its y
+    int f = i < sp.n ? slab_flag(sp.y[i], sl) : 1;
+    if (f == 3) f = 0;
+    const int keep = (i < sp.n && f == 0) ? 1 : 0;
     int rank, total;
     Scan(tmp).ExclusiveSum(keep, rank, total);
     if (keep) {
@@ -993,7 +998,10 @@ __global__ void __launch_bounds__(kTileParticles)
       const unsigned long long t = g0 + active[a];
       const CompactSpecies& c = C.s[compact_species_of(C, t)];
       const unsigned long long i = (t - c.tile0) * kTileParticles + threadIdx.x;
-      const int flag = i < c.sp.n ? c.flags[i] : 0;
+      // the mover's owner scan again, from the new y (bad particles were
+      // left in place, in this slab: 0; a CflViolation stays: 3 -> 0)
+      int flag = i < c.sp.n ? slab_flag(c.sp.y[i], C.sl) : 0;
+      if (flag == 3) flag = 0;
       const unsigned bp = __ballot_sync(~0u, flag == 1);
       const unsigned bn = __ballot_sync(~0u, flag == 2);
       __syncthreads();
@@ -1047,14 +1055,14 @@ void launch_compact(const CompactSet& C, void* temp, size_t temp_bytes,
 }
 
 void launch_fill(const SpeciesLaunch& sp, const unsigned long long* holes, uint64_t n_holes,
-                 const double* in_recs, uint64_t n_in, const uint8_t* flags, cudaStream_t st) {
+                 const double* in_recs, uint64_t n_in, const SlabLaunch& sl, cudaStream_t st) {
   if (n_in > 0) {
     fill_in_kernel<<<grid_for(n_in, 256), 256, 0, st>>>(sp, holes, n_holes, in_recs, n_in);
     note_launch();
   }
   if (n_in < n_holes) {
     const unsigned long long new_n = sp.n - n_holes + n_in;
-    fill_tail_kernel<<<1, 1024, 0, st>>>(sp, holes, n_in, flags, new_n);
+    fill_tail_kernel<<<1, 1024, 0, st>>>(sp, holes, n_in, sl, new_n);
     note_launch();
   }
 }
