@@ -333,7 +333,7 @@ b2m_status b2m_world_broadcast_field(b2m_ctx* ctx, int root) {
     return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no NCCL communicator (world > 1)");
   if (ctx->sl.rank == root && !ctx->field_ready)
     return fail(B2M_CONFIG_ERROR, "world_broadcast_field: no field uploaded on the root");
-  if (ctx->w.comm) {
+  if (ctx->w.comm && ctx->sl.world > 1) {  // (one rank: its field is already the root's)
     const size_t n = 3 * ctx->n_nodes;
     const size_t plane3 = 3 * static_cast<size_t>(ctx->grid.nx + 1) * (ctx->grid.ny + 1);
     bool full = true;
