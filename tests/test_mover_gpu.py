@@ -11,8 +11,8 @@ from paper_1904_03684_b200 import gem
 from paper_1904_03684_b200.engine import B200Engine, DeviceStore
 from paper_1904_03684_b200.errors import EngineFault, NumericalFault
 from paper_1904_03684_b200.mover import FieldMesh, Grid, MoverParams, move_batch
-from tests._util import (assert_bitwise, assert_within_contract, cells_of, digest, from_hex,
-                         random_field, random_particles, sort_keys_of, uniform_field)
+from tests._util import (assert_bitwise, assert_within_contract, cells_of, cramer_vbar, digest,
+                         from_hex, random_field, random_particles, sort_keys_of, uniform_field)
 
 pytestmark = pytest.mark.gpu
 
@@ -191,6 +191,61 @@ def test_uniform_field_pc_fixed_point(gpu, mode):
     assert_within_contract(a, b, grid, tol=1e-13)
     check(a, port_move(p0, E, B, grid, 0.1, -25.0, 1), grid, mode, "pc1")
     check(b, port_move(p0, E, B, grid, 0.1, -25.0, 3), grid, mode, "pc3")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_independent_cramer_oracle_uniform_fields(gpu, mode):
+    """The device mover against an independent solve (test_kernels.cpp:183-214,
+    test_acceptance.cpp:205-241): on uniform fields the implicit velocity is
+    the Cramer-rule solution of (I - beta[x B]) vbar = vn + beta E, so
+    x1 = wrap(x0 + vbar dt) and v1 = 2 vbar - v0 to 1e-14 absolute, the
+    reference's own bar, for qom in {1, -25}."""
+    grid = (8, 8, 8, 4.0, 4.0, 4.0)
+    rng = np.random.default_rng(23)
+    L = np.array(grid[3:])
+    for trial, qom in enumerate([1.0, -25.0, 1.0]):
+        E0, B0 = rng.standard_normal(3), rng.standard_normal(3)
+        E, B = uniform_field(grid, E0, B0)
+        p0 = random_particles(grid, 10000, 100 + trial)
+        dt = 0.1
+        got = gpu_move(p0, E, B, grid, dt, qom, 3, mode)
+        v0, x0 = np.stack(p0[3:], axis=1), np.stack(p0[:3], axis=1)
+        vbar = cramer_vbar(v0, np.broadcast_to(E0, v0.shape), np.broadcast_to(B0, v0.shape),
+                           qom * dt * 0.5)
+        x1 = x0 + vbar * dt
+        x1 = x1 - L * np.floor(x1 / L)
+        dx = np.abs(np.stack(got[:3], axis=1) - x1)
+        assert np.max(np.minimum(dx, L - dx)) <= 1e-14, (mode, qom)
+        assert np.max(np.abs(np.stack(got[3:], axis=1) - (2 * vbar - v0))) <= 1e-14, (mode, qom)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_gyration_and_exb_drift(gpu, mode):
+    """The reference's physics checks (test_kernels.cpp:365-403) through the
+    device mover: in a uniform B the speed is kept to 1e-13 over 100 steps;
+    in crossed E and B a particle from rest drifts at E/B to 1 % over one
+    gyration period."""
+    grid = (4, 4, 4, 8.0, 8.0, 8.0)
+    N = 32
+    dt = 2.0 * np.tan(np.pi / N)
+    E, B = uniform_field(grid, [0, 0, 0], [0, 0, 1])
+    p = [np.array([4.0]), np.array([4.0]), np.array([4.0]), np.array([0.2]), np.array([0.0]),
+         np.array([0.1])]
+    s0 = np.hypot(0.2, 0.1)
+    for _ in range(100):
+        p = gpu_move(p, E, B, grid, dt, 1.0, 3, mode)
+        assert abs(np.sqrt(p[3][0] ** 2 + p[4][0] ** 2 + p[5][0] ** 2) - s0) <= 1e-13 * s0
+    e, bz = 0.02, 1.0
+    E, B = uniform_field(grid, [0, e, 0], [0, 0, bz])
+    p = [np.array([4.0]), np.array([4.0]), np.array([4.0]), np.zeros(1), np.zeros(1), np.zeros(1)]
+    xu, xp = 4.0, 4.0
+    for _ in range(N):
+        p = gpu_move(p, E, B, grid, dt, 1.0, 3, mode)
+        d = p[0][0] - xp
+        d = d + 8.0 if d < -4.0 else (d - 8.0 if d > 4.0 else d)
+        xu += d
+        xp = p[0][0]
+    assert abs((xu - 4.0) / (N * dt) - e / bz) <= 0.01 * e / bz
 
 
 @pytest.mark.parametrize("path", ["counting", "radix_fallback"])
