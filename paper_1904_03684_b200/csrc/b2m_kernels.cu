@@ -465,54 +465,65 @@ __global__ void zinv_check_kernel(long long plane, long long nodes, const double
   if (!same) *flag = 1;
 }
 
+// z-invariant field: the bilinear column polynomial of plane k = 0 per x-y
+// column (the same P values as the 3-D table below, whose Q are all exactly
+// zero).  Thread = (column, component q); exits at once for a z-varying field.
+__global__ void field_to_cols_kernel(int nx, int ny, const double* __restrict__ E,
+                                     const double* __restrict__ B,
+                                     const __grid_constant__ CellTables T,
+                                     const int* __restrict__ zvar) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= 6LL * nx * ny || *zvar != 0) return;
+  const long long col = t / 6;
+  const int q = static_cast<int>(t % 6);
+  const int i = static_cast<int>(col % nx), j = static_cast<int>(col / nx);
+  const long long sx = nx + 1;
+  const double* F = (q < 3 ? E : B) + q % 3;
+  const double f00 = __ldg(F + 3 * (i + sx * j)), f10 = __ldg(F + 3 * (i + 1 + sx * j));
+  const double f01 = __ldg(F + 3 * (i + sx * (j + 1))), f11 = __ldg(F + 3 * (i + 1 + sx * (j + 1)));
+  for (int m = 0; m < T.n; ++m) {
+    const double c = T.scale[m];
+    const double g00 = c * f00, g10 = c * f10, g01 = c * f01, g11 = c * f11;
+    double* out = reinterpret_cast<double*>(T.out[m]) + col * 24 + 4 * q;
+    reinterpret_cast<double4*>(out)[0] =
+        make_double4(g00, g01 - g00, g10 - g00, (g11 - g10) - (g01 - g00));
+  }
+}
+
+// The general per-cell tables; a grid-stride loop over (cell, q), so for a
+// z-invariant field (zvar set and 0) the whole grid exits after one load.
 __global__ void field_to_cells_kernel(int nx, int ny, int nz, const double* __restrict__ E,
                                       const double* __restrict__ B,
                                       const __grid_constant__ CellTables T,
                                       const int* __restrict__ zvar) {
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (zvar && *zvar == 0) return;
   const long long ncell = static_cast<long long>(nx) * ny * nz;
-  if (t >= 6 * ncell) return;
-  const long long cell = t / 6;
-  const int q = static_cast<int>(t % 6);
-  const int i = static_cast<int>(cell % nx);
-  const int j = static_cast<int>((cell / nx) % ny);
-  const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
-  if (zvar && *zvar == 0) {
-    // z-invariant: the bilinear column polynomial of plane k = 0 (the same
-    // P values as the 3-D table below, whose Q are all exactly zero)
-    if (k != 0) return;
-    const long long sx = nx + 1;
+  const long long sx = nx + 1, sy = ny + 1;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < 6 * ncell;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long cell = t / 6;
+    const int q = static_cast<int>(t % 6);
+    const int i = static_cast<int>(cell % nx);
+    const int j = static_cast<int>((cell / nx) % ny);
+    const int k = static_cast<int>(cell / (static_cast<long long>(nx) * ny));
     const double* F = (q < 3 ? E : B) + q % 3;
-    const double f00 = __ldg(F + 3 * (i + sx * j)), f10 = __ldg(F + 3 * (i + 1 + sx * j));
-    const double f01 = __ldg(F + 3 * (i + sx * (j + 1))),
-                 f11 = __ldg(F + 3 * (i + 1 + sx * (j + 1)));
+    auto f = [&](int di, int dj, int dk) {
+      return __ldg(F + 3 * ((i + di) + sx * ((j + dj) + sy * (k + dk))));
+    };
+    // f<di dj dk>
+    const double f000 = f(0, 0, 0), f100 = f(1, 0, 0), f010 = f(0, 1, 0), f110 = f(1, 1, 0);
+    const double f001 = f(0, 0, 1), f101 = f(1, 0, 1), f011 = f(0, 1, 1), f111 = f(1, 1, 1);
     for (int m = 0; m < T.n; ++m) {
       const double c = T.scale[m];
-      const double g00 = c * f00, g10 = c * f10, g01 = c * f01, g11 = c * f11;
-      double* out = reinterpret_cast<double*>(T.out[m]) + cell * 24 + 4 * q;
-      reinterpret_cast<double4*>(out)[0] =
-          make_double4(g00, g01 - g00, g10 - g00, (g11 - g10) - (g01 - g00));
+      const double g000 = c * f000, g100 = c * f100, g010 = c * f010, g110 = c * f110;
+      const double g001 = c * f001, g101 = c * f101, g011 = c * f011, g111 = c * f111;
+      const double d00 = g001 - g000, d10 = g101 - g100, d01 = g011 - g010, d11 = g111 - g110;
+      double2* out = T.out[m] + cell * (kCellDoubles / 2) + 4 * q;
+      out[0] = make_double2(g000, d00);
+      out[1] = make_double2(g010 - g000, d01 - d00);
+      out[2] = make_double2(g100 - g000, d10 - d00);
+      out[3] = make_double2((g110 - g100) - (g010 - g000), (d11 - d10) - (d01 - d00));
     }
-    return;
-  }
-  const long long sx = nx + 1, sy = ny + 1;
-  const double* F = (q < 3 ? E : B) + q % 3;
-  auto f = [&](int di, int dj, int dk) {
-    return __ldg(F + 3 * ((i + di) + sx * ((j + dj) + sy * (k + dk))));
-  };
-  // f<di dj dk>
-  const double f000 = f(0, 0, 0), f100 = f(1, 0, 0), f010 = f(0, 1, 0), f110 = f(1, 1, 0);
-  const double f001 = f(0, 0, 1), f101 = f(1, 0, 1), f011 = f(0, 1, 1), f111 = f(1, 1, 1);
-  for (int m = 0; m < T.n; ++m) {
-    const double c = T.scale[m];
-    const double g000 = c * f000, g100 = c * f100, g010 = c * f010, g110 = c * f110;
-    const double g001 = c * f001, g101 = c * f101, g011 = c * f011, g111 = c * f111;
-    const double d00 = g001 - g000, d10 = g101 - g100, d01 = g011 - g010, d11 = g111 - g110;
-    double2* out = T.out[m] + cell * (kCellDoubles / 2) + 4 * q;
-    out[0] = make_double2(g000, d00);
-    out[1] = make_double2(g010 - g000, d01 - d00);
-    out[2] = make_double2(g100 - g000, d10 - d00);
-    out[3] = make_double2((g110 - g100) - (g010 - g000), (d11 - d10) - (d01 - d00));
   }
 }
 
@@ -851,7 +862,12 @@ void launch_field_to_cells(int nx, int ny, int nz, const double* E, const double
       T.out[T.n] = tables[base + T.n];
       T.scale[T.n] = scale[base + T.n];
     }
-    field_to_cells_kernel<<<grid_for(6 * ncell, 192), 192, 0, st>>>(nx, ny, nz, E, B, T, zvar);
+    if (zvar) {
+      field_to_cols_kernel<<<grid_for(6LL * nx * ny, 192), 192, 0, st>>>(nx, ny, E, B, T, zvar);
+      note_launch();
+    }
+    const long long blocks = std::min<long long>(grid_for(6 * ncell, 192), 8LL * device_sms());
+    field_to_cells_kernel<<<static_cast<int>(blocks), 192, 0, st>>>(nx, ny, nz, E, B, T, zvar);
     note_launch();
   }
 }
