@@ -13,11 +13,9 @@ from __future__ import annotations
 
 import ctypes as C
 
-import numpy as np
-
 from . import _capi
 from .errors import EngineFault, MinipicError, NumericalFault
-from .mover import MODES, FieldMesh, Grid, MoverParams, ParticleBatch
+from .mover import MODES, FieldMesh, Grid, MoverParams
 
 
 class DeviceStore:

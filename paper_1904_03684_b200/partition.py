@@ -21,14 +21,12 @@ double (tests/test_partition.py).
 from __future__ import annotations
 
 import ctypes as C
-import json
-import os
 import time
 from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import CflViolation, ConfigError, EngineFault
+from .errors import ConfigError, EngineFault
 
 
 @dataclass(frozen=True)

@@ -4,7 +4,6 @@ exceeds them (DeviceArena::configure, device_arena.cpp:20-55; the batch's
 fixed capacity, particle_batch.hpp:43-46), bad setups ConfigError
 (runtime.cpp:22-37 decompose, kernels.hpp:30-39 MoverParams), and nothing is
 silently truncated."""
-import numpy as np
 import pytest
 import torch
 

@@ -1,7 +1,6 @@
 """The product's native GEM generator (csrc/b2m_gem.cpp) against the
 reference's init_gem (init.cpp:62-102): bit-identical particles and field.
 Host code only -- runs on CPU."""
-import numpy as np
 import pytest
 
 import oracle

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1904_03684_b200 import DomainError, Grid, MomentMesh, ParticleBatch, deposit_moments
+from paper_1904_03684_b200 import DomainError, Grid, MomentMesh, deposit_moments
 from paper_1904_03684_b200 import gem
 from paper_1904_03684_b200.engine import DeviceStore
 from paper_1904_03684_b200.mover import MoverParams
