@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
               }
             }
             double y1 = 0.0;
-            const unsigned bad = fast_particle_2d<WT, R>(F.fg, F.U, cols, buf[st], p, cnt, C, &y1);
+            const unsigned bad = fast_particle_2d<WT, R, !DEP && B2M_2D_PRED_RELOAD>(
+                F.fg, F.U, cols, buf[st], p, cnt, C, &y1);
             after(j, bad, y1);
           }
         };
@@ -320,7 +321,8 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
 #pragma unroll (kUnroll3D)
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
-        const unsigned bad = fast_particle_v2<WT, R>(F.fg, F.U, cells, buf[st], p, cnt, C);
+        const unsigned bad = fast_particle_v2<WT, R, !DEP && B2M_3D_PRED_RELOAD>(F.fg, F.U, cells,
+                                                                                buf[st], p, cnt, C);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
         if (DEP) {
           if (B2M_DEP_STAGE_UVW) {

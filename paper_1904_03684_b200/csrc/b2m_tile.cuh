@@ -455,6 +455,10 @@ __device__ __forceinline__ bool finite3(double a, double b, double c) {
   return m != kE;
 }
 
+#ifndef B2M_3D_PRED_RELOAD
+#define B2M_3D_PRED_RELOAD 1    // the general kernel's cell reload as predicated loads (2.515 -> 2.46 ms; not in the fused kernel: spills)
+#endif
+
 struct FastCell {
   Coef8 K[6];
   double ci, cj, ck;  // the cached cell's corner in cell units
@@ -469,6 +473,7 @@ __device__ __forceinline__ void fast_cell_reset(FastCell& C) {
 // Locate a folded cell-unit position (indices clamped: a flagged NaN reads a
 // valid cell), load its coefficients when it is not the cached cell, and
 // return the fractions relative to it.
+template <bool PRED = false>
 __device__ __forceinline__ void fast_enter(const FastGrid& g, const double2* __restrict__ cells,
                                            FastCell& C, double tx, double ty, double tz,
                                            double& fx, double& fy, double& fz) {
@@ -481,7 +486,25 @@ __device__ __forceinline__ void fast_enter(const FastGrid& g, const double2* __r
   fy = ty - dj;
   fz = tz - dk;
   const int cell = i + g.nx * (j + g.ny * m);
-  if (cell != C.cell) {
+  if (PRED) {
+    const double2* c = cells + static_cast<long long>(cell) * 24;
+    const uint64_t pol = policy_evict_last();
+    const int diff = cell != C.cell;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %5, 0;\n\t"
+          "@p ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+          : "+d"(C.K[q].p0), "+d"(C.K[q].q0), "+d"(C.K[q].p1), "+d"(C.K[q].q1)
+          : "l"(c + 4 * q), "r"(diff), "l"(pol));
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %5, 0;\n\t"
+          "@p ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+          : "+d"(C.K[q].p2), "+d"(C.K[q].q2), "+d"(C.K[q].p3), "+d"(C.K[q].q3)
+          : "l"(c + 4 * q + 2), "r"(diff), "l"(pol));
+    }
+    C.cell = cell;
+  } else if (cell != C.cell) {
     const double2* c = cells + static_cast<long long>(cell) * 24;
 #pragma unroll
     for (int q = 0; q < 6; ++q) C.K[q] = load_coef8(c + 4 * q);
@@ -514,7 +537,7 @@ __device__ __forceinline__ void implicit_num(double u0, double v0, double w0, co
 // One FAST particle (kernels.cpp:52-104 in FMA form).  buf[a][p] holds input
 // a of particle p and receives its result when it finishes clean; returns 1
 // for a particle to report as faulted.
-template <int TILE, int ROUNDS>
+template <int TILE, int ROUNDS, bool PRED = false>
 __device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const FastUniform& U,
                                                      const double2* __restrict__ cells,
                                                      double (*buf)[TILE], int p, int cnt,
@@ -532,7 +555,7 @@ __device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const Fa
     const bool inside = (p < cnt) && in_range(x0, dbits(g.lx)) && in_range(y0, dbits(g.ly)) &&
                         in_range(z0, dbits(g.lz));
     bad = inside ? 0u : 1u;
-    fast_enter(g, cells, C, inside ? cx : 0.0, inside ? cy : 0.0, inside ? cz : 0.0, fx0, fy0,
+    fast_enter<PRED>(g, cells, C, inside ? cx : 0.0, inside ? cy : 0.0, inside ? cz : 0.0, fx0, fy0,
                fz0);
   }
   }
@@ -563,7 +586,7 @@ __device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const Fa
           ty = fold_fast(ty, g.nyd, dbits(g.nyd), g.rny, bad);
           tz = fold_fast(tz, g.nzd, dbits(g.nzd), g.rnz, bad);
         }
-        fast_enter(g, cells, C, tx, ty, tz, fx, fy, fz);
+        fast_enter<PRED>(g, cells, C, tx, ty, tz, fx, fy, fz);
         // the start position in the new cell's (folded) frame
         fx0 = fma(-bx, U.dc[0], fx);
         fy0 = fma(-by, U.dc[1], fy);
@@ -608,6 +631,9 @@ __device__ __forceinline__ unsigned fast_particle_v2(const FastGrid& g, const Fa
 // the z predictor feeds nothing but the gather, so it is not formed (a
 // non-finite vbar_z is still flagged, and z1 is checked at the end).
 
+#ifndef B2M_2D_PRED_RELOAD
+#define B2M_2D_PRED_RELOAD 1    // column reload as predicated loads, not a branch (1.158 -> 1.134 ms; not in the fused kernel)
+#endif
 #ifndef B2M_2D_LOCATE_ALWAYS
 #define B2M_2D_LOCATE_ALWAYS 1  // locate every particle's start (no frame test): 1.16 -> 1.13 ms
 #endif
@@ -640,6 +666,24 @@ __device__ __forceinline__ void fast_col_reset(FastCol& C) {
   C.ci = C.cj = -4.0;
 }
 
+// Column reload as six predicated 256-bit loads (no divergent branch, so no
+// reconvergence barrier: the scheduler can interleave the unrolled particles
+// around it); en = false leaves the cache untouched.
+__device__ __forceinline__ void reload_col_pred(FastCol& C, const double* __restrict__ cols,
+                                                int col, bool en) {
+  const double* c = cols + static_cast<long long>(col) * 24;
+  const uint64_t pol = policy_evict_last();
+  const int diff = en && col != C.col;
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %5, 0;\n\t"
+        "@p ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+        : "+d"(C.K[q].p0), "+d"(C.K[q].p1), "+d"(C.K[q].p2), "+d"(C.K[q].p3)
+        : "l"(c + 4 * q), "r"(diff), "l"(pol));
+}
+
+template <bool PRED = false>
 __device__ __forceinline__ void fast_enter2(const FastGrid& g, const double* __restrict__ cols,
                                             FastCol& C, double tx, double ty, double& fx,
                                             double& fy) {
@@ -649,7 +693,10 @@ __device__ __forceinline__ void fast_enter2(const FastGrid& g, const double* __r
   fx = tx - di;
   fy = ty - dj;
   const int col = i + g.nx * j;
-  if (col != C.col) {
+  if (PRED) {
+    reload_col_pred(C, cols, col, true);
+    C.col = col;
+  } else if (col != C.col) {
     const double* c = cols + static_cast<long long>(col) * 24;
 #pragma unroll
     for (int q = 0; q < 6; ++q) C.K[q] = load_coef4(c + 4 * q);
@@ -676,7 +723,7 @@ __device__ __forceinline__ void col_prefetch(const FastGrid& g, const double* __
 
 // y_out: the new y of a particle that moved clean (the migration scan reads
 // it from a register instead of the tile)
-template <int TILE, int ROUNDS>
+template <int TILE, int ROUNDS, bool PRED = false>
 __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const FastUniform& U,
                                                      const double* __restrict__ cols,
                                                      double (*buf)[TILE], int p, int cnt,
@@ -691,7 +738,8 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
     const bool inside = (p < cnt) & in_range(x0, dbits(g.lx)) & in_range(y0, dbits(g.ly)) &
                         in_range(z0, dbits(g.lz));
     bad = inside ? 0u : 1u;
-    fast_enter2(g, cols, C, inside ? x0 * g.rdx : 0.0, inside ? y0 * g.rdy : 0.0, fx0, fy0);
+    fast_enter2<PRED>(g, cols, C, inside ? x0 * g.rdx : 0.0, inside ? y0 * g.rdy : 0.0, fx0,
+                      fy0);
   } else {
     const double cx = x0 * g.rdx, cy = y0 * g.rdy;
     fx0 = cx - C.ci;
@@ -718,7 +766,8 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
       if (!finite3(nz, rc, rc)) bad = 1u;
       fx = fma(nx * U.dc[0], rc, fx0);
       fy = fma(ny * U.dc[1], rc, fy0);
-      if (!(in_unit(fx) & in_unit(fy))) {
+      const bool cross = !(in_unit(fx) & in_unit(fy));
+      if (cross) {
         const double bx = nx * rc, by = ny * rc;
         const double cx = lds_f64(&buf[0][p]) * g.rdx, cy = lds_f64(&buf[1][p]) * g.rdy;
         double tx = fma(bx, U.dc[0], cx), ty = fma(by, U.dc[1], cy);
@@ -726,7 +775,7 @@ __device__ __forceinline__ unsigned fast_particle_2d(const FastGrid& g, const Fa
           tx = fold_fast(tx, g.nxd, dbits(g.nxd), g.rnx, bad);
           ty = fold_fast(ty, g.nyd, dbits(g.nyd), g.rny, bad);
         }
-        fast_enter2(g, cols, C, tx, ty, fx, fy);
+        fast_enter2<PRED>(g, cols, C, tx, ty, fx, fy);
         fx0 = fma(-bx, U.dc[0], fx);
         fy0 = fma(-by, U.dc[1], fy);
       }
