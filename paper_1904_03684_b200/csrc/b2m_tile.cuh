@@ -962,6 +962,9 @@ struct PState {
 
 // Cell field cache.  FAST: 24 double2 polynomial pairs (b2m_mover.cuh
 // layout).  STRICT: the 8 corner nodes' (E, B) in corner order.
+#ifndef B2M_STRICT_PRED_RELOAD
+#define B2M_STRICT_PRED_RELOAD 1  // STRICT cache reload as predicated loads (3.077 -> 3.064 ms)
+#endif
 struct CellCache {
   double2 c[24];
   int cell;
@@ -986,6 +989,25 @@ __device__ __forceinline__ void cache_load_strict(CellCache& cc, const double* _
     cc.c[2 * q] = make_double2(a, b);
     cc.c[2 * q + 1] = make_double2(d, e);
   }
+  cc.cell = cell;
+}
+
+// The same reload as predicated loads (no divergent branch): the cache is
+// replaced only where `diff` is set.
+template <int DIM = 3>
+__device__ __forceinline__ void cache_load_strict_pred(CellCache& cc,
+                                                       const double* __restrict__ nodes, int cell,
+                                                       bool diff) {
+  const double* c = nodes + static_cast<long long>(cell) * 48;
+  const int d = diff;
+#pragma unroll
+  for (int q = 0; q < (DIM == 2 ? 6 : 12); ++q)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %5, 0;\n\t"
+        "@p ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+d"(cc.c[2 * q].x), "+d"(cc.c[2 * q].y), "+d"(cc.c[2 * q + 1].x),
+          "+d"(cc.c[2 * q + 1].y)
+        : "l"(c + 4 * q), "r"(d));
   cc.cell = cell;
 }
 
@@ -1117,7 +1139,8 @@ __device__ __forceinline__ unsigned strict_tile_thread_p1(const DevGrid& g, cons
     const int cell = strict_locate(P, g, wt, DIM == 2 ? &column : nullptr);
     if (!P.ok) return 1u;  // the reference's DomainError -> NumericalFault
     const int key = DIM == 2 ? column : cell;
-    if (key != cc.cell) cache_load_strict<DIM>(cc, nodes, key);
+    if (B2M_STRICT_PRED_RELOAD) cache_load_strict_pred<DIM>(cc, nodes, key, key != cc.cell);
+    else if (key != cc.cell) cache_load_strict<DIM>(cc, nodes, key);
     strict_round<DIM>(P, cc, wt, sp.beta);
     if (r + 1 < rounds) strict_predict(P, wg, sp.dto2);
   }

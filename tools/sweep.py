@@ -16,7 +16,7 @@ grid = Grid.make(64, 64, 32, 25.6, 12.8, 6.4)
 batches = gem.init_gem_species(grid, 216, pinned=True)
 field = gem.gem_bench_field(grid, z_varying=os.environ.get("SW_3D") == "1")
 mps = [MoverParams.make(0.1, b.qom, 3) for b in batches]
-st = DeviceStore(grid, [b.count() for b in batches], "fast")
+st = DeviceStore(grid, [b.count() for b in batches], os.environ.get("B2M_MODE", "fast"))
 st.upload_field(field)
 for s, b in enumerate(batches): st.upload(s, b.span())
 for s in range(4): st.sort(s)
