@@ -414,8 +414,9 @@ def c3_single_gpu(args, local, field_kind):
     mps = [MoverParams.make(DT, float(qom[s]), PC) for s in range(4)]
     time_steps(store, mps, args.warmup, True, False)
     torch.cuda.synchronize()
-    ev = time_steps(store, mps, args.steps, True, True)
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev = time_steps(store, mps, args.steps, True, True)
+        torch.cuda.synchronize()
     store.sync()
     store.close()
     n = sum(counts)
@@ -425,6 +426,7 @@ def c3_single_gpu(args, local, field_kind):
     return {"particles": n, "n_gpus": 1, "ms_per_step": ms, "value": n / (ms * 1e-3) / 1e6,
             "unit": "MPA/s", "kernel_ms": kms,
             "roofline_frac": BYTES_PER_PARTICLE * n / (kms * 1e-3) / 1e9 / peak,
+            "step_ms": [round(t, 4) for t, k in ev], "clocks": clk.summary(),
             "init_s": t_init,
             "workload": "GEM 128x128x64, L = (51.2, 25.6, 12.8), 235 ppc (SURVEY C3, BASELINE "
                         "configs[2]) on one GPU: field refresh + mover"}
