@@ -1,2 +1,2 @@
-python tools/sweep.py 4x3_base 4x3_ur 4x3_base 4x3_ur > gpurun_out/sweep_ur.log 2>&1
-cat gpurun_out/sweep_ur.log
+python tools/sweep.py 4x3_base:3d 4x3_pf3:3d 4x3_base:3d 4x3_pf3:3d > gpurun_out/sweep_pf3.log 2>&1
+cat gpurun_out/sweep_pf3.log
