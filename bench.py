@@ -834,17 +834,18 @@ def run_world(args):
             a.record()
             step()
             b.record()
-            per.append((a, b, (store.elapsed_ms(13, 14), store.elapsed_ms(14, 15))
-                        if native else (None, None)))
+            per.append((a, b))
         t1.record()
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1) / steps
         launches = _capi.lib().b2m_launch_count() - l0
-        step_ms = [a.elapsed_time(b) for a, b, _ in per]
-        mover = [x[0] for _, _, x in per if x[0] is not None]
-        exch = [x[1] for _, _, x in per if x[1] is not None]
-        return ms, step_ms, (sum(mover) / len(mover) if mover else None), \
-            (sum(exch) / len(exch) if exch else None), launches
+        step_ms = [a.elapsed_time(b) for a, b in per]
+        # the native step's phase events (slots 13-15: mover + scan + compaction,
+        # then exchange + merge) hold the LAST step; reading them inside the
+        # loop would add a host sync per step
+        if native:
+            return ms, step_ms, store.elapsed_ms(13, 14), store.elapsed_ms(14, 15), launches
+        return ms, step_ms, None, None, launches
 
     # ---- weak scaling: every rank a C2-sized slab ----
     grid = Grid.make(NX, NY * world, NZ, LX, LY * world, LZ)

@@ -294,15 +294,18 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
  * buffers without a communicator (world of 1, or b2m_world_loopback_step).
  * b2m_world_set_total: the global particle count, the conservation reference
  * (runtime.cpp:150).  b2m_world_step: b2m_move_migrate_all, the outbox counts
- * and then the records exchanged with prev / next (grouped ncclSend/ncclRecv),
- * merge, and one all-reduce of (count, faulted): returns this rank's typed
- * fault (NumericalFault / CflViolation / DomainError / AllocError) when it
- * faulted -- it still completes the exchange with empty outboxes so its peers
- * do not hang (the analogue of arrive_and_drop, runtime.cpp:283-288) --,
- * EngineFault when a peer faulted or the global count drifted.  Two host
- * synchronisations per step.  *sent = records this rank sent.  The step
- * records event slots 13 (start), 14 (mover + compaction enqueued) and 15
- * (exchange, merge and count all-reduce enqueued) on the context's stream, so
+ * exchanged with prev / next, one all-reduce of (count after the merge,
+ * failed ranks) computed on the device from those counts, then -- when no
+ * rank failed and the count is conserved -- the records exchanged (grouped
+ * ncclSend/ncclRecv) and merged.  Returns this rank's typed fault
+ * (NumericalFault / CflViolation / DomainError / AllocError) when it failed
+ * -- it still takes part in the counts round and the all-reduce with empty
+ * outboxes, so its peers do not hang (the analogue of arrive_and_drop,
+ * runtime.cpp:283-288) --, EngineFault when a peer failed or the global count
+ * drifted; every rank reads the same reduced verdict, so all take the same
+ * branch.  One host synchronisation per step.  *sent = records this rank
+ * sent.  The step records event slots 13 (start), 14 (mover + compaction
+ * enqueued) and 15 (exchange and merge enqueued) on the context's stream, so
  * b2m_event_elapsed_ms(13, 14) / (14, 15) split its device time. */
 #define B2M_WORLD_ID_BYTES 128
 b2m_status b2m_world_id(void* id);

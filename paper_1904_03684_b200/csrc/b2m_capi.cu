@@ -412,6 +412,7 @@ b2m_status b2m_ctx_destroy(b2m_ctx* ctx) {
   if (ctx->mig_totals_h) cudaFreeHost(ctx->mig_totals_h);
   if (ctx->w.cnt_h) cudaFreeHost(ctx->w.cnt_h);
   if (ctx->w.red_h) cudaFreeHost(ctx->w.red_h);
+  if (ctx->w.vin_h) cudaFreeHost(ctx->w.vin_h);
   if (ctx->w.bflag_h) cudaFreeHost(ctx->w.bflag_h);
   if (ctx->w.comm) nccl().CommDestroy(ctx->w.comm);
   if (ctx->fault_h) cudaFreeHost(ctx->fault_h);

@@ -153,6 +153,8 @@ struct b2m_ctx {
     std::vector<uint64_t> stage_cap;         // records per species
     long long* red = nullptr;                // device [2]: count, faulted
     long long* red_h = nullptr;              // pinned [2]
+    unsigned long long* vin = nullptr;       // device [3][ns]: pre-step count, capacity, stage cap
+    unsigned long long* vin_h = nullptr;     // pinned [3][ns]
     double* bstage = nullptr;                // device: field broadcast header + plane 0 (E, B)
     double* bflag_h = nullptr;               // pinned: the broadcast header (z-invariance flag)
     double* mstage = nullptr;                // device [world][mesh]: gathered moment meshes

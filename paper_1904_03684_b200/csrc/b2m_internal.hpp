@@ -78,6 +78,13 @@ void launch_fault_reset(FaultWord* fault, cudaStream_t st);
 void launch_pack_counts(const unsigned long long* const* totals, int ns,
                         const unsigned long long* cap, const FaultWord* fault,
                         unsigned long long* out, cudaStream_t st);
+// Native slab world: this rank's verdict for the closing all-reduce, from
+// device state after the counts round (b2m_world_step).  vin = [3][ns]:
+// count before the step, capacity, exchange-buffer records per species.
+void launch_world_verdict(const unsigned long long* const* totals, int ns,
+                          const unsigned long long* cap, const FaultWord* fault,
+                          const unsigned long long* cnt_recv, const unsigned long long* vin,
+                          int own_bad, long long* red, cudaStream_t st);
 
 // Cell keys of the current positions (cell-unit locate), for sorting.
 void launch_cell_keys(const FastGrid& g, const double* x, const double* y, const double* z,

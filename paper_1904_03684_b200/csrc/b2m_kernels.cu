@@ -968,6 +968,40 @@ void launch_pack_counts(const unsigned long long* const* totals, int ns,
   note_launch();
 }
 
+// The rank's contribution to the step's all-reduce, {count after the merge,
+// failed}: failed when the rank was already failing (own_bad), the mover
+// faulted, an outbox overflowed, or the arrivals the counts round announced
+// would overflow the exchange buffer or the species' capacity -- the same
+// tests the host then repeats for its typed error (world_counts), so every
+// failure a rank can see before the records round is in the sum every rank
+// reads at the same sync.
+__global__ void world_verdict_kernel(const unsigned long long* const* totals, int ns,
+                                     const unsigned long long* cap, const FaultWord* fault,
+                                     const unsigned long long* cnt_recv,
+                                     const unsigned long long* vin, int own_bad, long long* red) {
+  if (threadIdx.x != 0) return;
+  bool bad = own_bad != 0 || fault->numerical != ~0ull || fault->cfl != ~0ull ||
+             fault->domain != ~0ull;
+  long long n = 0;
+  for (int s = 0; s < ns; ++s) {
+    const unsigned long long in = cnt_recv[s] + cnt_recv[ns + s];
+    const unsigned long long pre = vin[s], holes = totals[s][2];
+    bad = bad || totals[s][0] > cap[s] || totals[s][1] > cap[s] || in > vin[2 * ns + s] ||
+          holes > pre || pre - holes + in > vin[ns + s];
+    n += static_cast<long long>(pre - holes + in);
+  }
+  red[0] = bad ? 0 : n;
+  red[1] = bad ? 1 : 0;
+}
+
+void launch_world_verdict(const unsigned long long* const* totals, int ns,
+                          const unsigned long long* cap, const FaultWord* fault,
+                          const unsigned long long* cnt_recv, const unsigned long long* vin,
+                          int own_bad, long long* red, cudaStream_t st) {
+  world_verdict_kernel<<<1, 32, 0, st>>>(totals, ns, cap, fault, cnt_recv, vin, own_bad, red);
+  note_launch();
+}
+
 uint64_t migrate_tiles(uint64_t n) { return (n + kTileParticles - 1) / kTileParticles; }
 
 size_t scan_temp_bytes(uint64_t n_tiles) {

@@ -182,6 +182,11 @@ b2m_status world_counts(b2m_ctx* ctx) {
       ctx->poison_msg = "arrivals exceed the exchange buffer";
       return fail(B2M_ALLOC_ERROR, ctx->poison_msg);
     }
+    if (S.pre_count - S.totals_h[2] + in > S.capacity) {  // b2m_inbox_append's test, early
+      ctx->poisoned = true;
+      ctx->poison_msg = "particle batch capacity exceeded (fixed at allocation)";
+      return fail(B2M_ALLOC_ERROR, ctx->poison_msg);
+    }
   }
   return B2M_OK;
 }
@@ -241,8 +246,10 @@ b2m_status world_alloc(b2m_ctx* ctx, const std::vector<uint64_t>& stage_cap) {
   if ((st = dalloc(ctx, &w.cnt_send, 2 * ns, "world counts")) != B2M_OK) return st;
   if ((st = dalloc(ctx, &w.cnt_recv, 2 * ns, "world counts")) != B2M_OK) return st;
   if ((st = dalloc(ctx, &w.red, 2, "world reduction")) != B2M_OK) return st;
+  if ((st = dalloc(ctx, &w.vin, 3 * ns, "world verdict inputs")) != B2M_OK) return st;
   if (cudaMallocHost(&w.cnt_h, 4 * ns * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMallocHost(&w.red_h, 2 * sizeof(long long)) != cudaSuccess) {
+      cudaMallocHost(&w.red_h, 2 * sizeof(long long)) != cudaSuccess ||
+      cudaMallocHost(&w.vin_h, 3 * ns * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     return fail(B2M_ALLOC_ERROR, "pinned world buffers");
   }
@@ -434,9 +441,11 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
                           uint64_t* global_count) {
   // Only argument errors that are the same on every rank return before the
   // collectives.  Any per-rank failure -- a context poisoned earlier, a
-  // missing field, a launch or tensor-map error, a device fault -- is carried
-  // like a fault: empty outboxes, every round of the protocol still run, the
-  // flag in the closing all-reduce, so no peer waits in a collective alone.
+  // missing field, a launch or tensor-map error, a device fault, an outbox,
+  // exchange-buffer or capacity overflow -- is carried like a fault: empty
+  // outboxes, the counts round still run, the flag in the all-reduce that
+  // every rank reads at the step's one host sync, so no peer ever waits in
+  // a collective alone.
   if (!ctx) return fail(B2M_INVALID_ARGUMENT, "null context");
   if (!ctx->w.on) return fail(B2M_CONFIG_ERROR, "world_step: call b2m_world_init first");
   if (!mp) return fail(B2M_INVALID_ARGUMENT, "null mover params");
@@ -468,8 +477,25 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
     B2M_NCCL(ctx, nccl().Recv(w.cnt_recv + ns, ns, ncclUint64, next, w.comm, ctx->stream));
     B2M_NCCL(ctx, nccl().GroupEnd());
   }
+  // the verdict (runtime.cpp:264-269's count check, with the failure flag
+  // riding along) reduced BEFORE the records round: {count after the merge,
+  // failed ranks} from device state, so one host sync per step serves the
+  // counts, the typed local error and the global decision
+  for (int s = 0; s < ns; ++s) {
+    const Species& S = ctx->sp[static_cast<size_t>(s)];
+    w.vin_h[s] = own == B2M_OK ? S.pre_count : 0;
+    w.vin_h[ns + s] = S.capacity;
+    w.vin_h[2 * ns + s] = w.stage_cap[static_cast<size_t>(s)];
+  }
+  cudaMemcpyAsync(w.vin, w.vin_h, 3 * ns * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                  ctx->stream);
+  launch_world_verdict(w.totals, ns, w.cap, ctx->fault, w.cnt_recv, w.vin, own != B2M_OK, w.red,
+                       ctx->stream);
+  if (w.comm)
+    B2M_NCCL(ctx, nccl().AllReduce(w.red, w.red, 2, ncclInt64, ncclSum, w.comm, ctx->stream));
+  cudaMemcpyAsync(w.red_h, w.red, 2 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
   if (own == B2M_OK) {
-    own = world_counts(ctx);  // host sync 1
+    own = world_counts(ctx);  // the host sync; typed fault, poisons
     if (own != B2M_OK) own_msg = b2m_last_error();
   } else {
     cudaMemcpyAsync(w.cnt_h, w.cnt_send, 2 * ns * sizeof(unsigned long long),
@@ -478,48 +504,46 @@ b2m_status b2m_world_step(b2m_ctx* ctx, const b2m_mover_params* mp, uint64_t* se
                     cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
   }
-  const unsigned long long* c = w.cnt_h;  // [to prev][to next][from prev][from next]
-  if (exchange) {
-    B2M_NCCL(ctx, nccl().GroupStart());
-    for (int s = 0; s < ns; ++s)
-      if (c[s])
-        B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[0], 6 * c[s], ncclFloat64,
-                               prev, w.comm, ctx->stream));
-    for (int s = 0; s < ns; ++s)
-      if (c[ns + s])
-        B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[1], 6 * c[ns + s],
-                               ncclFloat64, next, w.comm, ctx->stream));
-    for (int s = 0; s < ns; ++s)
-      if (c[2 * ns + s])
-        B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)], 6 * c[2 * ns + s], ncclFloat64,
-                               prev, w.comm, ctx->stream));
-    for (int s = 0; s < ns; ++s)
-      if (c[3 * ns + s])
-        B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)] + 6 * c[2 * ns + s],
-                               6 * c[3 * ns + s], ncclFloat64, next, w.comm, ctx->stream));
-    B2M_NCCL(ctx, nccl().GroupEnd());
-  }
   if (sent) *sent = world_sent(ctx);
-  if (own == B2M_OK) {
+  const long long n_after = w.red_h[0], failed = w.red_h[1];
+  if (own == B2M_OK && failed == 0 && !(w.total_set && static_cast<uint64_t>(n_after) != w.total)) {
+    // records round: every rank reached this branch (same reduced values)
+    const unsigned long long* c = w.cnt_h;  // [to prev][to next][from prev][from next]
+    if (exchange) {
+      B2M_NCCL(ctx, nccl().GroupStart());
+      for (int s = 0; s < ns; ++s)
+        if (c[s])
+          B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[0], 6 * c[s],
+                                 ncclFloat64, prev, w.comm, ctx->stream));
+      for (int s = 0; s < ns; ++s)
+        if (c[ns + s])
+          B2M_NCCL(ctx, nccl().Send(ctx->sp[static_cast<size_t>(s)].out[1], 6 * c[ns + s],
+                                 ncclFloat64, next, w.comm, ctx->stream));
+      for (int s = 0; s < ns; ++s)
+        if (c[2 * ns + s])
+          B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)], 6 * c[2 * ns + s],
+                                 ncclFloat64, prev, w.comm, ctx->stream));
+      for (int s = 0; s < ns; ++s)
+        if (c[3 * ns + s])
+          B2M_NCCL(ctx, nccl().Recv(w.stage[static_cast<size_t>(s)] + 6 * c[2 * ns + s],
+                                 6 * c[3 * ns + s], ncclFloat64, next, w.comm, ctx->stream));
+      B2M_NCCL(ctx, nccl().GroupEnd());
+    }
+    // the merge cannot overflow (tested above on every rank); a CUDA error
+    // here is this rank's alone and surfaces at its next call
     own = world_merge(ctx);
-    if (own != B2M_OK) own_msg = b2m_last_error();
-  }
-  // count check (runtime.cpp:264-269) with the fault flag riding along
-  w.red_h[0] = own == B2M_OK ? static_cast<long long>(world_local_count(ctx)) : 0;
-  w.red_h[1] = own == B2M_OK ? 0 : 1;
-  if (w.comm) {
-    cudaMemcpyAsync(w.red, w.red_h, 2 * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream);
-    B2M_NCCL(ctx, nccl().AllReduce(w.red, w.red, 2, ncclInt64, ncclSum, w.comm, ctx->stream));
-    cudaMemcpyAsync(w.red_h, w.red, 2 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaEventRecord(ctx->ev[15], ctx->stream);
+    if (own != B2M_OK) return own;
+    if (global_count) *global_count = static_cast<uint64_t>(n_after);
+    return B2M_OK;
   }
   cudaEventRecord(ctx->ev[15], ctx->stream);
-  if (w.comm) cudaStreamSynchronize(ctx->stream);  // host sync 2
-  if (own != B2M_OK && !ctx->poisoned) {  // e.g. an arrival overflowed the batch capacity
+  if (own != B2M_OK && !ctx->poisoned) {
     ctx->poisoned = true;
     ctx->poison_msg = own_msg;
   }
   if (own != B2M_OK) set_error(own_msg);
-  return world_verdict(ctx, own, w.red_h[0], own == B2M_OK ? w.red_h[1] : 0, global_count);
+  return world_verdict(ctx, own, n_after, own == B2M_OK ? failed : 0, global_count);
 }
 
 b2m_status b2m_world_loopback_step(b2m_ctx* const* ctxs, int world, const b2m_mover_params* mp,
