@@ -101,6 +101,7 @@ namespace b2m {
 
 b2m_status cuda_fail(b2m_ctx* ctx, cudaError_t e, const char* what) {
   std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // reported here: a non-sticky error must not resurface at a later check
   if (ctx) {
     ctx->poisoned = true;
     ctx->poison_msg = msg;
@@ -115,6 +116,10 @@ b2m_status check_ctx(b2m_ctx* ctx) {
     return fail(B2M_ENGINE_FAULT, "device state is invalid after an earlier fault: " + ctx->poison_msg);
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  // every entry point checks cudaGetLastError() after its launches: drop a
+  // non-sticky error some earlier, unrelated call of this host thread left
+  // behind (a device fault is sticky and still reported)
+  cudaGetLastError();
   return B2M_OK;
 }
 

@@ -760,6 +760,7 @@ bool launch_warp_tiles(const TileField& F, const SpeciesLaunch* sp, int n_spans,
       const int k = std::atoi(e);
       if (k > 0 && k < per_sm) cap = sms * k;
     }
+    cudaGetLastError();  // a failed query above falls back, it is not the caller's error
     return cap;
   }();
   // FAST launches share dt / pc_iterations across their spans (FastUniform):

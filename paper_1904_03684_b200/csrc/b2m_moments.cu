@@ -423,6 +423,7 @@ void launch_dmma(const DevGrid& g, const SpeciesLaunch& sp, double qv, const Mom
   static const int per_sm = [] {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_dmma_kernel<SET>, kDmmaThreads, 0);
+    cudaGetLastError();
     return b > 0 ? b : 1;
   }();
   const unsigned long long warps =
@@ -445,6 +446,7 @@ void launch_group(const DevGrid& g, const SpeciesLaunch& sp, double qv, const Mo
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, deposit_group_kernel<SET, EXACT>,
                                                   kGroupThreads, smem);
+    cudaGetLastError();
     return b > 0 ? b : 1;
   }();
   const unsigned long long warps =
