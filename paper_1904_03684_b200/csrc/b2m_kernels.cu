@@ -90,6 +90,9 @@ constexpr int kUnroll3D = B2M_3D_UNROLL;
 #ifndef B2M_TILE_RUN_3D
 #define B2M_TILE_RUN_3D 1      // 3-D kernels (runs of 2 and 4 measured 1 % slower)
 #endif
+#ifndef B2M_LEAVE_MASK
+#define B2M_LEAVE_MASK 1       // column kernel owner scan: a per-lane leave mask, classified per tile (-50 us at C2)
+#endif
 #ifndef B2M_TILE_PREFETCH
 #define B2M_TILE_PREFETCH 0    // 1: L1 prefetch of the next tile's first-row columns
 #endif
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       FastCol C;
       fast_col_reset(C);
       uint8_t* flags = S.flags[s];
+      unsigned leave = 0;  // B2M_LEAVE_MASK: bit j = this lane's row-j particle left the slab
       const double* cols = reinterpret_cast<const double*>(sp.cells);
       // per moved particle: fault record, fused deposit, migration flag
       auto after = [&](int j, unsigned bad, double y1) {
@@ -228,19 +232,28 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                         buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
           }
         }
-        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
-        // warp ballot; the compaction re-derives each leaver from its y
+        // owner scan (partition_outgoing, runtime.cpp:46-62)
         if (flags) {
-          int flag = 0;
-          if (p < cnt && !bad) {
-            flag = slab_flag(y1, sl);
-            if (flag == 3) {
-              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
-              flag = 0;
+          if (B2M_LEAVE_MASK && !DEP) {
+            // per particle only the one-compare "stays in my slab" test; the
+            // tile's leavers are classified after its last row (rare)
+            const unsigned long long b = dbits(y1) & kAbs;
+            const bool stay = b - dbits(sl.own_lo) < dbits(sl.own_hi) - dbits(sl.own_lo);
+            if ((p < cnt) & !bad & !stay) leave |= 1u << j;
+          } else {
+            // leavers per row by warp ballot; the compaction re-derives each
+            // leaver from its y
+            int flag = 0;
+            if (p < cnt && !bad) {
+              flag = slab_flag(y1, sl);
+              if (flag == 3) {
+                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
+                flag = 0;
+              }
             }
+            n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+            n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
           }
-          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
-          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       };
       if (B2M_2D_PAIR && (P % 2) == 0) {
@@ -308,6 +321,21 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
               F.U.rounds == 3 ? fast_particle_2d<WT, 3>(F.fg, F.U, cols, buf[st], p, cnt, C, &y1)
                               : fast_particle_2d<WT, 0>(F.fg, F.U, cols, buf[st], p, cnt, C, &y1);
           after(j, bad, y1);
+        }
+      }
+      if (B2M_LEAVE_MASK && !DEP && flags && __any_sync(0xffffffffu, leave)) {
+#pragma unroll 1
+        for (int j = 0; j < P; ++j) {
+          int flag = 0;
+          if ((leave >> j) & 1u) {
+            flag = slab_flag(buf[st][1][lane + 32 * j], sl);
+            if (flag == 3) {
+              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + lane + 32 * j));
+              flag = 0;
+            }
+          }
+          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
         }
       }
     } else if (B2M_FAST_V == 2) {
