@@ -335,8 +335,9 @@ class SlabWorld:
 class NativeSlabWorld:
     """One rank of the slab-partitioned mover with the whole per-cycle
     protocol in the native library (b2m_world_step: mover + owner scan +
-    compaction, NCCL exchange with prev / next, merge, count all-reduce --
-    two host synchronisations per step, no Python on the data path).
+    compaction, counts exchanged with prev / next, the (count, failed)
+    all-reduce, then records exchanged and merged -- one host
+    synchronisation per step, no Python on the data path).
 
     ``dist`` (torch.distributed, initialised) only carries the NCCL unique
     id from rank 0 to the others; ``store`` is this rank's DeviceStore."""
