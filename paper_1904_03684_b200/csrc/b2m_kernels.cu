@@ -93,6 +93,9 @@ constexpr int kUnroll3D = B2M_3D_UNROLL;
 #ifndef B2M_LEAVE_MASK
 #define B2M_LEAVE_MASK 1       // column kernel owner scan: a per-lane leave mask, classified per tile (-50 us at C2)
 #endif
+#ifndef B2M_2D_R45
+#define B2M_2D_R45 1           // column kernel bodies specialised for pc_iterations 4 and 5 too (C5 pc 4: 43.3k -> 45.7k)
+#endif
 #ifndef B2M_TILE_PREFETCH
 #define B2M_TILE_PREFETCH 0    // 1: L1 prefetch of the next tile's first-row columns
 #endif
@@ -294,6 +297,10 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           }
         };
         if (F.U.rounds == 3) run(std::integral_constant<int, 3>{});
+#if B2M_2D_R45
+        else if (!DEP && F.U.rounds == 4) run(std::integral_constant<int, 4>{});
+        else if (!DEP && F.U.rounds == 5) run(std::integral_constant<int, 5>{});
+#endif
         else run(std::integral_constant<int, 0>{});
       } else {
 #pragma unroll 1

@@ -521,7 +521,7 @@ def zinvariant_field(grid, seed, scale=0.7):
     return out[0], out[1]
 
 
-@pytest.mark.parametrize("seed,qom,pc", [(11, -25.0, 3), (12, 1.0, 5), (13, -25.0, 1)])
+@pytest.mark.parametrize("seed,qom,pc", [(11, -25.0, 3), (12, 1.0, 5), (13, -25.0, 1), (14, -25.0, 4)])
 def test_zinvariant_kernel_vs_oracle_and_general(gpu, monkeypatch, seed, qom, pc):
     """A z-invariant field runs the column (2-D-in-3-D) FAST kernel: within
     the contract of the oracle, cells exact, and equal to the general 3-D
