@@ -10,7 +10,8 @@ grouped ncclSend/ncclRecv with prev/next + merge + count all-reduce) through
 NativeSlabWorld, then deposits rho/J/pressure and reduces them across ranks
 (b2m_world_reduce_moments: all-gather + rank-ordered sum).
 MODE "ok", or "nan": rank 1 gets a NaN velocity -> its NumericalFault, and
-every peer an EngineFault, nobody hangs.  Rank r writes OUTDIR/rank{r}.npz
+every peer an EngineFault, nobody hangs; "cap": rank 0 cannot take the
+particles rank 1 sends it -> its AllocError, rank 1's EngineFault.  Rank r writes OUTDIR/rank{r}.npz
 (particles + reduced mesh) or OUTDIR/rank{r}.err."""
 import os
 import sys
@@ -50,7 +51,15 @@ def main():
     p6s = [b.span() for b in batches]
     if mode == "nan" and rank == 1:
         p6s[0][3][5] = np.nan
-    st = DeviceStore(grid, [int(b.count() * 1.5) + 4096 for b in batches], "strict", device=dev)
+    caps = [int(b.count() * 1.5) + 4096 for b in batches]
+    if mode == "cap":
+        # rank 1 hands 64 species-0 particles to rank 0 (y just below its own
+        # slab), and rank 0 has no room for arrivals: its capacity is its count
+        if rank == 1:
+            p6s[0][1][:64] = grid.ly / world - 1e-3
+        else:
+            caps[0] = batches[0].count()
+    st = DeviceStore(grid, caps, "strict", device=dev)
     st.upload_field(gem.gem_field(grid))
     for s, p in enumerate(p6s):
         st.upload(s, p)

@@ -144,6 +144,19 @@ def test_native_world_over_fake_nccl_fault_on_one_rank(gpu):
     assert errs[0].startswith("EngineFault"), (errs, logs)
 
 
+def test_native_world_over_fake_nccl_capacity_overflow_on_one_rank(gpu):
+    """Arrivals a rank cannot hold are caught from the counts round, before
+    the records round: the step's all-reduced verdict carries the failure,
+    so the full rank reports AllocError (the batch capacity is fixed at
+    allocation, particle_batch.hpp:43-46) and its peer EngineFault -- both
+    return, nobody waits in a collective alone."""
+    d, logs = _run(2, 1, "cap", env={"B2M_NCCL_LIB": fake_nccl_lib()})
+    errs = [open(os.path.join(d, f"rank{r}.err")).read() if os.path.exists(
+        os.path.join(d, f"rank{r}.err")) else "" for r in range(2)]
+    assert errs[0].startswith("AllocError") and "capacity" in errs[0], (errs, logs)
+    assert errs[1].startswith("EngineFault"), (errs, logs)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_nccl_world_matches_reference_simulation(gpu, world):
     if _gpus() < world:
