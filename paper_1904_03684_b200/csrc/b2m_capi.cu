@@ -1227,7 +1227,9 @@ b2m_status b2m_slab_config(b2m_ctx* ctx, int rank, int world) {
     // gem_like_field E accelerates electrons every cycle) migrates far more
     // than the physical ~0.2 % per cycle
     S.cap_out = std::max<uint64_t>(std::min<uint64_t>(cap, 1u << 16), cap / 2);
-    if ((st = dalloc(ctx, &S.flags, cap, "migration flags")) != B2M_OK) return st;
+    // the movers and the compaction only test S.flags for null (owner scan
+    // on); leavers are re-derived from y, so no per-particle byte is stored
+    if ((st = dalloc(ctx, &S.flags, 1, "migration marker")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[0], 6 * S.cap_out, "outbox prev")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.out[1], 6 * S.cap_out, "outbox next")) != B2M_OK) return st;
     if ((st = dalloc(ctx, &S.holes, cap, "hole list")) != B2M_OK) return st;

@@ -26,7 +26,7 @@ struct Species {
   uint64_t stride = 0;
   uint64_t count = 0;
   // migration scratch
-  uint8_t* flags = nullptr;
+  uint8_t* flags = nullptr;  // non-null: the owner scan is on (a 1-byte marker, nothing stored)
   unsigned long long* tcnt = nullptr;  // per-tile packed leaver counts (next << 32 | prev)
   unsigned long long* toff = nullptr;  // their exclusive scan
   double* out[2] = {};
