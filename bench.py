@@ -740,6 +740,7 @@ def run_world(args):
     from paper_1904_03684_b200 import _capi, gem
     from paper_1904_03684_b200.engine import B200Engine, DeviceStore
     from paper_1904_03684_b200.mover import Grid, MoverParams
+    from paper_1904_03684_b200.errors import ConfigError
     from paper_1904_03684_b200.partition import DeviceMigration, NativeSlabWorld, SlabWorld
 
     world_env = int(os.environ["WORLD_SIZE"])
@@ -771,6 +772,7 @@ def run_world(args):
     # process group (ranks sharing a GPU with B2M_NCCL_LIB = tests/fake_nccl)
     nw_env = os.environ.get("B2M_NATIVE_WORLD", "1")
     native = nw_env == "force" or (backend == "nccl" and nw_env != "0")
+    native_why = None
     field_of = (lambda g: gem.gem_bench_field(g)) if args.field == "gem+E" \
         else (lambda g: gem.gem_field(g))
 
@@ -789,9 +791,15 @@ def run_world(args):
             store.upload(s, b.span())
             if args.sort:
                 store.sort(s)
+        nonlocal native, native_why
         if native:
-            sw = NativeSlabWorld(grid, store, rank, world, dist, comm=True)
-        else:
+            try:
+                sw = NativeSlabWorld(grid, store, rank, world, dist, comm=True)
+            except ConfigError as e:
+                # raised on EVERY rank together (NativeSlabWorld's NCCL probe
+                # is agreed over dist): the same protocol in Python instead
+                native, native_why = False, str(e)
+        if not native:
             sw = SlabWorld(grid, DeviceMigration(store, rank, world), len(batches), dist, dev)
         sw.set_total()
         # field replication every cycle (runtime.cpp:143 / :221-223): rank 0's
@@ -964,7 +972,9 @@ def run_world(args):
                            "parallelism": f"y-slab x{world}, {backend}"
                                           + (" (ranks share GPUs: functional run)" if shared
                                              else "") + (", native b2m_world_step" if native
-                                                         else ", Python SlabWorld")},
+                                                         else ", Python SlabWorld")
+                                          + (f" (native world unavailable: {native_why})"
+                                             if native_why else "")},
                 "repetitions": reps,
                 "ranks": ranks,
                 "gpu_launches": int(launches),

@@ -357,8 +357,20 @@ class NativeSlabWorld:
             raise ConfigError("NativeSlabWorld: world > 1 needs torch.distributed (dist) to "
                               "share the NCCL unique id")
         if comm:
-            if rank == 0:
-                _capi.check(_capi.lib().b2m_world_id(uid))
+            # every rank probes NCCL (resolved at run time) and the ranks agree
+            # before any of them enters ncclCommInitRank: a rank without NCCL
+            # makes ALL of them raise ConfigError instead of leaving the others
+            # waiting in the communicator setup
+            st = _capi.lib().b2m_world_id(uid)
+            why = "" if st == 0 else (_capi.last_error() or "NCCL unavailable")
+            if dist is not None and world > 1:
+                votes = [None] * world
+                dist.all_gather_object(votes, why)
+                bad = [(r, w) for r, w in enumerate(votes) if w]
+                if bad:
+                    raise ConfigError(f"native world unavailable (rank {bad[0][0]}: {bad[0][1]})")
+            elif why:
+                raise ConfigError(f"native world unavailable: {why}")
             if dist is not None:
                 obj = [bytes(uid)]
                 dist.broadcast_object_list(obj, src=0)

@@ -3,7 +3,8 @@
     python tests/partition_worker.py RANK WORLD PORT OUTDIR CYCLES MODE
 
 MODE: "ok" (plain run), "cfl" (inject a particle jumping two slabs),
-"lose" (the store drops a particle -> count-drift EngineFault).
+"lose" (the store drops a particle -> count-drift EngineFault), "probe"
+(NativeSlabWorld when rank 1 cannot load NCCL -> ConfigError on every rank).
 Rank r writes OUTDIR/rank{r}.npz with its final particles, or OUTDIR/rank{r}.err.
 """
 import os
@@ -29,6 +30,24 @@ def main():
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo")
     grid = Grid.make(8, 8, 8, 6.4, 6.4, 6.4)          # the reference small_cfg
+    if mode == "probe":
+        # NativeSlabWorld's NCCL probe when rank 1 has no NCCL: every rank
+        # must raise ConfigError (none may enter the communicator setup)
+        if rank == 1:
+            os.environ["B2M_NCCL_LIB"] = "/nonexistent/libnccl.so.2"
+        from paper_1904_03684_b200.partition import NativeSlabWorld
+
+        class _NoStore:
+            h, n_species = None, 4
+        try:
+            NativeSlabWorld(grid, _NoStore(), rank, world, dist)
+            msg = "no error"
+        except Exception as e:  # noqa: BLE001
+            msg = f"{type(e).__name__}: {e}"
+        with open(os.path.join(outdir, f"rank{rank}.err"), "w") as fh:
+            fh.write(msg)
+        dist.destroy_process_group()
+        return
     batches = gem.init_gem_slab(grid, 8, rank, world, pinned=False)
     p6s = [b.span() for b in batches]
     if mode == "cfl" and rank == 0:

@@ -116,3 +116,16 @@ def test_slab_world_count_drift_is_detected(built):
     d, logs = _run_world(2, 1, "lose")
     errs = [open(os.path.join(d, f"rank{r}.err")).read() for r in range(2)]
     assert all(e.startswith("EngineFault") and "particle count drifted" in e for e in errs), errs
+
+
+def test_native_world_nccl_probe_is_agreed_by_every_rank(built):
+    """NativeSlabWorld probes NCCL on every rank and the ranks agree (over
+    torch.distributed, gloo here) before any enters ncclCommInitRank: when
+    one rank cannot load NCCL, every rank raises ConfigError -- none is left
+    waiting in the communicator setup.  bench.py then falls back to the
+    Python SlabWorld on all ranks together."""
+    d, logs = _run_world(2, 0, "probe")
+    errs = [open(os.path.join(d, f"rank{r}.err")).read() for r in range(2)]
+    for e in errs:
+        assert e.startswith("ConfigError: native world unavailable (rank "), (errs, logs)
+
