@@ -253,10 +253,45 @@ def cpu_reference_measure(field, steps, warmup, whole_budget_s=0.0):
                       f"{warmup} warm-up + {len(times)} timed cycles"}
 
 
+def reference_simulation_measure(field, cycles=3):
+    """SURVEY §8(d) CPU baseline (i): the reference's own pic::Simulation
+    (runtime.cpp, the path bench.cpp's run_benchmark times) with the cpu
+    engine on the whole C2 state and field, workers = the largest divisor of
+    ny not above the host's threads (runtime.cpp:24-30); MPA/s from the mean
+    per-cycle t_mover (max over workers, bench.cpp:78-81).  None when the
+    reference library was not built."""
+    import oracle
+    if not os.path.exists(oracle.REF_SO):
+        return None
+    threads, model = host_info()
+    grid_t = (NX, NY, NZ, LX, LY, LZ)
+    workers = max(w for w in range(1, min(threads, NY // 2) + 1) if NY % w == 0 and NY // w >= 2)
+    parts, E, B = oracle.ref_init_gem(grid_t, PPC)
+    if field == "gem+E":
+        E, _ = oracle.port_gem_like_field(grid_t)
+    total = sum(len(p[0]) for p in parts)
+    t0 = time.perf_counter()
+    sim = oracle.RefSimulation(grid_t, PPC, workers=workers, engine="cpu", pc=PC, dt=DT,
+                               inject=(parts, E, B))
+    sim.run(cycles)
+    t_mover = sim.mean_mover_s()
+    wall = time.perf_counter() - t0
+    del sim
+    return {"value": total / t_mover / 1e6, "unit": "MPA/s", "workers": workers,
+            "cycles": cycles, "t_mover_s": t_mover, "wall_s": wall, "cpu_model": model,
+            "what": f"pic::Simulation (cpu engine, {workers} workers) on the whole C2 state "
+                    f"({total} particles), field {field}; MPA/s = particles / mean per-cycle "
+                    f"t_mover (max over workers), as bench.cpp's run_benchmark reports"}
+
+
 def run_reference_arm(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
     cpu = cpu_reference_measure(args.field, args.steps, args.warmup, whole_budget_s=240.0)
+    try:
+        sim = reference_simulation_measure(args.field) if args.ref_sim else None
+    except Exception as e:  # noqa: BLE001 - an extra figure; the arm's value stands
+        sim = {"unavailable": f"{type(e).__name__}: {e}"}
     whole = cpu.get("sampled") == cpu["particles_total"]
     line = {
         "impl": "reference", "metric": "MPA/s in mover", "value": cpu["value"], "unit": "MPA/s",
@@ -271,6 +306,7 @@ def run_reference_arm(args):
                             "a bounded sample of the C2 state per step (the whole state would "
                             "not fit the run's time budget); same metric, unit and field")},
         "cpu_baseline": cpu,
+        "reference_simulation": sim,
         "e2e": {"value": cpu["value"], "unit": "MPA/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -1039,6 +1075,8 @@ def parse(argv=None):
     ap.add_argument("--moments", type=int, default=1)
     ap.add_argument("--general-3d", type=int, default=1,
                     help="also time the general 3-D kernel on a z-varying field")
+    ap.add_argument("--ref-sim", type=int, default=1,
+                    help="reference arm: also time the reference's own Simulation (cpu engine)")
     ap.add_argument("--c3", type=int, default=1,
                     help="the C3 leg (BASELINE configs[2]: 512M particles, 128x128x64)")
     ap.add_argument("--strong", type=int, default=1,

@@ -63,6 +63,8 @@ def test_under_torchrun_no_relaunch(monkeypatch):
 def test_reference_arm_only_on_rank_zero(monkeypatch, capsys):
     monkeypatch.setenv("RANK", "1")
     monkeypatch.setattr(bench, "cpu_reference_measure", lambda *a, **k: pytest.fail("rank 1 ran"))
+    monkeypatch.setattr(bench, "reference_simulation_measure",
+                        lambda *a, **k: pytest.fail("rank 1 ran"))
     assert bench.main(["--impl", "reference", "--gpus", "2"]) == 0
     assert capsys.readouterr().out == ""
 
@@ -73,11 +75,14 @@ def test_reference_arm_line(monkeypatch, capsys):
             "ms_per_step": 400.0, "steps": 20, "particles_total": 61046784,
             "sampled": 61046784, "sample": "s"}
     monkeypatch.setattr(bench, "cpu_reference_measure", lambda *a, **k: dict(fake))
+    monkeypatch.setattr(bench, "reference_simulation_measure",
+                        lambda *a, **k: {"value": 60.0, "unit": "MPA/s", "workers": 16})
     assert bench.main(["--impl", "reference", "--gpus", "8"]) == 0
     line = json.loads(capsys.readouterr().out)
     assert line["impl"] == "reference" and line["n_gpus"] == 8 and line["value"] == 80.0
     assert line["cpu_baseline"]["value"] == line["value"]
     assert line["config"]["same_config"] is True  # the whole C2 state was moved
+    assert line["reference_simulation"]["workers"] == 16
     assert line["e2e"] == {"value": 80.0, "unit": "MPA/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
 
