@@ -55,6 +55,36 @@ __device__ __forceinline__ int slab_flag(double y, const SlabLaunch& sl) {
   return own ? 0 : (prv ? 1 : (nxt ? 2 : 3));
 }
 
+// Owner scan, per particle: does the new y stay in this rank's slab (one
+// unsigned compare of the bit pattern; slab_flag's fast path)?
+__device__ __forceinline__ bool stays_in_slab(double y, const SlabLaunch& sl) {
+  const unsigned long long b = dbits(y) & kAbs;
+  return b - dbits(sl.own_lo) < dbits(sl.own_hi) - dbits(sl.own_lo);
+}
+
+// Owner scan, per tile with a leaver: bit j of `leave` marks this lane's
+// row-j particle (its new y in yrow[32 j + lane]); classify them (1 prev,
+// 2 next, 3 CflViolation) and add the warp's counts per direction.
+template <int P>
+__device__ __forceinline__ void classify_leavers(unsigned leave, const double* yrow,
+                                                 const SlabLaunch& sl, FaultWord* fault,
+                                                 int species, unsigned long long base, int lane,
+                                                 unsigned& n_prev, unsigned& n_next) {
+#pragma unroll 1
+  for (int j = 0; j < P; ++j) {
+    int flag = 0;
+    if ((leave >> j) & 1u) {
+      flag = slab_flag(yrow[lane + 32 * j], sl);
+      if (flag == 3) {
+        atomicMin(&fault->cfl, fault_key(species, base + lane + 32 * j));
+        flag = 0;
+      }
+    }
+    n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
+    n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
+  }
+}
+
 // The mover with warp-private TMA pipelines: every warp streams its own
 // tiles of 32*P particles (kWarpStages deep) through its slice of shared
 // memory with its own mbarriers -- no block-wide barrier anywhere.  One 2-D
@@ -183,6 +213,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       CellCache cc;
       cc.cell = -1;
       uint8_t* flags = S.flags[s];
+      unsigned leave = 0;  // bit j: this lane's row-j particle left the slab
 #pragma unroll 1
       for (int j = 0; j < P; ++j) {
         const int p = lane + 32 * j;
@@ -192,21 +223,14 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                 ? strict_tile_thread_p1<WT, 3, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc)
                 : strict_tile_thread_p1<WT, 0, DIM>(F.dg, F.fg, F.nodes, sp, buf[st], p, cnt, cc);
         if (bad) atomicMin(&fault->numerical, fault_key(sp.species, sp.base + off + p));
-        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
-        // warp ballot; the compaction re-derives each leaver from its y
-        if (flags) {
-          int flag = 0;
-          if (p < cnt && !bad) {
-            flag = slab_flag(buf[st][1][p], sl);
-            if (flag == 3) {
-              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
-              flag = 0;
-            }
-          }
-          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
-          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
-        }
+        // owner scan (partition_outgoing, runtime.cpp:46-62): the stay test per
+        // particle, the tile's leavers classified after its last row; the
+        // compaction re-derives each leaver from its y
+        if (flags && (p < cnt) & !bad & !stays_in_slab(buf[st][1][p], sl)) leave |= 1u << j;
       }
+      if (flags && __any_sync(0xffffffffu, leave))
+        classify_leavers<P>(leave, buf[st][1], sl, fault, sp.species, sp.base + off, lane, n_prev,
+                            n_next);
     } else if (B2M_ABL_STREAM_ONLY) {
       // ablation: the tile pipeline without the mover arithmetic
       if (lane < cnt) buf[st][0][lane] += 0.0;
@@ -238,11 +262,9 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
         // owner scan (partition_outgoing, runtime.cpp:46-62)
         if (flags) {
           if (B2M_LEAVE_MASK && !DEP) {
-            // per particle only the one-compare "stays in my slab" test; the
-            // tile's leavers are classified after its last row (rare)
-            const unsigned long long b = dbits(y1) & kAbs;
-            const bool stay = b - dbits(sl.own_lo) < dbits(sl.own_hi) - dbits(sl.own_lo);
-            if ((p < cnt) & !bad & !stay) leave |= 1u << j;
+            // per particle only the stay test; the tile's leavers are
+            // classified after its last row (rare)
+            if ((p < cnt) & !bad & !stays_in_slab(y1, sl)) leave |= 1u << j;
           } else {
             // leavers per row by warp ballot; the compaction re-derives each
             // leaver from its y
@@ -330,21 +352,9 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           after(j, bad, y1);
         }
       }
-      if (B2M_LEAVE_MASK && !DEP && flags && __any_sync(0xffffffffu, leave)) {
-#pragma unroll 1
-        for (int j = 0; j < P; ++j) {
-          int flag = 0;
-          if ((leave >> j) & 1u) {
-            flag = slab_flag(buf[st][1][lane + 32 * j], sl);
-            if (flag == 3) {
-              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + lane + 32 * j));
-              flag = 0;
-            }
-          }
-          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
-          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
-        }
-      }
+      if (B2M_LEAVE_MASK && !DEP && flags && __any_sync(0xffffffffu, leave))
+        classify_leavers<P>(leave, buf[st][1], sl, fault, sp.species, sp.base + off, lane, n_prev,
+                            n_next);
     } else if (B2M_FAST_V == 2) {
       // FAST v2 (b2m_tile.cuh): fractions relative to the lane's cached cell
       FastCell C;
