@@ -120,9 +120,6 @@ constexpr int kUnroll3D = B2M_3D_UNROLL;
 #ifndef B2M_TILE_RUN_3D
 #define B2M_TILE_RUN_3D 1      // 3-D kernels (runs of 2 and 4 measured 1 % slower)
 #endif
-#ifndef B2M_LEAVE_MASK
-#define B2M_LEAVE_MASK 1       // column kernel owner scan: a per-lane leave mask, classified per tile (-50 us at C2)
-#endif
 #ifndef B2M_2D_R45
 #define B2M_2D_R45 1           // column kernel bodies specialised for pc_iterations 4 and 5 too (C5 pc 4: 43.3k -> 45.7k)
 #endif
@@ -239,7 +236,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       FastCol C;
       fast_col_reset(C);
       uint8_t* flags = S.flags[s];
-      unsigned leave = 0;  // B2M_LEAVE_MASK: bit j = this lane's row-j particle left the slab
+      unsigned leave = 0;  // bit j: this lane's row-j particle left the slab
       const double* cols = reinterpret_cast<const double*>(sp.cells);
       // per moved particle: fault record, fused deposit, migration flag
       auto after = [&](int j, unsigned bad, double y1) {
@@ -259,27 +256,10 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                         buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
           }
         }
-        // owner scan (partition_outgoing, runtime.cpp:46-62)
-        if (flags) {
-          if (B2M_LEAVE_MASK && !DEP) {
-            // per particle only the stay test; the tile's leavers are
-            // classified after its last row (rare)
-            if ((p < cnt) & !bad & !stays_in_slab(y1, sl)) leave |= 1u << j;
-          } else {
-            // leavers per row by warp ballot; the compaction re-derives each
-            // leaver from its y
-            int flag = 0;
-            if (p < cnt && !bad) {
-              flag = slab_flag(y1, sl);
-              if (flag == 3) {
-                atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
-                flag = 0;
-              }
-            }
-            n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
-            n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
-          }
-        }
+        // owner scan (partition_outgoing, runtime.cpp:46-62): the stay test per
+        // particle, the tile's leavers classified after its last row (the fused
+        // launch never migrates)
+        if (!DEP && flags && (p < cnt) & !bad & !stays_in_slab(y1, sl)) leave |= 1u << j;
       };
       if (B2M_2D_PAIR && (P % 2) == 0) {
         // two particles per lane at a time (ILP 2, b2m_tile.cuh fast_pair_2d)
@@ -352,7 +332,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
           after(j, bad, y1);
         }
       }
-      if (B2M_LEAVE_MASK && !DEP && flags && __any_sync(0xffffffffu, leave))
+      if (!DEP && flags && __any_sync(0xffffffffu, leave))
         classify_leavers<P>(leave, buf[st][1], sl, fault, sp.species, sp.base + off, lane, n_prev,
                             n_next);
     } else if (B2M_FAST_V == 2) {
@@ -360,6 +340,7 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
       FastCell C;
       fast_cell_reset(C);
       uint8_t* flags = S.flags[s];
+      unsigned leave = 0;  // bit j: this lane's row-j particle left the slab
       const double2* cells = sp.cells;
       auto run3 = [&](auto rounds_tag) {
       constexpr int R = decltype(rounds_tag)::value;
@@ -383,25 +364,18 @@ __global__ void __launch_bounds__(kWarpThreads, DIM == 2 ? B2M_2D_MINBLOCKS : B2
                         buf[st][1][p], buf[st][2][p], p < cnt && !bad, lane);
           }
         }
-        // owner scan (partition_outgoing, runtime.cpp:46-62): leavers per row by
-        // warp ballot; the compaction re-derives each leaver from its y
-        if (flags) {
-          int flag = 0;
-          if (p < cnt && !bad) {
-            flag = slab_flag(buf[st][1][p], sl);
-            if (flag == 3) {
-              atomicMin(&fault->cfl, fault_key(sp.species, sp.base + off + p));
-              flag = 0;
-            }
-          }
-          n_prev += __popc(__ballot_sync(0xffffffffu, flag == 1));
-          n_next += __popc(__ballot_sync(0xffffffffu, flag == 2));
-        }
+        // owner scan (partition_outgoing, runtime.cpp:46-62): the stay test per
+        // particle, the tile's leavers classified after its last row
+        if (!DEP && flags && (p < cnt) & !bad & !stays_in_slab(buf[st][1][p], sl))
+          leave |= 1u << j;
       }
       };
       // pc_iterations dispatched once per tile
       if (F.U.rounds == 3) run3(std::integral_constant<int, 3>{});
       else run3(std::integral_constant<int, 0>{});
+      if (!DEP && flags && __any_sync(0xffffffffu, leave))
+        classify_leavers<P>(leave, buf[st][1], sl, fault, sp.species, sp.base + off, lane, n_prev,
+                            n_next);
     } else {
       const FastConst kc = make_const(F.fg, sp);
       // particles lane + 32*j, j < P, one after the other, sharing the
@@ -856,10 +830,13 @@ bool launch_move_fast(const FastGrid& g, const SpeciesLaunch* sp, int n_spans, F
   F.fg = g;
   F.zvar = zvar;
   if (mom) {
+    // the fused mover + deposit (b2m_move_deposit_all) never migrates: its
+    // kernels carry no owner scan
+    if (flags) return false;
     for (int m = 0; m < 4; ++m) F.mom[m] = mom[m];
-    if (zvar && !launch_warp_tiles<false, 2, true>(F, sp, n_spans, fault, st, sl, flags, tcnt))
+    if (zvar && !launch_warp_tiles<false, 2, true>(F, sp, n_spans, fault, st, sl, nullptr, nullptr))
       return false;
-    return launch_warp_tiles<false, 3, true>(F, sp, n_spans, fault, st, sl, flags, tcnt);
+    return launch_warp_tiles<false, 3, true>(F, sp, n_spans, fault, st, sl, nullptr, nullptr);
   }
   // both FAST kernels; the one the field's z-invariance flag rules out exits
   // at its first instruction (no host round trip to decide)

@@ -196,25 +196,31 @@ def test_world_step_per_rank_failure_runs_the_protocol(gpu):
     st.close()
 
 
-def test_loopback_four_ranks_equal_one_context_after_many_steps(gpu):
+@pytest.mark.parametrize("mode,field", [("strict", "gem"), ("fast", "gem+E"),
+                                        ("fast", "zvarying")])
+def test_loopback_four_ranks_equal_one_context_after_many_steps(gpu, mode, field):
     """1.2M GEM particles split over 4 slab ranks (loopback protocol) for 8
-    STRICT steps: every particle is on its owner rank, and the union is the
-    bitwise multiset of the same particles moved 8 times in one context (the
-    mover is per-particle, migration only relocates)."""
+    steps: every particle is on its owner rank, and the union is the bitwise
+    multiset of the same particles moved 8 times in one context (the mover is
+    per-particle, migration only relocates) -- STRICT, FAST on the
+    z-invariant bench field (the column kernel's owner scan) and FAST on a
+    z-varying field (the general kernel's)."""
     grid_t = (32, 32, 16, 12.8, 6.4, 3.2)
     g = Grid.make(*grid_t)
     world = 4
+    fld = (gem.gem_field(g) if field == "gem" else
+           gem.gem_bench_field(g, z_varying=(field == "zvarying")))
     full = gem.init_gem_species(g, 72, pinned=False)
     mps = [MoverParams.make(0.1, b.qom, 3) for b in full]
-    ref = DeviceStore(g, [b.count() for b in full], "strict")
-    ref.upload_field(gem.gem_field(g))
+    ref = DeviceStore(g, [b.count() for b in full], mode)
+    ref.upload_field(fld)
     for s, b in enumerate(full):
         ref.upload(s, b.span())
     stores = []
     for r in range(world):
         part = gem.init_gem_slab(g, 72, r, world, pinned=False)
-        st = DeviceStore(g, [b.count() * 2 + 4096 for b in part], "strict")
-        st.upload_field(gem.gem_field(g))
+        st = DeviceStore(g, [b.count() * 2 + 4096 for b in part], mode)
+        st.upload_field(fld)
         for s, b in enumerate(part):
             st.upload(s, b.span())
         stores.append(st)
