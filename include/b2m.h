@@ -309,6 +309,10 @@ b2m_status b2m_inbox_append(b2m_ctx* ctx, int s, const double* d_recs, uint64_t 
  * b2m_event_elapsed_ms(13, 14) / (14, 15) split its device time. */
 #define B2M_WORLD_ID_BYTES 128
 b2m_status b2m_world_id(void* id);
+/* B2M_OK when NCCL resolved in this process (B2M_NCCL_LIB, the process's own
+ * libnccl, or libnccl.so.2), else ConfigError with the reason: what every
+ * rank checks -- and the ranks agree on -- before b2m_world_init. */
+b2m_status b2m_world_nccl_available(void);
 b2m_status b2m_world_init(b2m_ctx* ctx, const void* id, int rank, int world);
 b2m_status b2m_world_set_total(b2m_ctx* ctx, uint64_t* total);
 /* Replicate the root rank's device field on every rank (ncclBroadcast of E

@@ -105,6 +105,7 @@ SIGNATURES = {
     "b2m_outbox": (_st, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_u64)]),
     "b2m_inbox_append": (_st, [C.c_void_p, C.c_int, C.c_void_p, _u64]),
     "b2m_world_id": (_st, [C.c_void_p]),
+    "b2m_world_nccl_available": (_st, []),
     "b2m_world_init": (_st, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "b2m_world_set_total": (_st, [C.c_void_p, C.POINTER(_u64)]),
     "b2m_world_broadcast_field": (_st, [C.c_void_p, C.c_int]),

@@ -281,6 +281,11 @@ b2m_status world_alloc(b2m_ctx* ctx, const std::vector<uint64_t>& stage_cap) {
 
 }  // namespace
 
+b2m_status b2m_world_nccl_available(void) {
+  if (!nccl().ok) return fail(B2M_CONFIG_ERROR, "NCCL unavailable: " + nccl().why);
+  return B2M_OK;
+}
+
 b2m_status b2m_world_id(void* id) {
   if (!id) return fail(B2M_INVALID_ARGUMENT, "null id buffer");
   if (!nccl().ok) return fail(B2M_CONFIG_ERROR, "NCCL unavailable: " + nccl().why);

@@ -361,7 +361,8 @@ class NativeSlabWorld:
             # before any of them enters ncclCommInitRank: a rank without NCCL
             # makes ALL of them raise ConfigError instead of leaving the others
             # waiting in the communicator setup
-            st = _capi.lib().b2m_world_id(uid)
+            st = (_capi.lib().b2m_world_id(uid) if rank == 0
+                  else _capi.lib().b2m_world_nccl_available())
             why = "" if st == 0 else (_capi.last_error() or "NCCL unavailable")
             if dist is not None and world > 1:
                 votes = [None] * world
